@@ -1,0 +1,249 @@
+"""CPU oracle for the extremum-graph hot path -- TEST INFRASTRUCTURE ONLY.
+
+Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s
+``cpu_baseline`` / ``--impl reference`` legs may import this package.  The
+product path (``paper_2303_02724_b200``) never imports it and shares no code
+with it; see the header of ``oracle/eg_oracle.c`` for what each step follows
+in PAPER.md.
+
+This module is a thin ctypes/numpy wrapper around ``liboracle`` (plain C,
+single thread, built with ``gcc -O2`` by :func:`build`).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+from dataclasses import dataclass
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "eg_oracle.c")
+_LIB = os.path.join(_HERE, "libeg_oracle.so")
+
+OK, ERR_INVALID, ERR_NAN, ERR_OOM = 0, 1, 2, 3
+
+
+def build(force: bool = False) -> str:
+    """Compile the oracle (gcc -O2, no OpenMP: single-threaded by construction)."""
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        subprocess.check_call(["gcc", "-O2", "-std=c11", "-shared", "-fPIC", "-o", _LIB, _SRC, "-lm"])
+    return _LIB
+
+
+class _Result(C.Structure):
+    _fields_ = [
+        ("n", C.c_int64),
+        ("ptr", C.POINTER(C.c_int64)),
+        ("label", C.POINTER(C.c_int64)),
+        ("beta", C.POINTER(C.c_int32)),
+        ("n_max", C.c_int64),
+        ("maxima", C.POINTER(C.c_int64)),
+        ("n_saddle", C.c_int64),
+        ("saddles", C.POINTER(C.c_int64)),
+        ("saddle_beta", C.POINTER(C.c_int32)),
+        ("n_arc", C.c_int64),
+        ("arc_s", C.POINTER(C.c_int64)),
+        ("arc_m", C.POINTER(C.c_int64)),
+        ("arc_mult", C.POINTER(C.c_int32)),
+        ("n_raw", C.c_int64),
+        ("raw_s", C.POINTER(C.c_int64)),
+        ("raw_rep", C.POINTER(C.c_int64)),
+        ("raw_m", C.POINTER(C.c_int64)),
+    ]
+
+
+_lib = None
+
+
+def _L():
+    global _lib
+    if _lib is None:
+        _lib = C.CDLL(build())
+        i64p, i32p, f32p = C.POINTER(C.c_int64), C.POINTER(C.c_int32), C.POINTER(C.c_float)
+        _lib.ego_grid.argtypes = [C.c_int, i64p, f32p, C.POINTER(_Result)]
+        _lib.ego_csr.argtypes = [C.c_int64, i64p, i32p, f32p, C.POINTER(_Result)]
+        _lib.ego_free.argtypes = [C.POINTER(_Result)]
+        _lib.ego_grid_adjacent.argtypes = [C.c_int, i64p, i64p]
+        _lib.ego_grid_link.argtypes = [C.c_int, i64p, C.c_int64, i64p]
+        _lib.ego_grid_link.restype = C.c_int64
+        _lib.ego_grid_vertex.argtypes = [C.c_int, i64p, f32p, C.c_int64, i64p, i32p, i64p, C.c_int32]
+        _lib.ego_csr_vertex.argtypes = [C.c_int64, i64p, i32p, f32p, C.c_int64, i64p, i32p, i64p, C.c_int32]
+        _lib.ego_grid_walk.argtypes = [C.c_int, i64p, f32p, C.c_int64, i64p]
+        _lib.ego_grid_walk.restype = C.c_int64
+        _lib.ego_csr_walk.argtypes = [C.c_int64, i64p, i32p, f32p, C.c_int64, i64p]
+        _lib.ego_csr_walk.restype = C.c_int64
+        _lib.ego_grid_euler.argtypes = [C.c_int, i64p, f32p, i64p]
+        _lib.ego_csr_euler.argtypes = [C.c_int64, i64p, i32p, f32p, i64p]
+        _lib.ego_grid_link_stats.argtypes = [C.c_int, i64p, C.c_int64, i64p, i64p, i64p]
+    return _lib
+
+
+def _p(a, ct):
+    return a.ctypes.data_as(C.POINTER(ct))
+
+
+@dataclass
+class Graph:
+    """Oracle output (O9): everything as int64 numpy arrays, ids are global."""
+    ptr: np.ndarray
+    label: np.ndarray
+    beta: np.ndarray
+    maxima: np.ndarray
+    saddles: np.ndarray
+    saddle_beta: np.ndarray
+    arc_s: np.ndarray
+    arc_m: np.ndarray
+    arc_mult: np.ndarray
+    raw_s: np.ndarray
+    raw_rep: np.ndarray
+    raw_m: np.ndarray
+
+    @property
+    def arcs(self):
+        return np.stack([self.arc_s, self.arc_m, self.arc_mult.astype(np.int64)], axis=1)
+
+
+class OracleError(RuntimeError):
+    pass
+
+
+def _take(res: _Result) -> Graph:
+    def arr(p, n, dt):
+        if n == 0:
+            return np.zeros(0, dt)
+        return np.ctypeslib.as_array(p, shape=(n,)).astype(dt, copy=True)
+
+    n = res.n
+    g = Graph(
+        ptr=arr(res.ptr, n, np.int64), label=arr(res.label, n, np.int64), beta=arr(res.beta, n, np.int32),
+        maxima=arr(res.maxima, res.n_max, np.int64), saddles=arr(res.saddles, res.n_saddle, np.int64),
+        saddle_beta=arr(res.saddle_beta, res.n_saddle, np.int32),
+        arc_s=arr(res.arc_s, res.n_arc, np.int64), arc_m=arr(res.arc_m, res.n_arc, np.int64),
+        arc_mult=arr(res.arc_mult, res.n_arc, np.int32),
+        raw_s=arr(res.raw_s, res.n_raw, np.int64), raw_rep=arr(res.raw_rep, res.n_raw, np.int64),
+        raw_m=arr(res.raw_m, res.n_raw, np.int64))
+    _L().ego_free(C.byref(res))
+    return g
+
+
+def _dims_arr(dims):
+    return np.ascontiguousarray(np.asarray(dims, dtype=np.int64))
+
+
+def grid(f: np.ndarray, dims) -> Graph:
+    """Extremum graph of a float32 field on a Freudenthal grid; ``dims`` is
+    fastest axis first and ``f`` is the flat row-major array (axis 0 fastest)."""
+    f = np.ascontiguousarray(np.asarray(f, dtype=np.float32).reshape(-1))
+    d = _dims_arr(dims)
+    res = _Result()
+    rc = _L().ego_grid(len(d), _p(d, C.c_int64), _p(f, C.c_float), C.byref(res))
+    if rc != OK:
+        raise OracleError(f"ego_grid failed: {rc}")
+    return _take(res)
+
+
+def csr(f: np.ndarray, row_ptr: np.ndarray, col_idx: np.ndarray) -> Graph:
+    f = np.ascontiguousarray(f, dtype=np.float32)
+    rp = np.ascontiguousarray(row_ptr, dtype=np.int64)
+    ci = np.ascontiguousarray(col_idx, dtype=np.int32)
+    res = _Result()
+    rc = _L().ego_csr(len(f), _p(rp, C.c_int64), _p(ci, C.c_int32), _p(f, C.c_float), C.byref(res))
+    if rc != OK:
+        raise OracleError(f"ego_csr failed: {rc}")
+    return _take(res)
+
+
+def grid_adjacent(p, q) -> bool:
+    p = _dims_arr(p)
+    q = _dims_arr(q)
+    if len(p) != len(q):
+        raise ValueError("dimension mismatch")
+    return bool(_L().ego_grid_adjacent(len(p), _p(p, C.c_int64), _p(q, C.c_int64)))
+
+
+def grid_link(dims, v: int) -> np.ndarray:
+    d = _dims_arr(dims)
+    out = np.zeros(3 ** len(d), np.int64)
+    n = _L().ego_grid_link(len(d), _p(d, C.c_int64), int(v), _p(out, C.c_int64))
+    if n < 0:
+        raise OracleError("bad vertex")
+    return out[:n].copy()
+
+
+def grid_link_stats(dims, v: int):
+    """(|Lk(v)|, #link edges, chi of the link's clique complex)."""
+    d = _dims_arr(dims)
+    a, b, c = C.c_int64(), C.c_int64(), C.c_int64()
+    rc = _L().ego_grid_link_stats(len(d), _p(d, C.c_int64), int(v), C.byref(a), C.byref(b), C.byref(c))
+    if rc != OK:
+        raise OracleError("bad vertex")
+    return a.value, b.value, c.value
+
+
+def grid_vertex(f, dims, v: int):
+    """(ptr, beta0+, reps) of one vertex (O3..O5)."""
+    f = np.ascontiguousarray(np.asarray(f, dtype=np.float32).reshape(-1))
+    d = _dims_arr(dims)
+    ptr, beta = C.c_int64(), C.c_int32()
+    reps = np.zeros(3 ** len(d), np.int64)
+    rc = _L().ego_grid_vertex(len(d), _p(d, C.c_int64), _p(f, C.c_float), int(v), C.byref(ptr), C.byref(beta),
+                              _p(reps, C.c_int64), len(reps))
+    if rc != OK:
+        raise OracleError("bad vertex")
+    return ptr.value, beta.value, reps[:beta.value].copy()
+
+
+def csr_vertex(f, row_ptr, col_idx, v: int):
+    f = np.ascontiguousarray(f, dtype=np.float32)
+    rp = np.ascontiguousarray(row_ptr, dtype=np.int64)
+    ci = np.ascontiguousarray(col_idx, dtype=np.int32)
+    ptr, beta = C.c_int64(), C.c_int32()
+    deg = int(rp[v + 1] - rp[v])
+    reps = np.zeros(max(deg, 1), np.int64)
+    rc = _L().ego_csr_vertex(len(f), _p(rp, C.c_int64), _p(ci, C.c_int32), _p(f, C.c_float), int(v),
+                             C.byref(ptr), C.byref(beta), _p(reps, C.c_int64), len(reps))
+    if rc != OK:
+        raise OracleError("bad vertex")
+    return ptr.value, beta.value, reps[:beta.value].copy()
+
+
+def grid_walk(f, dims, v: int):
+    """Alg. 2 walk from v: (maximum reached, number of steps)."""
+    f = np.ascontiguousarray(np.asarray(f, dtype=np.float32).reshape(-1))
+    d = _dims_arr(dims)
+    steps = C.c_int64()
+    m = _L().ego_grid_walk(len(d), _p(d, C.c_int64), _p(f, C.c_float), int(v), C.byref(steps))
+    return m, steps.value
+
+
+def csr_walk(f, row_ptr, col_idx, v: int):
+    f = np.ascontiguousarray(f, dtype=np.float32)
+    rp = np.ascontiguousarray(row_ptr, dtype=np.int64)
+    ci = np.ascontiguousarray(col_idx, dtype=np.int32)
+    steps = C.c_int64()
+    m = _L().ego_csr_walk(len(f), _p(rp, C.c_int64), _p(ci, C.c_int32), _p(f, C.c_float), int(v), C.byref(steps))
+    return m, steps.value
+
+
+def grid_euler(f, dims) -> int:
+    """sum_v (1 - chi(Lk+(v))) over the grid."""
+    f = np.ascontiguousarray(np.asarray(f, dtype=np.float32).reshape(-1))
+    d = _dims_arr(dims)
+    s = C.c_int64()
+    rc = _L().ego_grid_euler(len(d), _p(d, C.c_int64), _p(f, C.c_float), C.byref(s))
+    if rc != OK:
+        raise OracleError("euler failed")
+    return s.value
+
+
+def csr_euler(f, row_ptr, col_idx) -> int:
+    f = np.ascontiguousarray(f, dtype=np.float32)
+    rp = np.ascontiguousarray(row_ptr, dtype=np.int64)
+    ci = np.ascontiguousarray(col_idx, dtype=np.int32)
+    s = C.c_int64()
+    rc = _L().ego_csr_euler(len(f), _p(rp, C.c_int64), _p(ci, C.c_int32), _p(f, C.c_float), C.byref(s))
+    if rc != OK:
+        raise OracleError("euler failed")
+    return s.value
