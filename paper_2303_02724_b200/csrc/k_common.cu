@@ -1,0 +1,180 @@
+// Shared device passes: pointer jumping (S2), stable bitmap compaction of
+// maxima / saddles (S3 node lists), scans and arc emission (S4).
+#include <cub/cub.cuh>
+#include <thrust/iterator/counting_iterator.h>
+#include <thrust/iterator/transform_iterator.h>
+
+#include "eg_impl.h"
+
+namespace eg {
+
+static inline unsigned blocks_for(int64_t n, int bs) { return unsigned((n + bs - 1) / bs); }
+
+// ----------------------------------------------------------- S2 jumping
+// ptr <- ptr[ptr] in place.  Concurrent updates are benign: every value ever
+// written is a vertex further along the same ascending path, so any
+// interleaving converges to the path's end (the maximum Alg. 2 reaches,
+// P:205-208).  Targets outside [v0, v0 + n) are terminal (remote vertices).
+__global__ void __launch_bounds__(256) k_jump(int32_t *ptr, int64_t n, int64_t v0, int *changed, int round) {
+    if (round > 0 && *(volatile int *)&changed[round - 1] == 0) return;   // converged earlier
+    const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    bool ch = false;
+    if (i < n) {
+        const int32_t p = ptr[i];
+        const int64_t pi = int64_t(p) - v0;
+        if (pi >= 0 && pi < n) {
+            const int32_t pp = ptr[pi];
+            if (pp != p) {
+                ptr[i] = pp;
+                ch = true;
+            }
+        }
+    }
+    if (__any_sync(0xffffffffu, ch) && (threadIdx.x & 31) == 0) atomicOr(&changed[round], 1);
+}
+
+cudaError_t launch_jump_round(int32_t *ptr, int64_t n, int64_t v0, int *changed, int round, cudaStream_t st) {
+    if (n <= 0) return cudaSuccess;
+    k_jump<<<blocks_for(n, 256), 256, 0, st>>>(ptr, n, v0, changed, round);
+    return cudaGetLastError();
+}
+
+// ------------------------------------------------------ bitmap compaction
+// Stable: ids come out ascending.  Block b owns words [256 b, 256 b + 256).
+constexpr int kCompactBS = 256;
+
+__global__ void __launch_bounds__(kCompactBS) k_count_bits(const uint32_t *__restrict__ bits, int64_t words,
+                                                           int32_t *chunk_cnt) {
+    using BR = cub::BlockReduce<int, kCompactBS>;
+    __shared__ typename BR::TempStorage tmp;
+    const int64_t w = int64_t(blockIdx.x) * kCompactBS + threadIdx.x;
+    int c = w < words ? __popc(bits[w]) : 0;
+    int tot = BR(tmp).Sum(c);
+    if (threadIdx.x == 0) chunk_cnt[blockIdx.x] = tot;
+}
+
+__global__ void __launch_bounds__(kCompactBS) k_emit_bits(const uint32_t *__restrict__ bits, int64_t words, int64_t n,
+                                                          int64_t v0, const int64_t *__restrict__ chunk_off,
+                                                          int32_t *out32, int64_t *out64) {
+    using BS = cub::BlockScan<int, kCompactBS>;
+    __shared__ typename BS::TempStorage tmp;
+    const int64_t w = int64_t(blockIdx.x) * kCompactBS + threadIdx.x;
+    uint32_t x = w < words ? bits[w] : 0u;
+    if (w == words - 1 && (n & 31)) x &= (1u << (n & 31)) - 1u;   // tail
+    int pre;
+    BS(tmp).ExclusiveSum(__popc(x), pre);
+    int64_t o = chunk_off[blockIdx.x] + pre;
+    while (x) {
+        const int b = __ffs(x) - 1;
+        x &= x - 1;
+        const int64_t id = v0 + w * 32 + b;
+        if (out32) out32[o] = int32_t(id);
+        if (out64) out64[o] = id;
+        ++o;
+    }
+}
+
+struct PadI32 {
+    const int32_t *in;
+    int64_t n;
+    __host__ __device__ int64_t operator()(int64_t i) const { return i < n ? int64_t(in[i]) : 0; }
+};
+
+using PadIt = thrust::transform_iterator<PadI32, thrust::counting_iterator<int64_t>, int64_t>;
+
+size_t scan_scratch_bytes(int64_t n) {
+    size_t bytes = 0;
+    PadIt it(thrust::counting_iterator<int64_t>(0), PadI32{nullptr, n});
+    cub::DeviceScan::ExclusiveSum(nullptr, bytes, it, (int64_t *)nullptr, n + 1);
+    return bytes;
+}
+
+cudaError_t launch_scan_i32(const int32_t *in, int64_t *out, int64_t n, void *scratch, size_t scratch_bytes,
+                            cudaStream_t st) {
+    PadIt it(thrust::counting_iterator<int64_t>(0), PadI32{in, n});
+    return cub::DeviceScan::ExclusiveSum(scratch, scratch_bytes, it, out, n + 1, st);
+}
+
+size_t compact_scratch_bytes(int64_t n) {
+    const int64_t words = (n + 31) / 32;
+    const int64_t chunks = (words + kCompactBS - 1) / kCompactBS;
+    size_t b = scan_scratch_bytes(chunks);
+    // layout: [chunk_cnt int32 x chunks][chunk_off int64 x (chunks + 1)][cub scratch]
+    return size_t(chunks) * 4 + 16 + size_t(chunks + 1) * 8 + 16 + b + 256;
+}
+
+cudaError_t launch_compact_bits(const uint32_t *bits, int64_t n, int64_t v0, void *scratch, int32_t *out32,
+                                int64_t *out64, int64_t *d_count, cudaStream_t st) {
+    const int64_t words = (n + 31) / 32;
+    const int64_t chunks = (words + kCompactBS - 1) / kCompactBS;
+    if (n <= 0) return cudaMemsetAsync(d_count, 0, sizeof(int64_t), st);
+    char *p = static_cast<char *>(scratch);
+    int32_t *cnt = reinterpret_cast<int32_t *>(p);
+    p += (size_t(chunks) * 4 + 15) / 16 * 16 + 16;
+    int64_t *off = reinterpret_cast<int64_t *>(p);
+    p += (size_t(chunks + 1) * 8 + 15) / 16 * 16 + 16;
+    const size_t sb = scan_scratch_bytes(chunks);
+    k_count_bits<<<unsigned(chunks), kCompactBS, 0, st>>>(bits, words, cnt);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    // the tail word may carry junk bits above n only if the producer set them;
+    // producers only set bits of active lanes, so counts are exact.
+    e = launch_scan_i32(cnt, off, chunks, p, sb, st);
+    if (e != cudaSuccess) return e;
+    k_emit_bits<<<unsigned(chunks), kCompactBS, 0, st>>>(bits, words, n, v0, off, out32, out64);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    return cudaMemcpyAsync(d_count, off + chunks, sizeof(int64_t), cudaMemcpyDeviceToDevice, st);
+}
+
+// ------------------------------------------------------------ arc emission
+__global__ void k_emit_arcs(const int32_t *__restrict__ saddles, int64_t n_sad, const int64_t *__restrict__ slot_off,
+                            const int64_t *__restrict__ arc_off, const int32_t *__restrict__ tmp_m,
+                            const int32_t *__restrict__ tmp_mult, const int32_t *__restrict__ n_unique,
+                            int64_t *arc_s, int64_t *arc_m, int32_t *arc_mult) {
+    const int64_t j = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (j >= n_sad) return;
+    const int64_t so = slot_off[j], ao = arc_off[j];
+    const int u = n_unique[j];
+    const int64_t s = saddles[j];
+    for (int k = 0; k < u; ++k) {
+        arc_s[ao + k] = s;
+        arc_m[ao + k] = tmp_m[so + k];
+        arc_mult[ao + k] = tmp_mult[so + k];
+    }
+}
+
+cudaError_t launch_emit_arcs(const int32_t *saddles, int64_t n_sad, const int64_t *slot_off, const int64_t *arc_off,
+                             const int32_t *tmp_m, const int32_t *tmp_mult, const int32_t *n_unique,
+                             int64_t *arc_s, int64_t *arc_m, int32_t *arc_mult, cudaStream_t st) {
+    if (n_sad <= 0) return cudaSuccess;
+    k_emit_arcs<<<blocks_for(n_sad, 256), 256, 0, st>>>(saddles, n_sad, slot_off, arc_off, tmp_m, tmp_mult, n_unique,
+                                                        arc_s, arc_m, arc_mult);
+    return cudaGetLastError();
+}
+
+__global__ void k_i32_to_i64(const int32_t *__restrict__ in, int64_t *out, int64_t n) {
+    const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i < n) out[i] = in[i];
+}
+
+cudaError_t launch_i32_to_i64(const int32_t *in, int64_t *out, int64_t n, cudaStream_t st) {
+    if (n <= 0) return cudaSuccess;
+    k_i32_to_i64<<<blocks_for(n, 256), 256, 0, st>>>(in, out, n);
+    return cudaGetLastError();
+}
+
+__global__ void k_nan_scan(const float *__restrict__ f, int64_t n, int *flag) {
+    bool bad = false;
+    for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
+        bad |= (f[i] != f[i]);
+    if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(flag, 1);
+}
+
+cudaError_t launch_nan_scan(const float *f, int64_t n, int *flag, cudaStream_t st) {
+    if (n <= 0) return cudaSuccess;
+    k_nan_scan<<<148 * 8, 256, 0, st>>>(f, n, flag);
+    return cudaGetLastError();
+}
+
+}  // namespace eg

@@ -1,0 +1,198 @@
+"""GPU parity against the CPU oracle, element by element, through the C ABI.
+
+Bit-exact on every output (labels, maxima, saddles + beta0+, deduplicated and
+raw arcs, gradients): the method has no floating-point arithmetic, only
+comparisons (reading L16), so the tolerance is zero.  Small / ragged sizes
+that still span several tiles, every grid dimension 1..6, tie-heavy and
+signed-zero fields, the degenerate cases, and both the tiled 3-D path and the
+generic n-D kernels.
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+
+import eg_inputs as G
+import oracle as O
+from _parity import assert_graph_equal, first_diff
+
+pytestmark = pytest.mark.gpu
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden", "tiny_examples.json")
+PATHS = [0, "generic"]
+
+
+@pytest.fixture(scope="module")
+def eg():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    import paper_2303_02724_b200 as eg
+    return eg
+
+
+@pytest.fixture(scope="module")
+def ctx(eg):
+    c = eg.Context()
+    yield c
+    c.close()
+
+
+def _flags(eg, path, extra=0):
+    return extra | (eg.EG_FORCE_GENERIC if path == "generic" else 0)
+
+
+def _run(eg, ctx, f, dims, path=0, extra=0):
+    import torch
+    t = torch.from_numpy(np.ascontiguousarray(f, np.float32)).cuda()
+    return ctx.compute(t, dims=dims, flags=_flags(eg, path, extra | eg.EG_RAW_ARCS | eg.EG_CHECK_NAN))
+
+
+@pytest.mark.parametrize("path", PATHS)
+def test_golden(eg, ctx, path):
+    for case in json.load(open(GOLDEN))["cases"]:
+        g = _run(eg, ctx, np.array(case["f"], np.float32), case["dims"], path)
+        assert g.maxima.tolist() == case["maxima"], case["name"]
+        assert [[int(s), int(b)] for s, b in zip(g.saddles, g.saddle_beta)] == case["saddles"], case["name"]
+        assert g.arcs.tolist() == case["arcs"], case["name"]
+        assert g.labels.cpu().numpy().tolist() == case["labels"], case["name"]
+
+
+@pytest.mark.parametrize("path", PATHS)
+def test_c1_full(eg, ctx, path):
+    f, dims = G.c1_gaussians(0, 4.0)
+    o = O.grid(f, dims)
+    g = _run(eg, ctx, f, dims, path)
+    assert_graph_equal(g, o, raw=True, what=f"C1 ({path})")
+    assert len(g.maxima) == 8
+
+
+@pytest.mark.parametrize("path", PATHS)
+def test_sincos(eg, ctx, path):
+    f, dims, *_ = G.sincos(4, 4, 7)
+    assert_graph_equal(_run(eg, ctx, f, dims, path), O.grid(f, dims), raw=True, what="sincos")
+
+
+CASES = [
+    ([1], "normal"), ([2], "int"), ([37], "int"), ([1000], "normal"),
+    ([1, 1], "const"), ([7, 1], "int"), ([1, 9], "int"), ([33, 17], "int"), ([64, 64], "normal"),
+    ([130, 67], "signed_zero"), ([2, 2, 2], "int"), ([1, 1, 5], "int"), ([3, 1, 4], "int"),
+    ([33, 35, 19], "int"), ([65, 33, 17], "normal"), ([70, 9, 40], "signed_zero"), ([31, 64, 33], "const"),
+    ([7, 6, 5, 4], "int"), ([9, 8, 7, 6], "normal"), ([6, 5, 4, 3, 3], "int"), ([8, 7, 6, 5, 4], "normal"),
+    ([4, 3, 3, 2, 3, 3], "int"), ([5, 4, 4, 3, 3, 2], "normal"),
+]
+
+
+@pytest.mark.parametrize("path", PATHS)
+@pytest.mark.parametrize("dims,kind", CASES)
+def test_random_fields(eg, ctx, path, dims, kind):
+    f, _ = G.random_field(dims, 17 + len(dims), kind)
+    assert_graph_equal(_run(eg, ctx, f, dims, path), O.grid(f, dims), raw=True, what=f"{dims} {kind} {path}")
+
+
+@pytest.mark.parametrize("dims,kind", [([33, 17], "int"), ([65, 33, 17], "normal"), ([9, 8, 7, 6], "int"),
+                                       ([8, 7, 6, 5, 4], "normal"), ([4, 3, 3, 2, 3, 3], "int")])
+def test_gradient_and_beta(eg, ctx, dims, kind):
+    # S1 (gradient) and S3 (beta0+) per vertex
+    import torch
+    f, _ = G.random_field(dims, 3, kind)
+    o = O.grid(f, dims)
+    ptr, beta = ctx.gradient(torch.from_numpy(f).cuda(), dims=dims)
+    assert first_diff(ptr.cpu().numpy().astype(np.int64), o.ptr) is None
+    assert first_diff(beta.cpu().numpy().astype(np.int32), np.minimum(o.beta, 255)) is None
+
+
+def test_determinism(eg, ctx):
+    f, dims = G.random_field([70, 40, 30], 5, "int")
+    runs = [_run(eg, ctx, f, dims) for _ in range(3)]
+    for r in runs[1:]:
+        assert np.array_equal(r.arcs, runs[0].arcs)
+        assert np.array_equal(r.labels.cpu().numpy(), runs[0].labels.cpu().numpy())
+
+
+def test_tiled_equals_generic(eg, ctx):
+    f, dims = G.c2_gaussians_noise(n=96, seed=3, k=12)
+    a = _run(eg, ctx, f, dims, 0)
+    la = a.labels.cpu().numpy().copy()
+    b = _run(eg, ctx, f, dims, "generic")
+    assert np.array_equal(a.arcs, b.arcs) and np.array_equal(a.saddles, b.saddles)
+    assert np.array_equal(la, b.labels.cpu().numpy())
+
+
+def test_nan_rejected(eg, ctx):
+    f, dims = G.random_field([20, 10, 5], 1, "normal")
+    f[123] = np.nan
+    for path in PATHS:
+        with pytest.raises(eg.EgError) as e:
+            _run(eg, ctx, f, dims, path)
+        assert "EG_ERR_NAN" in str(e.value)
+    # the context stays usable after a NaN (not sticky)
+    f2, _ = G.random_field([20, 10, 5], 1, "normal")
+    assert_graph_equal(_run(eg, ctx, f2, dims), O.grid(f2, dims))
+
+
+def test_invalid_args(eg, ctx):
+    import torch
+    t = torch.zeros(8, device="cuda")
+    with pytest.raises(eg.EgError) as e:
+        ctx.compute(t, dims=[2, 0, 4])
+    assert "INVALID_ARG" in str(e.value)
+    with pytest.raises(eg.EgError) as e:
+        ctx.compute(t, dims=[2] * 7)
+    assert "UNSUPPORTED" in str(e.value)
+    with pytest.raises(eg.EgError) as e:      # N >= 2^31: rejected before touching memory
+        ctx.compute(t, dims=[2048, 2048, 1024])
+    assert "UNSUPPORTED" in str(e.value)
+
+
+def test_csr_equals_grid(eg, ctx):
+    # L14: the CSR kernels on the Freudenthal graph == the grid kernels
+    import torch
+    from oracle import brute
+    dims = [9, 7, 5]
+    f, _ = G.random_field(dims, 8, "int")
+    row_ptr, col_idx = brute.freudenthal_csr(dims)
+    csr = (torch.from_numpy(row_ptr).cuda(), torch.from_numpy(col_idx).cuda())
+    t = torch.from_numpy(f).cuda()
+    a = ctx.compute(t, csr=csr, flags=eg.EG_RAW_ARCS)
+    la = a.labels.cpu().numpy().copy()
+    b = ctx.compute(t, dims=dims, flags=eg.EG_RAW_ARCS)
+    assert np.array_equal(a.arcs, b.arcs) and np.array_equal(a.raw_arcs, b.raw_arcs)
+    assert np.array_equal(la, b.labels.cpu().numpy())
+
+
+@pytest.mark.parametrize("n,p,seed,kind", [(12, 0.3, 0, "normal"), (40, 0.2, 1, "int"), (300, 0.05, 2, "int"),
+                                           (500, 0.02, 3, "normal")])
+def test_csr_random(eg, ctx, n, p, seed, kind):
+    import torch
+    row_ptr, col_idx = G.random_csr(n, p, seed)
+    f, _ = G.random_field([n], seed, kind, levels=3)
+    o = O.csr(f, row_ptr, col_idx)
+    g = ctx.compute(torch.from_numpy(f).cuda(), csr=(torch.from_numpy(row_ptr).cuda(),
+                                                     torch.from_numpy(col_idx).cuda()),
+                    flags=eg.EG_RAW_ARCS | eg.EG_CHECK_NAN)
+    assert_graph_equal(g, o, raw=True, what="csr random")
+
+
+def test_csr_knn_small(eg, ctx):
+    import torch
+    X, f = G.gmm_points(20000, seed=10)
+    row_ptr, col_idx = G.knn_csr(X, 16, device="cuda")
+    o = O.csr(f, row_ptr, col_idx)
+    g = ctx.compute(torch.from_numpy(f).cuda(), csr=(torch.from_numpy(row_ptr).cuda(),
+                                                     torch.from_numpy(col_idx).cuda()), flags=eg.EG_RAW_ARCS)
+    assert_graph_equal(g, o, raw=True, what="knn 20K")
+
+
+def test_compute_host_e2e(eg, ctx):
+    import torch
+    f, dims = G.c2_gaussians_noise(n=64, seed=1, k=8)
+    o = O.grid(f, dims)
+    host = torch.from_numpy(f).pin_memory()
+    lab = torch.empty(len(f), dtype=torch.int32).pin_memory()
+    g = ctx.compute_host(host, dims=dims, labels_out=lab)
+    assert_graph_equal(g, o)
+    assert np.array_equal(lab.numpy().astype(np.int64), o.label)
+    g2 = ctx.compute_host(torch.from_numpy(f), dims=dims)      # pageable source
+    assert_graph_equal(g2, o)
