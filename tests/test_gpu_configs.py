@@ -1,0 +1,168 @@
+"""Parity at BASELINE.json's configurations, in the launch configuration
+bench.py times (one eg_compute on the resident field, default flags).
+
+* C1 (2D 64^2) and C2 (3D 256^3): the oracle runs on the whole field; every
+  output is compared element by element.
+* C3 (3D 1024^3): too large for the oracle in a test; sampled outputs the
+  oracle computes one by one (Alg. 2 walks for labels, single-vertex
+  classification for beta0+ / gradient, per-saddle arcs), plus properties that
+  hold at any size; and the same recipe at 128^3 in full.
+* C4 (5D 32^5 Schwefel): the closed form of the separable product rule
+  (16,807 maxima, 72,030 saddles, all beta0+ = 2), sampled vertices and
+  saddles against the oracle, and the recipe at 12^5 in full.
+* C5 (1M-point kNN CSR): sampled against the oracle; the recipe at 20K points
+  in full (test_gpu_parity.py).
+"""
+import numpy as np
+import pytest
+
+import eg_inputs as G
+import oracle as O
+from _parity import assert_graph_equal, first_diff
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def eg():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    import paper_2303_02724_b200 as eg
+    return eg
+
+
+@pytest.fixture(scope="module")
+def ctx(eg):
+    c = eg.Context()
+    yield c
+    c.close()
+
+
+def _sampled_grid_checks(g, f, dims, labels, n_lab=400, n_sad=150, seed=0):
+    """Sampled parity for a big grid: labels by the oracle's Alg. 2 walk,
+    saddles (beta0+, arcs) by the oracle's single-vertex classification."""
+    rng = np.random.default_rng(seed)
+    N = len(f)
+    for v in rng.integers(0, N, n_lab):
+        m, _ = O.grid_walk(f, dims, int(v))
+        assert labels[v] == m, f"label of {v}: gpu {labels[v]} oracle {m}"
+    # every reported maximum is a maximum, and is its own label
+    for m in rng.choice(g.maxima, min(len(g.maxima), 200), replace=False):
+        p, b, _ = O.grid_vertex(f, dims, int(m))
+        assert b == 0 and p == m and labels[m] == m
+    # sampled saddles: beta0+ and the deduplicated arcs
+    arcs_by_s = {}
+    for s, m, c in g.arcs.tolist():
+        arcs_by_s.setdefault(s, []).append((m, c))
+    js = rng.choice(len(g.saddles), min(len(g.saddles), n_sad), replace=False) if len(g.saddles) else []
+    for j in js:
+        s = int(g.saddles[j])
+        p, b, reps = O.grid_vertex(f, dims, s)
+        assert b == g.saddle_beta[j] and b >= 2
+        ms = sorted(O.grid_walk(f, dims, int(r))[0] for r in reps)
+        exp = sorted((m, ms.count(m)) for m in set(ms))
+        assert sorted(arcs_by_s[s]) == exp, f"arcs of saddle {s}"
+    # sampled non-saddle, non-maximum vertices really are regular (beta0+ == 1)
+    sad = set(g.saddles.tolist())
+    mx = set(g.maxima.tolist())
+    for v in rng.integers(0, N, n_lab):
+        if int(v) in sad or int(v) in mx:
+            continue
+        p, b, _ = O.grid_vertex(f, dims, int(v))
+        assert b == 1, f"vertex {v} has beta0+ {b} but is not reported"
+    # properties at any size
+    assert int(g.arcs[:, 2].sum()) == int(g.saddle_beta.sum())
+    assert np.all(np.diff(g.saddles) > 0) and np.all(np.diff(g.maxima) > 0)
+    assert np.all(labels[g.maxima] == g.maxima)
+
+
+def test_c1_config(eg, ctx):
+    import torch
+    f, dims = G.c1_gaussians(0, 4.0)
+    g = ctx.compute(torch.from_numpy(f).cuda(), dims=dims, flags=eg.EG_CHECK_NAN)
+    assert_graph_equal(g, O.grid(f, dims), what="C1")
+
+
+def test_c2_config_full(eg, ctx):
+    import torch
+    f, dims = G.c2_gaussians_noise()
+    o = O.grid(f, dims)
+    g = ctx.compute(torch.from_numpy(f).cuda(), dims=dims, flags=eg.EG_CHECK_NAN | eg.EG_RAW_ARCS)
+    assert_graph_equal(g, o, raw=True, what="C2 256^3")
+
+
+def test_c3_recipe_128_full(eg, ctx):
+    import torch
+    t, dims = G.turbulence(128, seed=1024, device="cuda")
+    f = t.cpu().numpy()
+    o = O.grid(f, dims)
+    g = ctx.compute(t, dims=dims, flags=eg.EG_CHECK_NAN | eg.EG_RAW_ARCS)
+    assert_graph_equal(g, o, raw=True, what="C3 recipe at 128^3")
+    g2 = ctx.compute(t, dims=dims, flags=eg.EG_FORCE_GENERIC)
+    assert_graph_equal(g2, o, what="C3 recipe at 128^3 (generic kernels)")
+
+
+def test_c3_config_sampled(eg, ctx):
+    import torch
+    t, dims = G.turbulence(1024, seed=1024, device="cuda")
+    g = ctx.compute(t, dims=dims, flags=eg.EG_CHECK_NAN)
+    labels = g.labels.cpu().numpy()
+    f = t.cpu().numpy()
+    del t
+    torch.cuda.empty_cache()
+    _sampled_grid_checks(g, f, dims, labels)
+    # SURVEY App. A expectations at this recipe (self-similar counts): order of
+    # 10^5 maxima, saddles about 3x maxima
+    assert 5e4 < len(g.maxima) < 5e5 and 1.5 * len(g.maxima) < len(g.saddles) < 6 * len(g.maxima)
+
+
+def test_c4_config_closed_form_and_sampled(eg, ctx):
+    import torch
+    f, dims = G.schwefel()
+    g = ctx.compute(torch.from_numpy(f).cuda(), dims=dims, flags=eg.EG_CHECK_NAN)
+    # separable product rule (tests/test_oracle_pins.py::test_schwefel_profile_counts)
+    assert len(g.maxima) == 7 ** 5 == 16807
+    assert len(g.saddles) == 5 * 6 * 7 ** 4 == 72030
+    assert (g.saddle_beta == 2).all()
+    labels = g.labels.cpu().numpy()
+    _sampled_grid_checks(g, f, dims, labels, n_lab=200, n_sad=100)
+
+
+def test_c4_recipe_small_full(eg, ctx):
+    import torch
+    for dims in ([12] * 5, [9, 10, 11, 12, 13]):
+        f, _ = G.schwefel(dims)
+        o = O.grid(f, dims)
+        g = ctx.compute(torch.from_numpy(f).cuda(), dims=dims, flags=eg.EG_RAW_ARCS)
+        assert_graph_equal(g, o, raw=True, what=f"Schwefel {dims}")
+    f, dims, *_ = G.sumcos([16] * 5, seed=5)
+    assert_graph_equal(ctx.compute(torch.from_numpy(f).cuda(), dims=dims), O.grid(f, dims), what="sumcos 16^5")
+
+
+def test_c5_config_sampled(eg, ctx):
+    import torch
+    X, f = G.gmm_points(1_000_000, seed=10)
+    rp, ci = G.knn_csr(X, 16, device="cuda")
+    csr = (torch.from_numpy(rp).cuda(), torch.from_numpy(ci).cuda())
+    g = ctx.compute(torch.from_numpy(f).cuda(), csr=csr, flags=eg.EG_CHECK_NAN)
+    labels = g.labels.cpu().numpy()
+    rng = np.random.default_rng(1)
+    for v in rng.integers(0, len(f), 300):
+        assert labels[v] == O.csr_walk(f, rp, ci, int(v))[0]
+    arcs_by_s = {}
+    for s, m, c in g.arcs.tolist():
+        arcs_by_s.setdefault(s, []).append((m, c))
+    for j in rng.choice(len(g.saddles), 200, replace=False):
+        s = int(g.saddles[j])
+        p, b, reps = O.csr_vertex(f, rp, ci, s)
+        assert b == g.saddle_beta[j]
+        ms = sorted(int(labels[r]) for r in reps)
+        assert sorted(arcs_by_s[s]) == sorted((m, ms.count(m)) for m in set(ms))
+    # gradient + beta0+ of sampled vertices
+    ptr, beta = ctx.gradient(torch.from_numpy(f).cuda(), csr=csr)
+    ptr, beta = ptr.cpu().numpy(), beta.cpu().numpy()
+    for v in rng.integers(0, len(f), 300):
+        p, b, _ = O.csr_vertex(f, rp, ci, int(v))
+        assert ptr[v] == p and beta[v] == min(b, 255)
+    assert int(g.arcs[:, 2].sum()) == int(g.saddle_beta.sum())
