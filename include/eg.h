@@ -101,6 +101,8 @@ typedef struct {
     int32_t path;                   /* 0 generic n-D grid, 1 tiled 3-D grid, 2 CSR */
     int64_t n_vertices, n_raw_arcs, n_exit_targets;
     int64_t bytes_alg;              /* algorithmic HBM bytes   */
+    double us_main;                 /* device time of the main per-vertex kernel(s) */
+    int64_t bytes_main;             /* their algorithmic bytes */
 } eg_stats;
 
 /* eg_compute flags */

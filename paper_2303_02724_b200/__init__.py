@@ -125,14 +125,21 @@ class Context:
 
     # -------------------------------------------------------------- calls
     def compute(self, field: torch.Tensor, dims: Optional[Sequence[int]] = None, csr=None, flags: int = 0,
-                slab=None, v_range=None) -> Graph:
-        """S1..S4 on a device-resident float32 field (flat, axis 0 fastest)."""
+                slab=None, v_range=None, materialize: bool = True) -> Optional[Graph]:
+        """S1..S4 on a device-resident float32 field (flat, axis 0 fastest).
+        The graph is always copied to host memory owned by the library; with
+        materialize=False no numpy copies are made (use graph() later)."""
         if not (field.is_cuda and field.dtype == torch.float32 and field.is_contiguous()):
             raise TypeError("field must be a contiguous CUDA float32 tensor")
         dom = self._domain(dims, csr, slab, v_range)
         st = _abi.lib().eg_compute(self._h, C.byref(dom), C.c_void_p(field.data_ptr()), flags)
         self._check(st, "eg_compute")
-        return self._graph(flags)
+        self._last_flags = flags
+        return self._graph(flags) if materialize else None
+
+    def graph(self) -> Graph:
+        """The graph of the last compute as numpy arrays (copies)."""
+        return self._graph(getattr(self, "_last_flags", 0))
 
     def compute_host(self, field: torch.Tensor, dims=None, csr=None, flags: int = 0, labels_out=None,
                      slab=None, v_range=None) -> Graph:
@@ -216,3 +223,36 @@ def nccl_unique_id() -> bytes:
     if st != _abi.EG_OK:
         raise EgError(st, "eg_nccl_unique_id failed")
     return buf.raw
+
+
+# ------------------------------------------------------------ multi-GPU host logic
+
+def plan_slabs(depth: int, world: int):
+    """Slab partition of the slowest grid axis (P:278 blocks along z; SURVEY
+    8(e)): `world` contiguous plane ranges [z0, z1) in rank order, balanced to
+    +-1 plane, each of at least 2 planes (the boundary exchange needs distinct
+    first and last planes)."""
+    if world < 1:
+        raise ValueError("world must be >= 1")
+    if world > 1 and depth < 2 * world:
+        raise ValueError(f"{world} slabs need at least {2 * world} planes, the grid has {depth}")
+    return [(depth * r // world, depth * (r + 1) // world) for r in range(world)]
+
+
+def plan_ranges(n: int, world: int):
+    """Vertex-range partition of a CSR graph: `world` contiguous ranges."""
+    return [(n * r // world, n * (r + 1) // world) for r in range(world)]
+
+
+def init_distributed(group=None, device: Optional[int] = None, stream=None) -> "Context":
+    """One Context per rank sharing an NCCL communicator owned by the library.
+    torch.distributed (any backend) only carries the 128-byte NCCL unique id
+    from rank 0 to the others; every exchange of the hot path is NCCL inside
+    libeg_b200.so.  Collective over `group`."""
+    import torch.distributed as dist
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    if world == 1:
+        return Context(device=device, stream=stream)
+    box = [nccl_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(box, src=dist.get_global_rank(group, 0) if group is not None else 0, group=group)
+    return Context(device=device, stream=stream, nccl_id=box[0], rank=rank, world=world)

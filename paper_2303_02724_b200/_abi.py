@@ -53,7 +53,8 @@ class EgStats(C.Structure):
                 ("us_label", C.c_double), ("us_arcs", C.c_double), ("us_graph", C.c_double),
                 ("us_total", C.c_double), ("jump_rounds", C.c_int32), ("boundary_rounds", C.c_int32),
                 ("kernel_launches", C.c_int32), ("path", C.c_int32), ("n_vertices", C.c_int64),
-                ("n_raw_arcs", C.c_int64), ("n_exit_targets", C.c_int64), ("bytes_alg", C.c_int64)]
+                ("n_raw_arcs", C.c_int64), ("n_exit_targets", C.c_int64), ("bytes_alg", C.c_int64),
+                ("us_main", C.c_double), ("bytes_main", C.c_int64)]
 
 
 _lib = None

@@ -24,6 +24,14 @@ NVCC_FLAGS = [
 ]
 
 
+def nccl_paths():
+    """The NCCL that torch loads (pip nvidia-nccl, 2.28.x): the library must use
+    the same one so that one process never mixes two NCCL builds."""
+    import nvidia.nccl
+    base = list(nvidia.nccl.__path__)[0]
+    return os.path.join(base, "include"), os.path.join(base, "lib")
+
+
 def sources():
     return sorted(glob.glob(os.path.join(HERE, "csrc", "*.cu")))
 
@@ -42,7 +50,9 @@ def stale() -> bool:
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not stale():
         return LIB
-    cmd = [NVCC, *NVCC_FLAGS, "-I", os.path.join(ROOT, "include"), "-o", LIB + ".tmp", *sources()]
+    inc, lib = nccl_paths()
+    cmd = [NVCC, *NVCC_FLAGS, "-I", os.path.join(ROOT, "include"), "-I", inc, "-o", LIB + ".tmp", *sources(),
+           "-L", lib, "-l:libnccl.so.2", "-Xlinker", "-rpath=" + lib]
     if verbose:
         print(" ".join(cmd), file=sys.stderr)
     subprocess.check_call(cmd)

@@ -1,11 +1,14 @@
 // C ABI (include/eg.h) and the host-side orchestration of one eg_compute.
 //
-// Stage order per compute:
-//   classify (S1 + S3) -> pointer jumping (S2) -> compaction of maxima and
-//   saddles -> per-saddle beta0+ / arcs (S4) -> graph to host.
-// The field stays resident in HBM; the only host<->device crossings are the
+// Per slab (one GPU, or one virtual partition):
+//   [halo exchange of f]  -> local labels (S1 + S3 + slab-local S2)
+//   [boundary exchange rounds over the two boundary planes]  -> finalize S2
+//   -> compaction of maxima / saddles -> beta0+ -> arcs (S4)
+// then the per-slab graphs are concatenated (rank order = id order) on every
+// rank.  The field stays resident in HBM; host <-> device crossings are the
 // counts needed to size outputs and the final (small) graph.
 #include <cuda_runtime.h>
+#include <nccl.h>
 
 #include <algorithm>
 #include <cstdarg>
@@ -66,6 +69,28 @@ struct HostBuf {
     T *as() const { return static_cast<T *>(p); }
 };
 
+// One slab of a grid (or one vertex range of a CSR graph).
+struct SlabState {
+    Slab s{};
+    FieldView F{};
+    int32_t *label = nullptr;          // owned labels (a view)
+    DevBuf f_lo, f_hi;                 // halo planes of f received from the neighbours
+    DevBuf sad_bits, max_bits, exit_bits;
+    DevBuf bval, hval_lo, hval_hi;     // boundary-plane label values (own / neighbours')
+    bool has_lo = false, has_hi = false;
+    Tiled3D *tiled = nullptr;
+    DevBuf maxima64, saddles32, saddles64, sbeta, slot_off, tmp_m, tmp_mult, n_unique, arc_off;
+    DevBuf arc_s, arc_m, arc_mult, raw_s, raw_rep, raw_m;
+    int64_t n_max = 0, n_sad = 0, n_arc = 0, n_raw = 0;
+    ~SlabState() {
+        DevBuf *b[] = {&f_lo, &f_hi, &sad_bits, &max_bits, &exit_bits, &bval, &hval_lo, &hval_hi, &maxima64,
+                       &saddles32, &saddles64, &sbeta, &slot_off, &tmp_m, &tmp_mult, &n_unique, &arc_off, &arc_s,
+                       &arc_m, &arc_mult, &raw_s, &raw_rep, &raw_m};
+        for (DevBuf *x : b) x->release();
+        tiled3d_destroy(tiled);
+    }
+};
+
 }  // namespace
 
 struct eg_ctx {
@@ -74,25 +99,19 @@ struct eg_ctx {
     bool poisoned = false;
     std::string err;
     int rank = 0, world = 1;
-    void *nccl = nullptr;
+    ncclComm_t comm = nullptr;
 
-    // device working set
-    DevBuf field;                  // eg_compute_host staging target
-    DevBuf ptr;                    // int32 per owned vertex: gradient, then label
-    DevBuf sad_bits, max_bits;     // one bit per owned vertex
-    DevBuf exit_bits;              // tiled path: vertices whose path leaves their tile
-    DevBuf flags;                  // [0] nan, [1] deg overflow, [2..] jump-changed per round
-    DevBuf scratch;                // compaction / scan scratch
-    DevBuf counts;                 // int64 counters
-    DevBuf maxima64, saddles32, saddles64, sbeta, slot_off, tmp_m, tmp_mult, n_unique, arc_off;
-    DevBuf arc_s, arc_m, arc_mult, raw_s, raw_rep, raw_m;
-    DevBuf tab;                    // LinkTable
-    DevBuf halo_label;
+    std::vector<SlabState *> slabs;
+    DevBuf label_all;                  // labels of every slab of this process
+    DevBuf field;                      // eg_compute_host staging target
+    DevBuf flags;                      // [0] nan, [1] deg overflow, [2..] jump-changed per round
+    DevBuf counts;                     // int64 / u64 counters
+    DevBuf scratch;                    // compaction / scan scratch
+    DevBuf tab;                        // LinkTable
+    DevBuf gsend, grecv;               // multi-GPU graph gather
     LinkTable host_tab;
     bool tab_valid = false;
-    eg::Tiled3D *tiled = nullptr;
 
-    // host outputs
     HostBuf h_maxima, h_saddles, h_sbeta, h_arc_s, h_arc_m, h_arc_mult, h_raw_s, h_raw_rep, h_raw_m, h_counts;
     HostBuf h_stage;
     int64_t n_max = 0, n_sad = 0, n_arc = 0, n_raw = 0, n_own = 0;
@@ -100,6 +119,7 @@ struct eg_ctx {
     const int32_t *d_labels = nullptr;
     eg_stats stats{};
     cudaEvent_t ev[8] = {};
+    cudaEvent_t ev_main[2] = {};       // around the main per-vertex kernel(s) of one slab
 };
 
 static eg_status set_err(eg_ctx *c, eg_status s, const char *fmt, ...) {
@@ -127,6 +147,19 @@ static eg_status set_err(eg_ctx *c, eg_status s, const char *fmt, ...) {
         }                                                                                              \
     } while (0)
 
+#define NK(expr)                                                                                             \
+    do {                                                                                                     \
+        ncclResult_t _r = (expr);                                                                            \
+        if (_r != ncclSuccess)                                                                               \
+            return set_err(c, EG_ERR_NCCL, "%s: %s (%s:%d)", #expr, ncclGetErrorString(_r), __FILE__, __LINE__); \
+    } while (0)
+
+#define ST(expr)                         \
+    do {                                 \
+        eg_status _s = (expr);           \
+        if (_s != EG_OK) return _s;      \
+    } while (0)
+
 // ------------------------------------------------------------- validation
 
 struct Problem {
@@ -134,8 +167,11 @@ struct Problem {
     int ndim;
     int64_t dims[8];
     int64_t N;             // total vertices
-    Slab slab;             // grid
+    int64_t plane;         // grid: vertices per plane of the slowest axis
+    int64_t D;             // grid: extent of the slowest axis
+    int64_t z0, z1;        // grid: this rank's planes
     int64_t v0, v1;        // owned range (both kinds)
+    int64_t nnz;
     const int64_t *row_ptr;
     const int32_t *col_idx;
 };
@@ -166,26 +202,22 @@ static eg_status validate(eg_ctx *c, const eg_domain *d, const float *field, boo
         if (N >= (int64_t(1) << 31))
             return set_err(c, EG_ERR_UNSUPPORTED, "N = %lld >= 2^31 (int32 labels)", (long long)N);
         const int64_t D = g.dims[g.ndim - 1];
-        const int64_t plane = N / D;
         int64_t z0 = g.slab_begin, z1 = g.slab_end;
         if (c->world == 1 && z0 == 0 && z1 == 0) z1 = D;   // convenience: 0,0 = whole grid
-        if (z0 < 0 || z1 > D || z0 >= z1) return set_err(c, EG_ERR_INVALID_ARG, "bad slab [%lld, %lld)", (long long)z0, (long long)z1);
+        if (z0 < 0 || z1 > D || z0 >= z1)
+            return set_err(c, EG_ERR_INVALID_ARG, "bad slab [%lld, %lld)", (long long)z0, (long long)z1);
         if (c->world == 1 && (z0 != 0 || z1 != D))
             return set_err(c, EG_ERR_INVALID_ARG, "single-GPU ctx needs the whole grid as its slab");
         P->grid = true;
         P->ndim = g.ndim;
         for (int i = 0; i < g.ndim; ++i) P->dims[i] = g.dims[i];
         P->N = N;
-        P->slab.z0 = z0;
-        P->slab.z1 = z1;
-        P->slab.h0 = z0 > 0 ? z0 - 1 : 0;
-        P->slab.h1 = z1 < D ? z1 + 1 : D;
-        P->slab.plane = plane;
-        P->slab.v0 = z0 * plane;
-        P->slab.v1 = z1 * plane;
-        P->slab.base = P->slab.h0 * plane;
-        P->v0 = P->slab.v0;
-        P->v1 = P->slab.v1;
+        P->D = D;
+        P->plane = N / D;
+        P->z0 = z0;
+        P->z1 = z1;
+        P->v0 = z0 * P->plane;
+        P->v1 = z1 * P->plane;
     } else if (d->kind == EG_DOMAIN_CSR) {
         const eg_csr &g = d->csr;
         if (g.n_vertices < 0 || g.nnz < 0) return set_err(c, EG_ERR_INVALID_ARG, "negative CSR sizes");
@@ -193,20 +225,23 @@ static eg_status validate(eg_ctx *c, const eg_domain *d, const float *field, boo
         int64_t v0 = g.v_begin, v1 = g.v_end;
         if (c->world == 1 && v0 == 0 && v1 == 0) v1 = g.n_vertices;
         if (v0 < 0 || v1 > g.n_vertices || v0 > v1) return set_err(c, EG_ERR_INVALID_ARG, "bad vertex range");
+        if (c->world == 1 && (v0 != 0 || v1 != g.n_vertices))
+            return set_err(c, EG_ERR_INVALID_ARG, "single-GPU ctx needs the whole vertex range");
         if (g.n_vertices > 0 && (!is_device_ptr(g.row_ptr) || (g.nnz > 0 && !is_device_ptr(g.col_idx))))
             return set_err(c, EG_ERR_INVALID_ARG, "row_ptr / col_idx must be device pointers");
         P->grid = false;
         P->N = g.n_vertices;
         P->v0 = v0;
         P->v1 = v1;
+        P->nnz = g.nnz;
         P->row_ptr = g.row_ptr;
         P->col_idx = g.col_idx;
     } else {
         return set_err(c, EG_ERR_INVALID_ARG, "unknown domain kind %d", d->kind);
     }
+    if (P->N > 0 && !field) return set_err(c, EG_ERR_INVALID_ARG, "field is NULL");
     if (P->N > 0 && need_device && !is_device_ptr(field))
         return set_err(c, EG_ERR_INVALID_ARG, "field must be a device pointer");
-    if (P->N > 0 && !field) return set_err(c, EG_ERR_INVALID_ARG, "field is NULL");
     return EG_OK;
 }
 
@@ -228,36 +263,69 @@ static float ev_us(cudaEvent_t a, cudaEvent_t b) {
     return ms * 1000.f;
 }
 
-// -------------------------------------------------------------- pipeline
-
-// S1 + S3 + S2 on the generic path: leaves labels in c->ptr (int32, owned).
-static eg_status run_generic_labels(eg_ctx *c, const Problem &P, const float *f) {
-    const int64_t n = P.v1 - P.v0;
-    const int64_t words = (n + 31) / 32;
-    int *flags = c->flags.as<int>();
-    if (P.grid) {
-        CK(launch_classify_grid(c->tab.as<LinkTable>(), P.ndim, f, P.slab, c->ptr.as<int32_t>(),
-                                c->sad_bits.as<uint32_t>(), c->max_bits.as<uint32_t>(), nullptr, flags, c->stream));
-    } else {
-        CK(launch_classify_csr(P.row_ptr, P.col_idx, f, P.v0, P.v1, c->ptr.as<int32_t>(), c->sad_bits.as<uint32_t>(),
-                               c->max_bits.as<uint32_t>(), nullptr, flags, flags + 1, c->stream));
+static void set_slab_count(eg_ctx *c, size_t k) {
+    while (c->slabs.size() > k) {
+        delete c->slabs.back();
+        c->slabs.pop_back();
     }
+    while (c->slabs.size() < k) c->slabs.push_back(new SlabState());
+}
+
+// ------------------------------------------------------- NCCL transport
+
+static eg_status nccl_allgather_i64(eg_ctx *c, const int64_t *h_in, int n, std::vector<int64_t> &h_out) {
+    CK(c->counts.ensure(sizeof(int64_t) * 16 * (c->world + 1)));
+    int64_t *d = c->counts.as<int64_t>();
+    CK(cudaMemcpyAsync(d, h_in, sizeof(int64_t) * n, cudaMemcpyHostToDevice, c->stream));
+    NK(ncclAllGather(d, d + 16, size_t(n), ncclInt64, c->comm, c->stream));
+    h_out.assign(size_t(n) * c->world, 0);
+    CK(cudaMemcpyAsync(h_out.data(), d + 16, sizeof(int64_t) * n * c->world, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    return EG_OK;
+}
+
+// plane exchange with the neighbour ranks: send_lo (our first plane) goes to
+// rank - 1 and arrives there as its recv_hi; send_hi to rank + 1 as recv_lo
+static eg_status nccl_exchange(eg_ctx *c, const void *send_lo, const void *send_hi, void *recv_lo, void *recv_hi,
+                               size_t count, ncclDataType_t dt) {
+    NK(ncclGroupStart());
+    if (c->rank > 0) {
+        NK(ncclSend(send_lo, count, dt, c->rank - 1, c->comm, c->stream));
+        NK(ncclRecv(recv_lo, count, dt, c->rank - 1, c->comm, c->stream));
+    }
+    if (c->rank < c->world - 1) {
+        NK(ncclSend(send_hi, count, dt, c->rank + 1, c->comm, c->stream));
+        NK(ncclRecv(recv_hi, count, dt, c->rank + 1, c->comm, c->stream));
+    }
+    NK(ncclGroupEnd());
+    return EG_OK;
+}
+
+// ------------------------------------------------------------ grid stages
+
+static eg_status generic_local(eg_ctx *c, const Problem &P, SlabState &S, bool multi, bool timed) {
+    const int64_t n = S.s.v1 - S.s.v0;
+    int *flags = c->flags.as<int>();
+    if (timed) CK(cudaEventRecord(c->ev_main[0], c->stream));
+    CK(launch_classify_grid(c->tab.as<LinkTable>(), P.ndim, S.F, S.s, S.label, S.sad_bits.as<uint32_t>(),
+                            S.max_bits.as<uint32_t>(), nullptr, flags, c->stream));
+    if (timed) CK(cudaEventRecord(c->ev_main[1], c->stream));
     c->stats.kernel_launches += 1;
-    (void)words;
-    CK(cudaEventRecord(c->ev[1], c->stream));
-    // S2: rounds are launched in batches; a round whose predecessor changed
-    // nothing exits at once, so only the flag read-back costs a sync.
+    // S2 inside the slab: rounds are launched in batches; a round whose
+    // predecessor changed nothing exits at once, so only the flag read-back
+    // costs a sync.
     int *changed = flags + 2;
+    CK(cudaMemsetAsync(changed, 0, sizeof(int) * 64, c->stream));
     int rounds = 0;
     const int kBatch = 6;
-    std::vector<int> hflag(64);
-    for (int r0 = 0; r0 < 62; r0 += kBatch) {
-        int r1 = std::min(62, r0 + kBatch);
+    int hflag[64];
+    for (int r0 = 0; r0 < 60; r0 += kBatch) {
+        const int r1 = std::min(60, r0 + kBatch);
         for (int r = r0; r < r1; ++r) {
-            CK(launch_jump_round(c->ptr.as<int32_t>(), n, P.v0, changed, r, c->stream));
+            CK(launch_jump_round(S.label, n, S.s.v0, changed, r, c->stream));
             c->stats.kernel_launches += 1;
         }
-        CK(cudaMemcpyAsync(hflag.data(), changed, sizeof(int) * r1, cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaMemcpyAsync(hflag, changed, sizeof(int) * r1, cudaMemcpyDeviceToHost, c->stream));
         CK(cudaStreamSynchronize(c->stream));
         int first_zero = -1;
         for (int r = 0; r < r1; ++r)
@@ -265,13 +333,100 @@ static eg_status run_generic_labels(eg_ctx *c, const Problem &P, const float *f)
                 first_zero = r;
                 break;
             }
-        if (first_zero >= 0) {
-            rounds = first_zero + 1;
-            break;
-        }
-        rounds = r1;
+        rounds = first_zero >= 0 ? first_zero + 1 : r1;
+        if (first_zero >= 0) break;
     }
-    c->stats.jump_rounds = rounds;
+    c->stats.jump_rounds = std::max(c->stats.jump_rounds, rounds);
+    if (multi) {
+        CK(launch_flag_remote(S.label, n, S.s.v0, c->stream));
+        c->stats.kernel_launches += 1;
+    }
+    return EG_OK;
+}
+
+static eg_status grid_graph(eg_ctx *c, const Problem &P, SlabState &S, bool raw) {
+    const int64_t n = S.s.v1 - S.s.v0;
+    int64_t *cnt = c->counts.as<int64_t>();
+    CK(c->scratch.ensure(std::max(compact_scratch_bytes(std::max<int64_t>(n, 1)), size_t(1) << 16)));
+    CK(launch_count_bits(S.max_bits.as<uint32_t>(), n, c->scratch.p, cnt + 0, c->stream));
+    CK(launch_count_bits(S.sad_bits.as<uint32_t>(), n, c->scratch.p, cnt + 1, c->stream));
+    c->stats.kernel_launches += 4;
+    CK(c->h_counts.ensure(sizeof(int64_t) * 8));
+    int64_t *hc = c->h_counts.as<int64_t>();
+    CK(cudaMemcpyAsync(hc, cnt, sizeof(int64_t) * 2, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    S.n_max = hc[0];
+    S.n_sad = hc[1];
+    const int64_t ns = S.n_sad;
+    CK(S.maxima64.ensure(sizeof(int64_t) * std::max<int64_t>(S.n_max, 1)));
+    CK(S.saddles32.ensure(sizeof(int32_t) * std::max<int64_t>(ns, 1)));
+    CK(S.saddles64.ensure(sizeof(int64_t) * std::max<int64_t>(ns, 1)));
+    CK(launch_compact_bits(S.max_bits.as<uint32_t>(), n, S.s.v0, c->scratch.p, nullptr, S.maxima64.as<int64_t>(),
+                           cnt + 0, c->stream));
+    CK(launch_compact_bits(S.sad_bits.as<uint32_t>(), n, S.s.v0, c->scratch.p, S.saddles32.as<int32_t>(),
+                           S.saddles64.as<int64_t>(), cnt + 1, c->stream));
+    c->stats.kernel_launches += 6;
+    CK(cudaEventRecord(c->ev[3], c->stream));
+
+    // beta0+ per saddle and slot offsets (sum beta0+ = raw arcs)
+    CK(S.sbeta.ensure(sizeof(int32_t) * std::max<int64_t>(ns, 1)));
+    CK(S.slot_off.ensure(sizeof(int64_t) * (ns + 1)));
+    CK(S.arc_off.ensure(sizeof(int64_t) * (ns + 1)));
+    CK(S.n_unique.ensure(sizeof(int32_t) * std::max<int64_t>(ns, 1)));
+    const size_t sb = scan_scratch_bytes(std::max<int64_t>(ns, 1));
+    CK(c->scratch.ensure(sb));
+    if (P.grid)
+        CK(launch_saddle_beta_grid(c->tab.as<LinkTable>(), P.ndim, S.F, S.saddles32.as<int32_t>(), ns,
+                                   S.sbeta.as<int32_t>(), c->stream));
+    else
+        CK(launch_saddle_beta_csr(P.row_ptr, P.col_idx, S.F.own, S.saddles32.as<int32_t>(), ns,
+                                  S.sbeta.as<int32_t>(), c->stream));
+    CK(launch_scan_i32(S.sbeta.as<int32_t>(), S.slot_off.as<int64_t>(), ns, c->scratch.p, sb, c->stream));
+    c->stats.kernel_launches += 2;
+    CK(cudaMemcpyAsync(hc, S.slot_off.as<int64_t>() + ns, sizeof(int64_t), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    const int64_t nraw = hc[0];
+    S.n_raw = nraw;
+    CK(S.tmp_m.ensure(sizeof(int32_t) * std::max<int64_t>(nraw, 1)));
+    CK(S.tmp_mult.ensure(sizeof(int32_t) * std::max<int64_t>(nraw, 1)));
+    if (raw) {
+        CK(S.raw_s.ensure(sizeof(int64_t) * std::max<int64_t>(nraw, 1)));
+        CK(S.raw_rep.ensure(sizeof(int64_t) * std::max<int64_t>(nraw, 1)));
+        CK(S.raw_m.ensure(sizeof(int64_t) * std::max<int64_t>(nraw, 1)));
+    }
+    LabelView lv{};
+    if (P.grid) {
+        lv.own = S.label;
+        lv.v0 = S.s.v0;
+        lv.v1 = S.s.v1;
+        lv.lo = S.has_lo ? S.hval_lo.as<int32_t>() : nullptr;
+        lv.hi = S.has_hi ? S.hval_hi.as<int32_t>() : nullptr;
+        lv.plane = S.s.plane;
+        CK(launch_arcs_grid(c->tab.as<LinkTable>(), P.ndim, S.F, S.saddles32.as<int32_t>(), ns,
+                            S.slot_off.as<int64_t>(), lv, S.tmp_m.as<int32_t>(), S.tmp_mult.as<int32_t>(),
+                            S.n_unique.as<int32_t>(), raw ? S.raw_s.as<int64_t>() : nullptr,
+                            raw ? S.raw_rep.as<int64_t>() : nullptr, raw ? S.raw_m.as<int64_t>() : nullptr, c->stream));
+    } else {
+        lv.own = c->label_all.as<int32_t>();     // CSR: labels of every vertex
+        lv.v0 = 0;
+        lv.v1 = P.N;
+        CK(launch_arcs_csr(P.row_ptr, P.col_idx, S.F.own, S.saddles32.as<int32_t>(), ns, S.slot_off.as<int64_t>(),
+                           lv, S.tmp_m.as<int32_t>(), S.tmp_mult.as<int32_t>(), S.n_unique.as<int32_t>(),
+                           raw ? S.raw_s.as<int64_t>() : nullptr, raw ? S.raw_rep.as<int64_t>() : nullptr,
+                           raw ? S.raw_m.as<int64_t>() : nullptr, c->stream));
+    }
+    CK(launch_scan_i32(S.n_unique.as<int32_t>(), S.arc_off.as<int64_t>(), ns, c->scratch.p, sb, c->stream));
+    c->stats.kernel_launches += 2;
+    CK(cudaMemcpyAsync(hc, S.arc_off.as<int64_t>() + ns, sizeof(int64_t), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    S.n_arc = hc[0];
+    CK(S.arc_s.ensure(sizeof(int64_t) * std::max<int64_t>(S.n_arc, 1)));
+    CK(S.arc_m.ensure(sizeof(int64_t) * std::max<int64_t>(S.n_arc, 1)));
+    CK(S.arc_mult.ensure(sizeof(int32_t) * std::max<int64_t>(S.n_arc, 1)));
+    CK(launch_emit_arcs(S.saddles32.as<int32_t>(), ns, S.slot_off.as<int64_t>(), S.arc_off.as<int64_t>(),
+                        S.tmp_m.as<int32_t>(), S.tmp_mult.as<int32_t>(), S.n_unique.as<int32_t>(),
+                        S.arc_s.as<int64_t>(), S.arc_m.as<int64_t>(), S.arc_mult.as<int32_t>(), c->stream));
+    c->stats.kernel_launches += 1;
     return EG_OK;
 }
 
@@ -279,107 +434,43 @@ static eg_status fail_if_flags(eg_ctx *c) {
     int h[2] = {0, 0};
     CK(cudaMemcpyAsync(h, c->flags.p, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
     CK(cudaStreamSynchronize(c->stream));
+    if (c->world > 1) {
+        int64_t mine[2] = {h[0], h[1]};
+        std::vector<int64_t> all;
+        ST(nccl_allgather_i64(c, mine, 2, all));
+        for (int r = 0; r < c->world; ++r) {
+            h[0] |= int(all[2 * r]);
+            h[1] |= int(all[2 * r + 1]);
+        }
+    }
     if (h[0]) return set_err(c, EG_ERR_NAN, "NaN in the scalar field (reading L2)");
     if (h[1]) return set_err(c, EG_ERR_UNSUPPORTED, "CSR vertex degree > %d", kCsrMaxDeg);
     return EG_OK;
 }
 
-// Node lists, beta0+, arcs (S3 lists + S4) for the owned range; labels in c->ptr.
-static eg_status run_graph(eg_ctx *c, const Problem &P, const float *f, uint32_t flags) {
-    const int64_t n = P.v1 - P.v0;
-    int64_t *cnt = c->counts.as<int64_t>();
-    CK(c->scratch.ensure(std::max(compact_scratch_bytes(std::max<int64_t>(n, 1)), size_t(1) << 16)));
-    // maxima (ascending, int64 for the host) and saddles (int32 for the kernels)
-    CK(c->maxima64.ensure(sizeof(int64_t) * 1));
-    // counts first (exact sizes): two cheap compaction passes
-    // pass 1: count only (out pointers null)
-    CK(launch_compact_bits(c->max_bits.as<uint32_t>(), n, P.v0, c->scratch.p, nullptr, nullptr, cnt + 0, c->stream));
-    CK(launch_compact_bits(c->sad_bits.as<uint32_t>(), n, P.v0, c->scratch.p, nullptr, nullptr, cnt + 1, c->stream));
-    c->stats.kernel_launches += 6;
-    CK(c->h_counts.ensure(sizeof(int64_t) * 8));
-    int64_t *hc = c->h_counts.as<int64_t>();
-    CK(cudaMemcpyAsync(hc, cnt, sizeof(int64_t) * 2, cudaMemcpyDeviceToHost, c->stream));
-    CK(cudaStreamSynchronize(c->stream));
-    c->n_max = hc[0];
-    c->n_sad = hc[1];
-    CK(c->maxima64.ensure(sizeof(int64_t) * std::max<int64_t>(c->n_max, 1)));
-    CK(c->saddles32.ensure(sizeof(int32_t) * std::max<int64_t>(c->n_sad, 1)));
-    CK(c->saddles64.ensure(sizeof(int64_t) * std::max<int64_t>(c->n_sad, 1)));
-    CK(launch_compact_bits(c->max_bits.as<uint32_t>(), n, P.v0, c->scratch.p, nullptr, c->maxima64.as<int64_t>(),
-                           cnt + 0, c->stream));
-    CK(launch_compact_bits(c->sad_bits.as<uint32_t>(), n, P.v0, c->scratch.p, c->saddles32.as<int32_t>(),
-                           c->saddles64.as<int64_t>(), cnt + 1, c->stream));
-    c->stats.kernel_launches += 6;
-    CK(cudaEventRecord(c->ev[3], c->stream));
-
-    // beta0+ per saddle and slot offsets (sum beta = raw arcs)
-    const int64_t ns = c->n_sad;
-    CK(c->sbeta.ensure(sizeof(int32_t) * std::max<int64_t>(ns, 1)));
-    CK(c->slot_off.ensure(sizeof(int64_t) * (ns + 1)));
-    CK(c->arc_off.ensure(sizeof(int64_t) * (ns + 1)));
-    CK(c->n_unique.ensure(sizeof(int32_t) * std::max<int64_t>(ns, 1)));
-    size_t sb = scan_scratch_bytes(std::max<int64_t>(ns, 1));
-    CK(c->scratch.ensure(sb));
-    if (P.grid)
-        CK(launch_saddle_beta_grid(c->tab.as<LinkTable>(), P.ndim, f, P.slab, c->saddles32.as<int32_t>(), ns,
-                                   c->sbeta.as<int32_t>(), c->stream));
-    else
-        CK(launch_saddle_beta_csr(P.row_ptr, P.col_idx, f, c->saddles32.as<int32_t>(), ns, c->sbeta.as<int32_t>(),
-                                  c->stream));
-    CK(launch_scan_i32(c->sbeta.as<int32_t>(), c->slot_off.as<int64_t>(), ns, c->scratch.p, sb, c->stream));
-    c->stats.kernel_launches += 2;
-    CK(cudaMemcpyAsync(hc, c->slot_off.as<int64_t>() + ns, sizeof(int64_t), cudaMemcpyDeviceToHost, c->stream));
-    CK(cudaStreamSynchronize(c->stream));
-    const int64_t nraw = hc[0];
-    c->n_raw = nraw;
-    CK(c->tmp_m.ensure(sizeof(int32_t) * std::max<int64_t>(nraw, 1)));
-    CK(c->tmp_mult.ensure(sizeof(int32_t) * std::max<int64_t>(nraw, 1)));
-    const bool raw = (flags & EG_RAW_ARCS) != 0;
-    if (raw) {
-        CK(c->raw_s.ensure(sizeof(int64_t) * std::max<int64_t>(nraw, 1)));
-        CK(c->raw_rep.ensure(sizeof(int64_t) * std::max<int64_t>(nraw, 1)));
-        CK(c->raw_m.ensure(sizeof(int64_t) * std::max<int64_t>(nraw, 1)));
+// copy every slab's graph to the host (rank order = id order); multi-GPU:
+// all-gather so that every rank holds the whole graph
+static eg_status gather_graph(eg_ctx *c, bool raw) {
+    int64_t nm = 0, ns = 0, na = 0, nr = 0;
+    for (SlabState *S : c->slabs) {
+        nm += S->n_max;
+        ns += S->n_sad;
+        na += S->n_arc;
+        nr += S->n_raw;
     }
-    LabelView lv{};
-    lv.own = c->d_labels;
-    lv.v0 = P.v0;
-    lv.v1 = P.v1;
-    lv.halo = c->halo_label.as<int32_t>();
-    if (P.grid) {
-        lv.plane = P.slab.plane;
-        lv.lo_base = P.slab.z0 > 0 ? (P.slab.z0 - 1) * P.slab.plane : -1;
-        lv.hi_base = P.slab.z1 < P.dims[P.ndim - 1] ? P.slab.z1 * P.slab.plane : -1;
-        CK(launch_arcs_grid(c->tab.as<LinkTable>(), P.ndim, f, P.slab, c->saddles32.as<int32_t>(), ns,
-                            c->slot_off.as<int64_t>(), lv, c->tmp_m.as<int32_t>(), c->tmp_mult.as<int32_t>(),
-                            c->n_unique.as<int32_t>(), raw ? c->raw_s.as<int64_t>() : nullptr,
-                            raw ? c->raw_rep.as<int64_t>() : nullptr, raw ? c->raw_m.as<int64_t>() : nullptr,
-                            c->stream));
-    } else {
-        CK(launch_arcs_csr(P.row_ptr, P.col_idx, f, c->saddles32.as<int32_t>(), ns, c->slot_off.as<int64_t>(), lv,
-                           c->tmp_m.as<int32_t>(), c->tmp_mult.as<int32_t>(), c->n_unique.as<int32_t>(),
-                           raw ? c->raw_s.as<int64_t>() : nullptr, raw ? c->raw_rep.as<int64_t>() : nullptr,
-                           raw ? c->raw_m.as<int64_t>() : nullptr, c->stream));
+    std::vector<int64_t> all;
+    int64_t mx[3] = {0, 0, 0};
+    if (c->world > 1) {
+        int64_t mine[3] = {nm, ns, na};
+        ST(nccl_allgather_i64(c, mine, 3, all));
+        nm = ns = na = 0;
+        for (int r = 0; r < c->world; ++r) {
+            nm += all[3 * r];
+            ns += all[3 * r + 1];
+            na += all[3 * r + 2];
+            for (int k = 0; k < 3; ++k) mx[k] = std::max(mx[k], all[3 * r + k]);
+        }
     }
-    CK(launch_scan_i32(c->n_unique.as<int32_t>(), c->arc_off.as<int64_t>(), ns, c->scratch.p, sb, c->stream));
-    c->stats.kernel_launches += 2;
-    CK(cudaMemcpyAsync(hc, c->arc_off.as<int64_t>() + ns, sizeof(int64_t), cudaMemcpyDeviceToHost, c->stream));
-    CK(cudaStreamSynchronize(c->stream));
-    c->n_arc = hc[0];
-    CK(c->arc_s.ensure(sizeof(int64_t) * std::max<int64_t>(c->n_arc, 1)));
-    CK(c->arc_m.ensure(sizeof(int64_t) * std::max<int64_t>(c->n_arc, 1)));
-    CK(c->arc_mult.ensure(sizeof(int32_t) * std::max<int64_t>(c->n_arc, 1)));
-    CK(launch_emit_arcs(c->saddles32.as<int32_t>(), ns, c->slot_off.as<int64_t>(), c->arc_off.as<int64_t>(),
-                        c->tmp_m.as<int32_t>(), c->tmp_mult.as<int32_t>(), c->n_unique.as<int32_t>(),
-                        c->arc_s.as<int64_t>(), c->arc_m.as<int64_t>(), c->arc_mult.as<int32_t>(), c->stream));
-    c->stats.kernel_launches += 1;
-    CK(cudaEventRecord(c->ev[4], c->stream));
-    c->stats.n_raw_arcs = nraw;
-    c->raw_valid = raw;
-    return EG_OK;
-}
-
-static eg_status graph_to_host(eg_ctx *c, bool raw) {
-    const int64_t nm = c->n_max, ns = c->n_sad, na = c->n_arc;
     CK(c->h_maxima.ensure(sizeof(int64_t) * std::max<int64_t>(nm, 1)));
     CK(c->h_saddles.ensure(sizeof(int64_t) * std::max<int64_t>(ns, 1)));
     CK(c->h_sbeta.ensure(sizeof(int32_t) * std::max<int64_t>(ns, 1)));
@@ -387,97 +478,386 @@ static eg_status graph_to_host(eg_ctx *c, bool raw) {
     CK(c->h_arc_m.ensure(sizeof(int64_t) * std::max<int64_t>(na, 1)));
     CK(c->h_arc_mult.ensure(sizeof(int32_t) * std::max<int64_t>(na, 1)));
     cudaStream_t st = c->stream;
-    if (nm) CK(cudaMemcpyAsync(c->h_maxima.p, c->maxima64.p, sizeof(int64_t) * nm, cudaMemcpyDeviceToHost, st));
-    if (ns) {
-        CK(cudaMemcpyAsync(c->h_saddles.p, c->saddles64.p, sizeof(int64_t) * ns, cudaMemcpyDeviceToHost, st));
-        CK(cudaMemcpyAsync(c->h_sbeta.p, c->sbeta.p, sizeof(int32_t) * ns, cudaMemcpyDeviceToHost, st));
-    }
-    if (na) {
-        CK(cudaMemcpyAsync(c->h_arc_s.p, c->arc_s.p, sizeof(int64_t) * na, cudaMemcpyDeviceToHost, st));
-        CK(cudaMemcpyAsync(c->h_arc_m.p, c->arc_m.p, sizeof(int64_t) * na, cudaMemcpyDeviceToHost, st));
-        CK(cudaMemcpyAsync(c->h_arc_mult.p, c->arc_mult.p, sizeof(int32_t) * na, cudaMemcpyDeviceToHost, st));
+    if (c->world == 1) {
+        int64_t om = 0, os = 0, oa = 0;
+        for (SlabState *S : c->slabs) {
+            if (S->n_max)
+                CK(cudaMemcpyAsync(c->h_maxima.as<int64_t>() + om, S->maxima64.p, sizeof(int64_t) * S->n_max,
+                                   cudaMemcpyDeviceToHost, st));
+            if (S->n_sad) {
+                CK(cudaMemcpyAsync(c->h_saddles.as<int64_t>() + os, S->saddles64.p, sizeof(int64_t) * S->n_sad,
+                                   cudaMemcpyDeviceToHost, st));
+                CK(cudaMemcpyAsync(c->h_sbeta.as<int32_t>() + os, S->sbeta.p, sizeof(int32_t) * S->n_sad,
+                                   cudaMemcpyDeviceToHost, st));
+            }
+            if (S->n_arc) {
+                CK(cudaMemcpyAsync(c->h_arc_s.as<int64_t>() + oa, S->arc_s.p, sizeof(int64_t) * S->n_arc,
+                                   cudaMemcpyDeviceToHost, st));
+                CK(cudaMemcpyAsync(c->h_arc_m.as<int64_t>() + oa, S->arc_m.p, sizeof(int64_t) * S->n_arc,
+                                   cudaMemcpyDeviceToHost, st));
+                CK(cudaMemcpyAsync(c->h_arc_mult.as<int32_t>() + oa, S->arc_mult.p, sizeof(int32_t) * S->n_arc,
+                                   cudaMemcpyDeviceToHost, st));
+            }
+            om += S->n_max;
+            os += S->n_sad;
+            oa += S->n_arc;
+        }
+    } else {
+        // padded all-gather of 6 arrays through one staging buffer, 8-byte slots
+        SlabState &S = *c->slabs[0];
+        const int W = c->world;
+        const int64_t m3[6] = {mx[0], mx[1], mx[1], mx[2], mx[2], mx[2]};
+        const int64_t mine[6] = {S.n_max, S.n_sad, S.n_sad, S.n_arc, S.n_arc, S.n_arc};
+        const void *src[6] = {S.maxima64.p, S.saddles64.p, S.sbeta.p, S.arc_s.p, S.arc_m.p, S.arc_mult.p};
+        const size_t esz[6] = {8, 8, 4, 8, 8, 4};
+        void *dst[6] = {c->h_maxima.p, c->h_saddles.p, c->h_sbeta.p, c->h_arc_s.p, c->h_arc_m.p, c->h_arc_mult.p};
+        for (int a = 0; a < 6; ++a) {
+            const size_t slot = size_t(std::max<int64_t>(m3[a], 1)) * esz[a];
+            CK(c->gsend.ensure(slot));
+            CK(c->grecv.ensure(slot * W));
+            if (mine[a]) CK(cudaMemcpyAsync(c->gsend.p, src[a], mine[a] * esz[a], cudaMemcpyDeviceToDevice, st));
+            NK(ncclAllGather(c->gsend.p, c->grecv.p, slot, ncclUint8, c->comm, st));
+            int64_t off = 0;
+            for (int r = 0; r < W; ++r) {
+                const int64_t cnt = (a == 0) ? all[3 * r] : (a < 3 ? all[3 * r + 1] : all[3 * r + 2]);
+                if (cnt)
+                    CK(cudaMemcpyAsync(static_cast<char *>(dst[a]) + off * esz[a], c->grecv.as<char>() + r * slot,
+                                       cnt * esz[a], cudaMemcpyDeviceToHost, st));
+                off += cnt;
+            }
+        }
     }
     if (raw) {
-        const int64_t nr = c->n_raw;
         CK(c->h_raw_s.ensure(sizeof(int64_t) * std::max<int64_t>(nr, 1)));
         CK(c->h_raw_rep.ensure(sizeof(int64_t) * std::max<int64_t>(nr, 1)));
         CK(c->h_raw_m.ensure(sizeof(int64_t) * std::max<int64_t>(nr, 1)));
-        if (nr) {
-            CK(cudaMemcpyAsync(c->h_raw_s.p, c->raw_s.p, sizeof(int64_t) * nr, cudaMemcpyDeviceToHost, st));
-            CK(cudaMemcpyAsync(c->h_raw_rep.p, c->raw_rep.p, sizeof(int64_t) * nr, cudaMemcpyDeviceToHost, st));
-            CK(cudaMemcpyAsync(c->h_raw_m.p, c->raw_m.p, sizeof(int64_t) * nr, cudaMemcpyDeviceToHost, st));
+        int64_t o = 0;
+        for (SlabState *S : c->slabs) {
+            if (S->n_raw) {
+                CK(cudaMemcpyAsync(c->h_raw_s.as<int64_t>() + o, S->raw_s.p, 8 * S->n_raw, cudaMemcpyDeviceToHost, st));
+                CK(cudaMemcpyAsync(c->h_raw_rep.as<int64_t>() + o, S->raw_rep.p, 8 * S->n_raw, cudaMemcpyDeviceToHost,
+                                   st));
+                CK(cudaMemcpyAsync(c->h_raw_m.as<int64_t>() + o, S->raw_m.p, 8 * S->n_raw, cudaMemcpyDeviceToHost, st));
+            }
+            o += S->n_raw;
         }
     }
+    c->n_max = nm;
+    c->n_sad = ns;
+    c->n_arc = na;
+    c->n_raw = nr;
+    return EG_OK;
+}
+
+// the boundary exchange: rounds of neighbour plane exchange and
+// jumping until no boundary value of any slab is unresolved
+static eg_status boundary_rounds(eg_ctx *c, int *rounds_out) {
+    auto &slabs = c->slabs;
+    const size_t K = slabs.size();
+    unsigned long long *d_unres = reinterpret_cast<unsigned long long *>(c->counts.as<int64_t>() + 8);
+    for (SlabState *S : slabs) {
+        CK(launch_bval_init(S->label, S->s, S->bval.as<int32_t>(), c->stream));
+        c->stats.kernel_launches += 1;
+    }
+    int rounds = 0;
+    for (int it = 0;; ++it) {
+        // exchange: hval_lo of slab k = bval_hi of slab k-1; hval_hi = bval_lo of slab k+1
+        const int64_t plane = slabs[0]->s.plane;
+        if (c->world > 1) {
+            SlabState &S = *slabs[0];
+            ST(nccl_exchange(c, S.bval.as<int32_t>(), S.bval.as<int32_t>() + plane, S.hval_lo.as<int32_t>(),
+                             S.hval_hi.as<int32_t>(), size_t(plane), ncclInt32));
+        } else {
+            for (size_t k = 0; k < K; ++k) {
+                if (k > 0)
+                    CK(cudaMemcpyAsync(slabs[k]->hval_lo.p, slabs[k - 1]->bval.as<int32_t>() + plane, 4 * plane,
+                                       cudaMemcpyDeviceToDevice, c->stream));
+                if (k + 1 < K)
+                    CK(cudaMemcpyAsync(slabs[k]->hval_hi.p, slabs[k + 1]->bval.as<int32_t>(), 4 * plane,
+                                       cudaMemcpyDeviceToDevice, c->stream));
+            }
+        }
+        if (it > 0) {
+            // the previous update left no unresolved value anywhere: the
+            // exchange just done made the halo values final too
+            unsigned long long u = 0;
+            CK(cudaMemcpyAsync(&u, d_unres, sizeof(u), cudaMemcpyDeviceToHost, c->stream));
+            CK(cudaStreamSynchronize(c->stream));
+            if (u == 0) break;
+        }
+        if (it > 4096) return set_err(c, EG_ERR_STATE, "boundary exchange did not converge");
+        CK(cudaMemsetAsync(d_unres, 0, sizeof(unsigned long long), c->stream));
+        for (SlabState *S : slabs) {
+            CK(launch_bval_update(S->bval.as<int32_t>(), S->has_lo ? S->hval_lo.as<int32_t>() : nullptr,
+                                  S->has_hi ? S->hval_hi.as<int32_t>() : nullptr, S->s, d_unres, c->stream));
+            c->stats.kernel_launches += 1;
+        }
+        if (c->world > 1) NK(ncclAllReduce(d_unres, d_unres, 1, ncclUint64, ncclSum, c->comm, c->stream));
+        ++rounds;
+    }
+    *rounds_out = rounds;
+    return EG_OK;
+}
+
+static eg_status compute_grid(eg_ctx *c, const Problem &P, const float *f, uint32_t flags) {
+    const int vparts = int((flags >> 8) & 0xffffff);
+    // ---- plan the slabs of this process
+    std::vector<std::pair<int64_t, int64_t>> plan;
+    if (c->world > 1) {
+        plan.push_back({P.z0, P.z1});
+        int64_t mine[2] = {P.z0, P.z1};
+        std::vector<int64_t> all;
+        ST(nccl_allgather_i64(c, mine, 2, all));
+        for (int r = 0; r < c->world; ++r) {
+            const int64_t a = all[2 * r], b = all[2 * r + 1];
+            const int64_t prev = r ? all[2 * r - 1] : 0;
+            if (a != prev || b - a < 2 || (r == c->world - 1 && b != P.D))
+                return set_err(c, EG_ERR_INVALID_ARG, "slabs must tile the slowest axis in rank order, >= 2 planes each");
+        }
+    } else if (vparts > 1) {
+        if (P.D < 2 * vparts) return set_err(c, EG_ERR_INVALID_ARG, "%d virtual slabs need >= %d planes", vparts, 2 * vparts);
+        for (int k = 0; k < vparts; ++k) plan.push_back({P.D * k / vparts, P.D * (k + 1) / vparts});
+    } else {
+        plan.push_back({0, P.D});
+    }
+    const bool multi = plan.size() > 1 || c->world > 1;
+    const bool tiled = P.ndim <= 3 && !(flags & EG_FORCE_GENERIC) && (!multi || P.ndim == 3);
+    set_slab_count(c, plan.size());
+    // labels: one array for every slab of this process (a view per slab)
+    const int64_t nlab = (c->world > 1) ? P.v1 - P.v0 : P.N;
+    CK(c->label_all.ensure(sizeof(int32_t) * std::max<int64_t>(nlab, 1)));
+    const int64_t base_v = (c->world > 1) ? P.v0 : 0;
+    for (size_t k = 0; k < plan.size(); ++k) {
+        SlabState &S = *c->slabs[k];
+        S.s.z0 = plan[k].first;
+        S.s.z1 = plan[k].second;
+        S.s.plane = P.plane;
+        S.s.v0 = S.s.z0 * P.plane;
+        S.s.v1 = S.s.z1 * P.plane;
+        const int64_t n = S.s.v1 - S.s.v0, words = (n + 31) / 32;
+        S.label = c->label_all.as<int32_t>() + (S.s.v0 - base_v);
+        S.F.own = f + (S.s.v0 - base_v);     // f holds the whole grid (single / virtual) or the owned planes
+        S.F.v0 = S.s.v0;
+        S.F.v1 = S.s.v1;
+        S.F.plane = P.plane;
+        S.has_lo = multi && S.s.z0 > 0;
+        S.has_hi = multi && S.s.z1 < P.D;
+        CK(S.sad_bits.ensure(sizeof(uint32_t) * std::max<int64_t>(words, 1)));
+        CK(S.max_bits.ensure(sizeof(uint32_t) * std::max<int64_t>(words, 1)));
+        if (tiled) {
+            CK(S.exit_bits.ensure(sizeof(uint32_t) * std::max<int64_t>(words, 1)));
+            if (!S.tiled) S.tiled = tiled3d_create();
+        }
+        if (multi) {
+            CK(S.f_lo.ensure(sizeof(float) * P.plane));
+            CK(S.f_hi.ensure(sizeof(float) * P.plane));
+            CK(S.bval.ensure(sizeof(int32_t) * 2 * P.plane));
+            CK(S.hval_lo.ensure(sizeof(int32_t) * P.plane));
+            CK(S.hval_hi.ensure(sizeof(int32_t) * P.plane));
+        }
+        S.F.lo = S.has_lo ? S.f_lo.as<float>() : nullptr;
+        S.F.hi = S.has_hi ? S.f_hi.as<float>() : nullptr;
+    }
+    ST(ensure_table(c, P));
+    CK(cudaEventRecord(c->ev[0], c->stream));
+
+    // ---- halo planes of f (P:281 ghost vertices)
+    if (multi) {
+        if (c->world > 1) {
+            SlabState &S = *c->slabs[0];
+            const int64_t np = S.s.z1 - S.s.z0;
+            ST(nccl_exchange(c, S.F.own, S.F.own + (np - 1) * P.plane, S.f_lo.p, S.f_hi.p, size_t(P.plane), ncclFloat32));
+        } else {
+            for (size_t k = 0; k < plan.size(); ++k) {
+                SlabState &S = *c->slabs[k];
+                if (S.has_lo) {
+                    SlabState &L = *c->slabs[k - 1];
+                    CK(cudaMemcpyAsync(S.f_lo.p, L.F.own + (L.s.v1 - L.s.v0 - P.plane), 4 * P.plane,
+                                       cudaMemcpyDeviceToDevice, c->stream));
+                }
+                if (S.has_hi)
+                    CK(cudaMemcpyAsync(S.f_hi.p, c->slabs[k + 1]->F.own, 4 * P.plane, cudaMemcpyDeviceToDevice,
+                                       c->stream));
+            }
+        }
+    }
+    // ---- local labels (the main kernel of slab 0 is timed for the roofline)
+    c->stats.bytes_main = 8 * (c->slabs[0]->s.v1 - c->slabs[0]->s.v0);   // read f + write label once
+    for (SlabState *S : c->slabs) {
+        const bool first = S == c->slabs[0];
+        if (tiled) {
+            eg_status s = tiled3d_local(S->tiled, P.ndim, P.dims, S->s, S->F, S->label, S->sad_bits.as<uint32_t>(),
+                                        S->max_bits.as<uint32_t>(), S->exit_bits.as<uint32_t>(), c->flags.as<int>(),
+                                        c->stream, &c->stats, &c->err, first ? c->ev_main[0] : nullptr,
+                                        first ? c->ev_main[1] : nullptr);
+            if (s != EG_OK) {
+                if (s == EG_ERR_CUDA) c->poisoned = true;
+                return s;
+            }
+        } else {
+            ST(generic_local(c, P, *S, multi, first));
+        }
+    }
+    c->stats.path = tiled ? 1 : 0;
+    CK(cudaEventRecord(c->ev[1], c->stream));
+    // ---- cross-slab resolution, then every unresolved owned label
+    if (multi) {
+        int rounds = 0;
+        ST(boundary_rounds(c, &rounds));
+        c->stats.boundary_rounds = rounds;
+    }
+    for (SlabState *S : c->slabs) {
+        if (!tiled && !multi) continue;           // generic single slab: already final
+        CK(launch_finalize(S->label, tiled ? S->exit_bits.as<uint32_t>() : nullptr, S->s.v0, S->s.v1,
+                           S->has_lo ? S->hval_lo.as<int32_t>() : nullptr,
+                           S->has_hi ? S->hval_hi.as<int32_t>() : nullptr, P.plane, c->stream));
+        c->stats.kernel_launches += 1;
+    }
+    CK(cudaEventRecord(c->ev[2], c->stream));
+    ST(fail_if_flags(c));
+    c->d_labels = c->label_all.as<int32_t>();
+    c->n_own = nlab;
+    c->have_labels = true;
+    const bool raw = (flags & EG_RAW_ARCS) != 0;
+    for (SlabState *S : c->slabs) ST(grid_graph(c, P, *S, raw));
+    CK(cudaEventRecord(c->ev[4], c->stream));
+    c->raw_valid = raw;
+    return EG_OK;
+}
+
+// ------------------------------------------------------------- CSR stages
+
+static eg_status compute_csr(eg_ctx *c, const Problem &P, const float *f, uint32_t flags) {
+    const int vparts = int((flags >> 8) & 0xffffff);
+    std::vector<std::pair<int64_t, int64_t>> plan;       // vertex ranges of this process
+    std::vector<int64_t> all;                            // every rank's range (multi-GPU)
+    if (c->world > 1) {
+        plan.push_back({P.v0, P.v1});
+        int64_t mine[2] = {P.v0, P.v1};
+        ST(nccl_allgather_i64(c, mine, 2, all));
+        for (int r = 0; r < c->world; ++r) {
+            const int64_t prev = r ? all[2 * r - 1] : 0;
+            if (all[2 * r] != prev || (r == c->world - 1 && all[2 * r + 1] != P.N))
+                return set_err(c, EG_ERR_INVALID_ARG, "vertex ranges must tile [0, N) in rank order");
+        }
+    } else if (vparts > 1) {
+        for (int k = 0; k < vparts; ++k) plan.push_back({P.N * k / vparts, P.N * (k + 1) / vparts});
+    } else {
+        plan.push_back({0, P.N});
+    }
+    set_slab_count(c, plan.size());
+    // every rank holds the full pointer / label array (the graph is replicated)
+    CK(c->label_all.ensure(sizeof(int32_t) * std::max<int64_t>(P.N, 1)));
+    for (size_t k = 0; k < plan.size(); ++k) {
+        SlabState &S = *c->slabs[k];
+        S.s = Slab{0, 0, 0, plan[k].first, plan[k].second};
+        S.F = FieldView{f, nullptr, nullptr, 0, P.N, 0};
+        S.label = c->label_all.as<int32_t>() + S.s.v0;
+        const int64_t words = (S.s.v1 - S.s.v0 + 31) / 32;
+        CK(S.sad_bits.ensure(sizeof(uint32_t) * std::max<int64_t>(words, 1)));
+        CK(S.max_bits.ensure(sizeof(uint32_t) * std::max<int64_t>(words, 1)));
+        S.has_lo = S.has_hi = false;
+    }
+    CK(cudaEventRecord(c->ev[0], c->stream));
+    int *fl = c->flags.as<int>();
+    {
+        const int64_t n0 = c->slabs[0]->s.v1 - c->slabs[0]->s.v0;
+        // f, the CSR rows of the range, the gradient written once
+        c->stats.bytes_main = 8 * n0 + 8 * (n0 + 1) + 4 * (P.nnz * n0 / std::max<int64_t>(P.N, 1));
+    }
+    for (SlabState *S : c->slabs) {
+        const bool first = S == c->slabs[0];
+        if (first) CK(cudaEventRecord(c->ev_main[0], c->stream));
+        CK(launch_classify_csr(P.row_ptr, P.col_idx, f, S->s.v0, S->s.v1, S->label, S->sad_bits.as<uint32_t>(),
+                               S->max_bits.as<uint32_t>(), nullptr, fl, fl + 1, c->stream));
+        if (first) CK(cudaEventRecord(c->ev_main[1], c->stream));
+        c->stats.kernel_launches += 1;
+    }
+    if (c->world > 1) {
+        // the one exchange step: every rank's gradients to every rank
+        NK(ncclGroupStart());
+        for (int r = 0; r < c->world; ++r) {
+            const int64_t a = all[2 * r], b = all[2 * r + 1];
+            if (b > a)
+                NK(ncclBroadcast(c->label_all.as<int32_t>() + a, c->label_all.as<int32_t>() + a, size_t(b - a),
+                                 ncclInt32, r, c->comm, c->stream));
+        }
+        NK(ncclGroupEnd());
+    }
+    CK(cudaEventRecord(c->ev[1], c->stream));
+    // S2 on the full array (every rank; N is small for CSR workloads)
+    SlabState whole;
+    whole.s = Slab{0, 0, 0, 0, P.N};
+    whole.label = c->label_all.as<int32_t>();
+    {
+        int *changed = fl + 2;
+        CK(cudaMemsetAsync(changed, 0, sizeof(int) * 64, c->stream));
+        int hflag[64], rounds = 0;
+        for (int r0 = 0; r0 < 60; r0 += 6) {
+            const int r1 = std::min(60, r0 + 6);
+            for (int r = r0; r < r1; ++r) {
+                CK(launch_jump_round(whole.label, P.N, 0, changed, r, c->stream));
+                c->stats.kernel_launches += 1;
+            }
+            CK(cudaMemcpyAsync(hflag, changed, sizeof(int) * r1, cudaMemcpyDeviceToHost, c->stream));
+            CK(cudaStreamSynchronize(c->stream));
+            int fz = -1;
+            for (int r = 0; r < r1; ++r)
+                if (hflag[r] == 0) {
+                    fz = r;
+                    break;
+                }
+            rounds = fz >= 0 ? fz + 1 : r1;
+            if (fz >= 0) break;
+        }
+        c->stats.jump_rounds = rounds;
+    }
+    whole.label = nullptr;
+    CK(cudaEventRecord(c->ev[2], c->stream));
+    ST(fail_if_flags(c));
+    c->stats.path = 2;
+    c->d_labels = c->label_all.as<int32_t>() + (c->world > 1 ? P.v0 : 0);
+    c->n_own = (c->world > 1) ? P.v1 - P.v0 : P.N;
+    c->have_labels = true;
+    const bool raw = (flags & EG_RAW_ARCS) != 0;
+    for (SlabState *S : c->slabs) ST(grid_graph(c, P, *S, raw));
+    CK(cudaEventRecord(c->ev[4], c->stream));
+    c->raw_valid = raw;
     return EG_OK;
 }
 
 static eg_status compute_impl(eg_ctx *c, const eg_domain *d, const float *f, uint32_t flags, bool device_field) {
     if (!c) return EG_ERR_INVALID_ARG;
-    if (c->poisoned) return set_err(c, EG_ERR_STATE, "context is poisoned by an earlier CUDA/NCCL error: %s", c->err.c_str());
+    if (c->poisoned)
+        return set_err(c, EG_ERR_STATE, "context is poisoned by an earlier CUDA/NCCL error: %s", c->err.c_str());
     c->have_graph = c->have_labels = c->graph_on_host = false;
     Problem P;
-    eg_status s = validate(c, d, f, device_field, &P);
-    if (s != EG_OK) return s;
+    ST(validate(c, d, f, device_field, &P));
     CK(cudaSetDevice(c->device));
     std::memset(&c->stats, 0, sizeof(c->stats));
     c->stats.n_vertices = P.N;
-    const int64_t n = P.v1 - P.v0;
-    c->n_own = n;
-    const int64_t words = (n + 31) / 32;
-    CK(c->ptr.ensure(sizeof(int32_t) * std::max<int64_t>(n, 1)));
-    CK(c->sad_bits.ensure(sizeof(uint32_t) * std::max<int64_t>(words, 1)));
-    CK(c->max_bits.ensure(sizeof(uint32_t) * std::max<int64_t>(words, 1)));
     CK(c->flags.ensure(sizeof(int) * 128));
-    CK(c->counts.ensure(sizeof(int64_t) * 16));
-    CK(c->halo_label.ensure(sizeof(int32_t) * 2));
+    CK(c->counts.ensure(sizeof(int64_t) * 16 * (c->world + 1)));
     CK(cudaMemsetAsync(c->flags.p, 0, sizeof(int) * 128, c->stream));
-    if (P.grid) {
-        s = ensure_table(c, P);
-        if (s != EG_OK) return s;
-    }
-    CK(cudaEventRecord(c->ev[0], c->stream));
-
-    const bool tiled = P.grid && P.ndim <= 3 && !(flags & EG_FORCE_GENERIC) && c->world == 1 && c->tiled != nullptr;
-    if (tiled) {
-        c->stats.path = 1;
-        CK(c->exit_bits.ensure(sizeof(uint32_t) * std::max<int64_t>(words, 1)));
-        s = tiled3d_labels(c->tiled, P.ndim, P.dims, f, c->ptr.as<int32_t>(), c->sad_bits.as<uint32_t>(),
-                           c->max_bits.as<uint32_t>(), c->flags.as<int>(), c->stream, &c->stats, &c->err,
-                           c->exit_bits.as<uint32_t>());
-        if (s != EG_OK) {
-            if (s == EG_ERR_CUDA) c->poisoned = true;
-            return s;
-        }
-        CK(cudaEventRecord(c->ev[1], c->stream));
-    } else {
-        c->stats.path = P.grid ? 0 : 2;
-        s = run_generic_labels(c, P, f);
-        if (s != EG_OK) return s;
-    }
-    CK(cudaEventRecord(c->ev[2], c->stream));
-    s = fail_if_flags(c);
-    if (s != EG_OK) return s;
-    c->d_labels = c->ptr.as<int32_t>();
-    c->have_labels = true;
-
-    s = run_graph(c, P, f, flags);
-    if (s != EG_OK) return s;
+    if (P.grid) ST(compute_grid(c, P, f, flags));
+    else ST(compute_csr(c, P, f, flags));
     if (!(flags & EG_NO_GRAPH_D2H)) {
-        s = graph_to_host(c, (flags & EG_RAW_ARCS) != 0);
-        if (s != EG_OK) return s;
+        ST(gather_graph(c, (flags & EG_RAW_ARCS) != 0));
         c->graph_on_host = true;
     }
     CK(cudaEventRecord(c->ev[5], c->stream));
     CK(cudaStreamSynchronize(c->stream));
     c->have_graph = true;
     c->stats.us_classify = ev_us(c->ev[0], c->ev[1]);
-    c->stats.us_jump = ev_us(c->ev[1], c->ev[2]);
+    c->stats.us_jump = 0;
+    c->stats.us_boundary = ev_us(c->ev[1], c->ev[2]);
     c->stats.us_label = 0;
     c->stats.us_arcs = ev_us(c->ev[2], c->ev[4]);
     c->stats.us_graph = ev_us(c->ev[4], c->ev[5]);
     c->stats.us_total = ev_us(c->ev[0], c->ev[5]);
+    c->stats.us_main = ev_us(c->ev_main[0], c->ev_main[1]);
     c->stats.bytes_alg = 8 * P.N + 4 * c->n_max + 5 * c->n_sad + 12 * c->n_arc +
-                         (P.grid ? 0 : 8 * (P.N + 1) + 4 * (P.row_ptr ? d->csr.nnz : 0));
+                         (P.grid ? 0 : 8 * (P.N + 1) + 4 * P.nnz);
     return EG_OK;
 }
 
@@ -507,8 +887,41 @@ eg_status eg_create(eg_ctx **out, int cuda_device, void *cuda_stream) {
             delete c;
             return EG_ERR_CUDA;
         }
-    c->tiled = tiled3d_create();
+    for (auto &e : c->ev_main)
+        if (cudaEventCreate(&e) != cudaSuccess) {
+            delete c;
+            return EG_ERR_CUDA;
+        }
     *out = c;
+    return EG_OK;
+}
+
+eg_status eg_nccl_unique_id(void *out128) {
+    if (!out128) return EG_ERR_INVALID_ARG;
+    ncclUniqueId id;
+    if (ncclGetUniqueId(&id) != ncclSuccess) return EG_ERR_NCCL;
+    static_assert(sizeof(id) == 128, "ncclUniqueId is 128 bytes");
+    std::memcpy(out128, &id, sizeof(id));
+    return EG_OK;
+}
+
+eg_status eg_create_dist(eg_ctx **out, int cuda_device, void *cuda_stream, const void *nccl_id128, int rank,
+                         int world) {
+    if (!out || !nccl_id128 || world < 1 || rank < 0 || rank >= world) return EG_ERR_INVALID_ARG;
+    eg_status s = eg_create(out, cuda_device, cuda_stream);
+    if (s != EG_OK) return s;
+    eg_ctx *c = *out;
+    c->rank = rank;
+    c->world = world;
+    if (world > 1) {
+        ncclUniqueId id;
+        std::memcpy(&id, nccl_id128, sizeof(id));
+        ncclResult_t r = ncclCommInitRank(&c->comm, world, id, rank);
+        if (r != ncclSuccess) {
+            set_err(c, EG_ERR_NCCL, "ncclCommInitRank: %s", ncclGetErrorString(r));
+            return EG_ERR_NCCL;       // the ctx stays valid for eg_last_error / eg_destroy
+        }
+    }
     return EG_OK;
 }
 
@@ -520,43 +933,37 @@ eg_status eg_compute_host(eg_ctx *c, const eg_domain *d, const float *h_field, i
     if (!c) return EG_ERR_INVALID_ARG;
     if (c->poisoned) return set_err(c, EG_ERR_STATE, "context is poisoned: %s", c->err.c_str());
     Problem P;
-    eg_status s = validate(c, d, h_field, false, &P);
-    if (s != EG_OK) return s;
+    ST(validate(c, d, h_field, false, &P));
     if (is_device_ptr(h_field)) return set_err(c, EG_ERR_INVALID_ARG, "eg_compute_host takes a host field");
     CK(cudaSetDevice(c->device));
-    int64_t nfield;
-    if (P.grid) {
-        nfield = (P.slab.z1 - P.slab.z0) * P.slab.plane;
-    } else {
-        nfield = P.N;
-    }
+    const int64_t nfield = P.grid ? (P.v1 - P.v0) : P.N;
     CK(c->field.ensure(sizeof(float) * std::max<int64_t>(nfield, 1)));
     cudaPointerAttributes a;
-    bool pinned = cudaPointerGetAttributes(&a, h_field) == cudaSuccess && a.type == cudaMemoryTypeHost;
+    const bool pinned = cudaPointerGetAttributes(&a, h_field) == cudaSuccess && a.type == cudaMemoryTypeHost;
     cudaGetLastError();
     if (pinned || nfield * 4 <= (int64_t(1) << 20)) {
         CK(cudaMemcpyAsync(c->field.p, h_field, sizeof(float) * nfield, cudaMemcpyHostToDevice, c->stream));
     } else {
+        // pageable source: stage through two pinned halves
         const size_t chunk = size_t(64) << 20;
         CK(c->h_stage.ensure(2 * chunk));
         char *stage = c->h_stage.as<char>();
         const char *src = reinterpret_cast<const char *>(h_field);
         char *dst = c->field.as<char>();
-        size_t total = sizeof(float) * size_t(nfield);
+        const size_t total = sizeof(float) * size_t(nfield);
+        cudaEvent_t done[2] = {c->ev[6], c->ev[7]};
+        bool used[2] = {false, false};
         int k = 0;
         for (size_t off = 0; off < total; off += chunk, k ^= 1) {
-            size_t len = std::min(chunk, total - off);
-            // the previous copy out of this half must be complete before reuse
-            CK(cudaStreamSynchronize(c->stream));
+            const size_t len = std::min(chunk, total - off);
+            if (used[k]) CK(cudaEventSynchronize(done[k]));
             std::memcpy(stage + k * chunk, src + off, len);
             CK(cudaMemcpyAsync(dst + off, stage + k * chunk, len, cudaMemcpyHostToDevice, c->stream));
+            CK(cudaEventRecord(done[k], c->stream));
+            used[k] = true;
         }
     }
-    if (!P.grid) {
-        // CSR: the field copy above is the full replicated field
-    }
-    s = compute_impl(c, d, c->field.as<float>(), flags, true);
-    if (s != EG_OK) return s;
+    ST(compute_impl(c, d, c->field.as<float>(), flags, true));
     if (h_labels) {
         CK(cudaMemcpyAsync(h_labels, c->d_labels, sizeof(int32_t) * c->n_own, cudaMemcpyDeviceToHost, c->stream));
         CK(cudaStreamSynchronize(c->stream));
@@ -567,25 +974,28 @@ eg_status eg_compute_host(eg_ctx *c, const eg_domain *d, const float *h_field, i
 eg_status eg_gradient(eg_ctx *c, const eg_domain *d, const float *d_field, int32_t *d_ptr, uint8_t *d_beta) {
     if (!c) return EG_ERR_INVALID_ARG;
     if (c->poisoned) return set_err(c, EG_ERR_STATE, "context is poisoned: %s", c->err.c_str());
+    if (c->world > 1) return set_err(c, EG_ERR_UNSUPPORTED, "eg_gradient is single-GPU");
     Problem P;
-    eg_status s = validate(c, d, d_field, true, &P);
-    if (s != EG_OK) return s;
+    ST(validate(c, d, d_field, true, &P));
     if (!is_device_ptr(d_ptr) || !is_device_ptr(d_beta))
         return set_err(c, EG_ERR_INVALID_ARG, "d_ptr / d_beta must be device pointers");
     CK(cudaSetDevice(c->device));
     const int64_t n = P.v1 - P.v0, words = (n + 31) / 32;
-    CK(c->sad_bits.ensure(sizeof(uint32_t) * std::max<int64_t>(words, 1)));
-    CK(c->max_bits.ensure(sizeof(uint32_t) * std::max<int64_t>(words, 1)));
+    set_slab_count(c, std::max<size_t>(c->slabs.size(), 1));
+    SlabState &S = *c->slabs[0];
+    CK(S.sad_bits.ensure(sizeof(uint32_t) * std::max<int64_t>(words, 1)));
+    CK(S.max_bits.ensure(sizeof(uint32_t) * std::max<int64_t>(words, 1)));
     CK(c->flags.ensure(sizeof(int) * 128));
     CK(cudaMemsetAsync(c->flags.p, 0, sizeof(int) * 128, c->stream));
     if (P.grid) {
-        s = ensure_table(c, P);
-        if (s != EG_OK) return s;
-        CK(launch_classify_grid(c->tab.as<LinkTable>(), P.ndim, d_field, P.slab, d_ptr, c->sad_bits.as<uint32_t>(),
-                                c->max_bits.as<uint32_t>(), d_beta, c->flags.as<int>(), c->stream));
+        ST(ensure_table(c, P));
+        const Slab s{0, P.D, P.plane, 0, P.N};
+        const FieldView F{d_field, nullptr, nullptr, 0, P.N, P.plane};
+        CK(launch_classify_grid(c->tab.as<LinkTable>(), P.ndim, F, s, d_ptr, S.sad_bits.as<uint32_t>(),
+                                S.max_bits.as<uint32_t>(), d_beta, c->flags.as<int>(), c->stream));
     } else {
-        CK(launch_classify_csr(P.row_ptr, P.col_idx, d_field, P.v0, P.v1, d_ptr, c->sad_bits.as<uint32_t>(),
-                               c->max_bits.as<uint32_t>(), d_beta, c->flags.as<int>(), c->flags.as<int>() + 1,
+        CK(launch_classify_csr(P.row_ptr, P.col_idx, d_field, P.v0, P.v1, d_ptr, S.sad_bits.as<uint32_t>(),
+                               S.max_bits.as<uint32_t>(), d_beta, c->flags.as<int>(), c->flags.as<int>() + 1,
                                c->stream));
     }
     return fail_if_flags(c);
@@ -636,17 +1046,17 @@ eg_status eg_destroy(eg_ctx *c) {
     if (!c) return EG_OK;
     cudaSetDevice(c->device);
     cudaStreamSynchronize(c->stream);
-    DevBuf *bufs[] = {&c->field, &c->ptr, &c->sad_bits, &c->max_bits, &c->exit_bits, &c->flags, &c->scratch, &c->counts,
-                      &c->maxima64, &c->saddles32, &c->saddles64, &c->sbeta, &c->slot_off, &c->tmp_m, &c->tmp_mult,
-                      &c->n_unique, &c->arc_off, &c->arc_s, &c->arc_m, &c->arc_mult, &c->raw_s, &c->raw_rep,
-                      &c->raw_m, &c->tab, &c->halo_label};
+    set_slab_count(c, 0);
+    DevBuf *bufs[] = {&c->label_all, &c->field, &c->flags, &c->counts, &c->scratch, &c->tab, &c->gsend, &c->grecv};
     for (DevBuf *b : bufs) b->release();
     HostBuf *hb[] = {&c->h_maxima, &c->h_saddles, &c->h_sbeta, &c->h_arc_s, &c->h_arc_m, &c->h_arc_mult,
                      &c->h_raw_s, &c->h_raw_rep, &c->h_raw_m, &c->h_counts, &c->h_stage};
     for (HostBuf *b : hb) b->release();
     for (auto &e : c->ev)
         if (e) cudaEventDestroy(e);
-    tiled3d_destroy(c->tiled);
+    for (auto &e : c->ev_main)
+        if (e) cudaEventDestroy(e);
+    if (c->comm) ncclCommDestroy(c->comm);
     delete c;
     return EG_OK;
 }
@@ -654,17 +1064,6 @@ eg_status eg_destroy(eg_ctx *c) {
 const char *eg_last_error(const eg_ctx *c) {
     if (!c) return "null context";
     return c->err.c_str();
-}
-
-eg_status eg_nccl_unique_id(void *out128) {
-    (void)out128;
-    return EG_ERR_UNSUPPORTED;
-}
-
-eg_status eg_create_dist(eg_ctx **out, int cuda_device, void *cuda_stream, const void *nccl_id128, int rank,
-                         int world) {
-    (void)out; (void)cuda_device; (void)cuda_stream; (void)nccl_id128; (void)rank; (void)world;
-    return EG_ERR_UNSUPPORTED;
 }
 
 }  // extern "C"

@@ -14,6 +14,7 @@ namespace eg {
 constexpr int kMaxDim = 6;                 // generic grid kernels: n <= 6
 constexpr int kMaxLink = 126;              // 2 (2^6 - 1)
 constexpr int kCsrMaxDeg = 128;            // thread-per-vertex CSR kernel
+constexpr uint32_t kUnresolved = 0x80000000u;   // label bit 31: not final, low bits = a vertex further on the path
 
 // Freudenthal link of an interior vertex: the offsets d in
 // {-1,0,1}^n \ 0 whose non-zero entries share one sign, i.e. the difference
@@ -35,15 +36,44 @@ LinkTable make_link_table(int ndim, const int64_t *dims);
 // beta0+ for every 14-bit upper mask of the 3-D link (n = 3, K = 14).
 std::vector<uint8_t> make_beta_lut3(const LinkTable &t);
 
-// A slab of the grid as seen by one rank (or one virtual partition).
-// Owned vertices: global ids [v0, v1) = planes [z0, z1) of the slowest axis.
-// The local field buffer holds planes [h0, h1) = owned planes plus a
-// one-plane halo on each side that exists (P:281 ghost vertices).
+// A slab of the grid as seen by one rank (or one virtual partition): the
+// planes [z0, z1) of the slowest axis ("blocks ... along the z-axis"),
+// i.e. the global ids [v0, v1).  One GPU = one slab covering the grid.
 struct Slab {
-    int64_t z0, z1, h0, h1;
+    int64_t z0, z1;
     int64_t plane;                         // vertices per plane of the slowest axis
     int64_t v0, v1;                        // owned global ids
-    int64_t base;                          // global id of local element 0 = h0 * plane
+};
+
+// Field values visible to a slab: the owned planes plus the one-plane halo on
+// each side that exists ("ghost vertices"), fetched from the
+// neighbours.  Grids only; on one GPU lo = hi = null and own = the field.
+struct FieldView {
+    const float *own, *lo, *hi;
+    int64_t v0, v1, plane;
+#ifdef __CUDACC__
+    __device__ __forceinline__ float at(int64_t g) const {
+        if (g >= v0 && g < v1) return __ldg(own + (g - v0));
+        if (g < v0) return __ldg(lo + (g - v0 + plane));
+        return __ldg(hi + (g - v1));
+    }
+#endif
+};
+
+// Labels visible to a slab: the owned labels plus the (final) labels of the
+// halo planes received in the boundary exchange.  CSR: own = every vertex.
+struct LabelView {
+    const int32_t *own;
+    int64_t v0, v1;
+    const int32_t *lo, *hi;                // halo planes z0 - 1 and z1 (grid, multi-slab) or null
+    int64_t plane;
+#ifdef __CUDACC__
+    __device__ __forceinline__ int32_t at(int64_t g) const {
+        if (g >= v0 && g < v1) return own[g - v0];
+        if (g < v0) return lo[g - v0 + plane];
+        return hi[g - v1];
+    }
+#endif
 };
 
 // --------------------------------------------------------------- kernels
@@ -51,39 +81,31 @@ struct Slab {
 
 // S1 + S3, generic n: ptr[i] (global id) for owned i, saddle / maximum bits
 // (bit i of word i/32), optional beta0+ per vertex.
-cudaError_t launch_classify_grid(const LinkTable *d_tab, int ndim, const float *f_local, const Slab &s,
-                                 int32_t *ptr, uint32_t *sad_bits, uint32_t *max_bits, uint8_t *beta_out,
-                                 int *nan_flag, cudaStream_t st);
+cudaError_t launch_classify_grid(const LinkTable *d_tab, int ndim, FieldView F, const Slab &s, int32_t *ptr,
+                                 uint32_t *sad_bits, uint32_t *max_bits, uint8_t *beta_out, int *nan_flag,
+                                 cudaStream_t st);
 cudaError_t launch_classify_csr(const int64_t *row_ptr, const int32_t *col_idx, const float *f, int64_t v0,
                                 int64_t v1, int32_t *ptr, uint32_t *sad_bits, uint32_t *max_bits,
                                 uint8_t *beta_out, int *nan_flag, int *deg_overflow, cudaStream_t st);
 
 // S2: in-place pointer jumping over ptr[0..n) whose entries are global ids;
-// entries outside [v0, v1) are terminal (remote).  changed[r] is set when
+// entries outside [v0, v0 + n) are terminal (remote).  changed[r] is set when
 // round r modified something; round r exits immediately if round r-1 did not.
 cudaError_t launch_jump_round(int32_t *ptr, int64_t n, int64_t v0, int *changed, int round, cudaStream_t st);
 
 // Compaction of a bitmap over owned indices [0, n) into ascending global ids
-// (v0 + i) as int32 and int64.  Needs a scratch of compact_scratch_words(n).
+// (v0 + i) as int32 and int64.
 size_t compact_scratch_bytes(int64_t n);
 cudaError_t launch_compact_bits(const uint32_t *bits, int64_t n, int64_t v0, void *scratch, int32_t *out32,
                                 int64_t *out64, int64_t *d_count, cudaStream_t st);
+cudaError_t launch_count_bits(const uint32_t *bits, int64_t n, void *scratch, int64_t *d_count, cudaStream_t st);
 
-// S4 for grids and CSR.  Label lookup: label[g - v0] for owned g, else
-// halo_label[g - halo_lo_base] for the lower halo plane or
-// halo_label[plane + g - halo_hi_base] for the upper halo plane.
-struct LabelView {
-    const int32_t *own;
-    int64_t v0, v1;
-    const int32_t *halo;                   // [2 * plane] or null
-    int64_t lo_base, hi_base, plane;       // global id of the first vertex of each halo plane
-};
-cudaError_t launch_saddle_beta_grid(const LinkTable *d_tab, int ndim, const float *f_local, const Slab &s,
-                                    const int32_t *saddles, int64_t n_sad, int32_t *beta, cudaStream_t st);
-cudaError_t launch_arcs_grid(const LinkTable *d_tab, int ndim, const float *f_local, const Slab &s,
-                             const int32_t *saddles, int64_t n_sad, const int64_t *slot_off, LabelView lv,
-                             int32_t *tmp_m, int32_t *tmp_mult, int32_t *n_unique, int64_t *raw_s, int64_t *raw_rep,
-                             int64_t *raw_m, cudaStream_t st);
+// S4 for grids and CSR.
+cudaError_t launch_saddle_beta_grid(const LinkTable *d_tab, int ndim, FieldView F, const int32_t *saddles,
+                                    int64_t n_sad, int32_t *beta, cudaStream_t st);
+cudaError_t launch_arcs_grid(const LinkTable *d_tab, int ndim, FieldView F, const int32_t *saddles, int64_t n_sad,
+                             const int64_t *slot_off, LabelView lv, int32_t *tmp_m, int32_t *tmp_mult,
+                             int32_t *n_unique, int64_t *raw_s, int64_t *raw_rep, int64_t *raw_m, cudaStream_t st);
 cudaError_t launch_saddle_beta_csr(const int64_t *row_ptr, const int32_t *col_idx, const float *f,
                                    const int32_t *saddles, int64_t n_sad, int32_t *beta, cudaStream_t st);
 cudaError_t launch_arcs_csr(const int64_t *row_ptr, const int32_t *col_idx, const float *f, const int32_t *saddles,
@@ -97,9 +119,27 @@ cudaError_t launch_emit_arcs(const int32_t *saddles, int64_t n_sad, const int64_
 size_t scan_scratch_bytes(int64_t n);
 cudaError_t launch_scan_i32(const int32_t *in, int64_t *out, int64_t n, void *scratch, size_t scratch_bytes,
                             cudaStream_t st);
-cudaError_t launch_i32_to_i64(const int32_t *in, int64_t *out, int64_t n, cudaStream_t st);
-cudaError_t launch_nan_scan(const float *f, int64_t n, int *flag, cudaStream_t st);
 
-// --- tiled 3-D path (n <= 3), see k_grid3d.cu
-struct Tiled3D;
+// ------------------------------------------------ cross-slab label resolution
+// (k_slab.cu; the paper's partial paths P:296 become "exit
+// pointers" into the neighbours' boundary planes)
+//
+// Label convention inside a slab after the local phase: label >= 0 is final
+// (a maximum); label = kUnresolved | x means "the path continues at x", where
+// x is either an owned vertex whose own label is (locally) final-or-remote,
+// or a vertex of a halo plane (remote).
+
+// generic path: after local pointer jumping, mark remote targets unresolved
+cudaError_t launch_flag_remote(int32_t *label, int64_t n, int64_t v0, cudaStream_t st);
+// bval[0..plane) = resolved-as-far-as-possible values of plane z0, bval[plane..2 plane) of plane z1 - 1
+cudaError_t launch_bval_init(const int32_t *label, const Slab &s, int32_t *bval, cudaStream_t st);
+// one exchange round: bval entries pointing into a halo plane take the
+// neighbour's value (hval lo = plane z0 - 1, hi = plane z1); counts unresolved
+cudaError_t launch_bval_update(int32_t *bval, const int32_t *hval_lo, const int32_t *hval_hi, const Slab &s,
+                               unsigned long long *unresolved, cudaStream_t st);
+// final pass: every unresolved owned label (all owned vertices, or only those
+// whose bit is set in `bits`) becomes final, via owned labels and the final
+// halo-plane values
+cudaError_t launch_finalize(int32_t *label, const uint32_t *bits, int64_t v0, int64_t v1, const int32_t *hval_lo,
+                            const int32_t *hval_hi, int64_t plane, cudaStream_t st);
 }  // namespace eg

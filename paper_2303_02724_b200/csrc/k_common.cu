@@ -127,6 +127,24 @@ cudaError_t launch_compact_bits(const uint32_t *bits, int64_t n, int64_t v0, voi
     return cudaMemcpyAsync(d_count, off + chunks, sizeof(int64_t), cudaMemcpyDeviceToDevice, st);
 }
 
+cudaError_t launch_count_bits(const uint32_t *bits, int64_t n, void *scratch, int64_t *d_count, cudaStream_t st) {
+    const int64_t words = (n + 31) / 32;
+    const int64_t chunks = (words + kCompactBS - 1) / kCompactBS;
+    if (n <= 0) return cudaMemsetAsync(d_count, 0, sizeof(int64_t), st);
+    char *p = static_cast<char *>(scratch);
+    int32_t *cnt = reinterpret_cast<int32_t *>(p);
+    p += (size_t(chunks) * 4 + 15) / 16 * 16 + 16;
+    int64_t *off = reinterpret_cast<int64_t *>(p);
+    p += (size_t(chunks + 1) * 8 + 15) / 16 * 16 + 16;
+    const size_t sb = scan_scratch_bytes(chunks);
+    k_count_bits<<<unsigned(chunks), kCompactBS, 0, st>>>(bits, words, cnt);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    e = launch_scan_i32(cnt, off, chunks, p, sb, st);
+    if (e != cudaSuccess) return e;
+    return cudaMemcpyAsync(d_count, off + chunks, sizeof(int64_t), cudaMemcpyDeviceToDevice, st);
+}
+
 // ------------------------------------------------------------ arc emission
 __global__ void k_emit_arcs(const int32_t *__restrict__ saddles, int64_t n_sad, const int64_t *__restrict__ slot_off,
                             const int64_t *__restrict__ arc_off, const int32_t *__restrict__ tmp_m,

@@ -67,8 +67,8 @@ __device__ __forceinline__ void load_tables(GridSmem<NDIM> &S, const LinkTable *
 // equal values (simulated perturbation, reading L1).  Returns the mask; *best
 // is the gradient (v for a maximum).
 template <int NDIM>
-__device__ __forceinline__ Bits<GridSmem<NDIM>::NW> upper_link(const GridSmem<NDIM> &S, const float *__restrict__ f,
-                                                               int64_t base, int64_t v, float fv, int64_t *best) {
+__device__ __forceinline__ Bits<GridSmem<NDIM>::NW> upper_link(const GridSmem<NDIM> &S, const FieldView &F, int64_t v,
+                                                               float fv, int64_t *best) {
     constexpr int K = GridSmem<NDIM>::K;
     int32_t c[NDIM];
     int64_t r = v;
@@ -91,7 +91,7 @@ __device__ __forceinline__ Bits<GridSmem<NDIM>::NW> upper_link(const GridSmem<ND
         }
         if (!ok) continue;
         int64_t u = v + S.delta[k];
-        float fu = __ldg(f + (u - base));
+        float fu = F.at(u);
         bool up = S.delta[k] > 0 ? (fu >= fv) : (fu > fv);
         if (up) {
             m.set(k);
@@ -109,8 +109,8 @@ __device__ __forceinline__ Bits<GridSmem<NDIM>::NW> upper_link(const GridSmem<ND
 // the constant link adjacency.  If reps != null, also the highest vertex of
 // every component (UpperLinkRep), in component order.
 template <int NDIM>
-__device__ __forceinline__ int components(const GridSmem<NDIM> &S, Bits<GridSmem<NDIM>::NW> rem,
-                                          const float *__restrict__ f, int64_t base, int64_t v, int32_t *reps) {
+__device__ __forceinline__ int components(const GridSmem<NDIM> &S, Bits<GridSmem<NDIM>::NW> rem, const FieldView &F,
+                                          int64_t v, int32_t *reps) {
     constexpr int NW = GridSmem<NDIM>::NW;
     int beta = 0;
     while (rem.any()) {
@@ -124,7 +124,7 @@ __device__ __forceinline__ int components(const GridSmem<NDIM> &S, Bits<GridSmem
         while ((k = front.pop_lowest()) >= 0) {
             if (reps) {
                 int64_t u = v + S.delta[k];
-                float fu = __ldg(f + (u - base));
+                float fu = F.at(u);
                 if (rep < 0 || fu > rf || (fu == rf && u > rep)) {
                     rep = u;
                     rf = fu;
@@ -144,8 +144,8 @@ __device__ __forceinline__ int components(const GridSmem<NDIM> &S, Bits<GridSmem
 }
 
 template <int NDIM>
-__global__ void __launch_bounds__(256) k_classify_grid(const LinkTable *__restrict__ tab,
-                                                       const float *__restrict__ f, Slab s, int32_t *ptr,
+__global__ void __launch_bounds__(256) k_classify_grid(const LinkTable *__restrict__ tab, FieldView F, Slab s,
+                                                       int32_t *ptr,
                                                        uint32_t *sad_bits, uint32_t *max_bits, uint8_t *beta_out,
                                                        int *nan_flag) {
     __shared__ GridSmem<NDIM> S;
@@ -156,12 +156,12 @@ __global__ void __launch_bounds__(256) k_classify_grid(const LinkTable *__restri
     bool is_sad = false, is_max = false;
     if (active) {
         const int64_t v = s.v0 + i;
-        const float fv = __ldg(f + (v - s.base));
+        const float fv = F.at(v);
         if (fv != fv) atomicOr(nan_flag, 1);
         int64_t best;
-        auto m = upper_link<NDIM>(S, f, s.base, v, fv, &best);
+        auto m = upper_link<NDIM>(S, F, v, fv, &best);
         is_max = !m.any();
-        int beta = is_max ? 0 : components<NDIM>(S, m, f, s.base, v, nullptr);
+        int beta = is_max ? 0 : components<NDIM>(S, m, F, v, nullptr);
         is_sad = beta >= 2;
         ptr[i] = int32_t(best);
         if (beta_out) beta_out[i] = uint8_t(beta > 255 ? 255 : beta);
@@ -175,8 +175,7 @@ __global__ void __launch_bounds__(256) k_classify_grid(const LinkTable *__restri
 }
 
 template <int NDIM>
-__global__ void __launch_bounds__(256) k_saddle_beta_grid(const LinkTable *__restrict__ tab,
-                                                          const float *__restrict__ f, Slab s,
+__global__ void __launch_bounds__(256) k_saddle_beta_grid(const LinkTable *__restrict__ tab, FieldView F,
                                                           const int32_t *__restrict__ saddles, int64_t n_sad,
                                                           int32_t *beta) {
     __shared__ GridSmem<NDIM> S;
@@ -184,17 +183,12 @@ __global__ void __launch_bounds__(256) k_saddle_beta_grid(const LinkTable *__res
     const int64_t j = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (j >= n_sad) return;
     const int64_t v = saddles[j];
-    const float fv = __ldg(f + (v - s.base));
+    const float fv = F.at(v);
     int64_t best;
-    auto m = upper_link<NDIM>(S, f, s.base, v, fv, &best);
-    beta[j] = components<NDIM>(S, m, f, s.base, v, nullptr);
+    auto m = upper_link<NDIM>(S, F, v, fv, &best);
+    beta[j] = components<NDIM>(S, m, F, v, nullptr);
 }
 
-__device__ __forceinline__ int32_t label_of(const LabelView &lv, int64_t g) {
-    if (g >= lv.v0 && g < lv.v1) return lv.own[g - lv.v0];
-    if (g >= lv.lo_base && g < lv.lo_base + lv.plane) return lv.halo[g - lv.lo_base];
-    return lv.halo[lv.plane + (g - lv.hi_base)];
-}
 
 // Per saddle: for every component, m = label[rep]; sort the (<= K) m values
 // and reduce to unique (m, multiplicity) (reading L7).  Writes into the
@@ -235,8 +229,8 @@ __device__ __forceinline__ void sort_reps(int32_t *reps, int b) {
 }
 
 template <int NDIM>
-__global__ void __launch_bounds__(128) k_arcs_grid(const LinkTable *__restrict__ tab, const float *__restrict__ f,
-                                                   Slab s, const int32_t *__restrict__ saddles, int64_t n_sad,
+__global__ void __launch_bounds__(128) k_arcs_grid(const LinkTable *__restrict__ tab, FieldView F,
+                                                   const int32_t *__restrict__ saddles, int64_t n_sad,
                                                    const int64_t *__restrict__ slot_off, LabelView lv,
                                                    int32_t *tmp_m, int32_t *tmp_mult, int32_t *n_unique,
                                                    int64_t *raw_s, int64_t *raw_rep, int64_t *raw_m) {
@@ -247,15 +241,15 @@ __global__ void __launch_bounds__(128) k_arcs_grid(const LinkTable *__restrict__
     constexpr int K = GridSmem<NDIM>::K;
     int32_t reps[K];
     const int64_t v = saddles[j];
-    const float fv = __ldg(f + (v - s.base));
+    const float fv = F.at(v);
     int64_t best;
-    auto m = upper_link<NDIM>(S, f, s.base, v, fv, &best);
-    int b = components<NDIM>(S, m, f, s.base, v, reps);
+    auto m = upper_link<NDIM>(S, F, v, fv, &best);
+    int b = components<NDIM>(S, m, F, v, reps);
     sort_reps(reps, b);
     const int64_t off = slot_off[j];
     int32_t ms[K];
     for (int c = 0; c < b; ++c) {
-        ms[c] = label_of(lv, reps[c]);
+        ms[c] = lv.at(reps[c]);
         if (raw_s) {
             raw_s[off + c] = v;
             raw_rep[off + c] = reps[c];
@@ -278,33 +272,33 @@ __global__ void __launch_bounds__(128) k_arcs_grid(const LinkTable *__restrict__
 
 static inline unsigned blocks_for(int64_t n, int bs) { return unsigned((n + bs - 1) / bs); }
 
-cudaError_t launch_classify_grid(const LinkTable *d_tab, int ndim, const float *f_local, const Slab &s,
-                                 int32_t *ptr, uint32_t *sad_bits, uint32_t *max_bits, uint8_t *beta_out,
-                                 int *nan_flag, cudaStream_t st) {
+cudaError_t launch_classify_grid(const LinkTable *d_tab, int ndim, FieldView F, const Slab &s, int32_t *ptr,
+                                 uint32_t *sad_bits, uint32_t *max_bits, uint8_t *beta_out, int *nan_flag,
+                                 cudaStream_t st) {
     const int64_t n = s.v1 - s.v0;
     if (n <= 0) return cudaSuccess;
-#define CALL(D) k_classify_grid<D><<<blocks_for(n, 256), 256, 0, st>>>(d_tab, f_local, s, ptr, sad_bits, max_bits, beta_out, nan_flag)
+#define CALL(D) k_classify_grid<D><<<blocks_for(n, 256), 256, 0, st>>>(d_tab, F, s, ptr, sad_bits, max_bits, beta_out, nan_flag)
     EG_DISPATCH_NDIM(ndim, CALL)
 #undef CALL
     return cudaGetLastError();
 }
 
-cudaError_t launch_saddle_beta_grid(const LinkTable *d_tab, int ndim, const float *f_local, const Slab &s,
-                                    const int32_t *saddles, int64_t n_sad, int32_t *beta, cudaStream_t st) {
+cudaError_t launch_saddle_beta_grid(const LinkTable *d_tab, int ndim, FieldView F, const int32_t *saddles,
+                                    int64_t n_sad, int32_t *beta, cudaStream_t st) {
     if (n_sad <= 0) return cudaSuccess;
-#define CALL(D) k_saddle_beta_grid<D><<<blocks_for(n_sad, 256), 256, 0, st>>>(d_tab, f_local, s, saddles, n_sad, beta)
+#define CALL(D) k_saddle_beta_grid<D><<<blocks_for(n_sad, 256), 256, 0, st>>>(d_tab, F, saddles, n_sad, beta)
     EG_DISPATCH_NDIM(ndim, CALL)
 #undef CALL
     return cudaGetLastError();
 }
 
-cudaError_t launch_arcs_grid(const LinkTable *d_tab, int ndim, const float *f_local, const Slab &s,
-                             const int32_t *saddles, int64_t n_sad, const int64_t *slot_off, LabelView lv,
+cudaError_t launch_arcs_grid(const LinkTable *d_tab, int ndim, FieldView F, const int32_t *saddles, int64_t n_sad,
+                             const int64_t *slot_off, LabelView lv,
                              int32_t *tmp_m, int32_t *tmp_mult, int32_t *n_unique, int64_t *raw_s, int64_t *raw_rep,
                              int64_t *raw_m, cudaStream_t st) {
     if (n_sad <= 0) return cudaSuccess;
 #define CALL(D)                                                                                            \
-    k_arcs_grid<D><<<blocks_for(n_sad, 128), 128, 0, st>>>(d_tab, f_local, s, saddles, n_sad, slot_off, lv, \
+    k_arcs_grid<D><<<blocks_for(n_sad, 128), 128, 0, st>>>(d_tab, F, saddles, n_sad, slot_off, lv, \
                                                            tmp_m, tmp_mult, n_unique, raw_s, raw_rep, raw_m)
     EG_DISPATCH_NDIM(ndim, CALL)
 #undef CALL

@@ -1,40 +1,66 @@
 // Tiled path for n <= 3 grids (2-D and 1-D grids are 3-D grids with unit
 // axes: the Freudenthal link of a 2-D vertex is exactly the dz = 0 part of the
-// 3-D link).
+// 3-D link, Fig. 2).
 //
-// Pass T  (k_tile): one CTA per 32 x 16 x 16 tile.  The tile plus a one-vertex
-//         halo is staged in shared memory; every thread walks one z-column,
-//         keeping the 2-D stars of three planes in registers, and computes
-//           S1  the gradient (SoS argmax of the closed star),
-//           S3  the 14-bit upper mask -> beta0+ from a 16 KB LUT.
-//         The gradient of every tile vertex is then stored as a 16-bit index
-//         into the halo box and chased in shared memory to its local root
-//         (S2 inside the tile): an in-tile maximum (final label) or the first
-//         halo vertex on the path (an "exit": the path leaves the tile, the
-//         paper's partial path P:296).  The kernel writes label[v] = global id
-//         of that root, and bit v of the exit / saddle / maximum bitmaps.
-// Pass X  (k_exit_fixup): for every exiting vertex, follow label[] through
-//         the exit bitmap (tile hop by tile hop) to the maximum and store it.
-//         In-place and race-benign: every value ever stored on a chain is a
-//         later vertex of the same ascending path.
+// Pass T  (k_tile): one CTA per 32 x 16 x 16 tile (2 CTAs per SM).  The tile
+//         plus a one-vertex halo ("ghost vertices") is brought into
+//         shared memory by one TMA bulk-tensor copy; every thread walks one
+//         z-column and computes, per vertex,
+//           S1  the gradient = SoS argmax of the closed star,
+//               separably: closed star = box(v) u box(v - 1), box(w) = w + {0,1}^3,
+//               so the argmax is 2x2 in-plane maxima combined across z;
+//           S3  the 14-bit upper mask -> "beta0+ >= 2" from a 2 KB bit LUT
+//               (Table 1; maximum iff the mask is empty).
+//         The gradients are stored as 16-bit indices into the halo box and
+//         compressed by pointer doubling in shared memory (S2 inside the tile):
+//         every vertex ends at an in-tile maximum (its final label) or at the
+//         first halo vertex on its path (an exit: the path leaves the tile, the
+//         paper's partial path P:296).  label[v] = global id of that root, with
+//         bit 31 set for exits; the distinct exit targets of the tile are
+//         appended to a list E.
+// Pass E  (k_resolve_exits): for every e in E, follow label[] (one dependent
+//         load per tile hop) to the maximum and store it in label[e].
+// Pass X  (k_exit_final): every exiting vertex takes label[label[v]] (its exit
+//         target is in E, hence final).
+// All in-place updates are race-benign: every value ever stored on a chain is
+// a later vertex of the same ascending path.
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <cstdio>
+#include <cstring>
+#include <vector>
 
 #include "eg_tiled.h"
 
 namespace eg {
 
 constexpr int TX = 32, TY = 16, TZ = 16;
-constexpr int BX = TX + 2, BY = TY + 2, BZ = TZ + 2;
-constexpr int BOX = BX * BY * BZ;                    // 11016 < 65536: 16-bit box indices
-constexpr int kThreads = TX * TY;                   // one z-column per thread
-constexpr int kLut = 1 << 14;
-constexpr size_t kTileSmem = 6 * BOX + kLut;        // 82,480 B -> 2 CTAs per SM
+constexpr int XO = 4;                                // box x index of the tile's first column
+constexpr int BX = TX + 2 * XO;                      // 40: TMA box starts at x0 - 4 (16-byte aligned start)
+constexpr int BY = TY + 2, BZ = TZ + 2;
+constexpr int PL = BX * BY;
+constexpr int BOX = PL * BZ;                         // 11664 < 65536: 16-bit box indices
+constexpr int kThreads = TX * TY;                    // one z-column per thread
+constexpr int kLutWords = (1 << 14) / 32;            // 1 bit per 14-bit upper mask: beta0+ >= 2
+constexpr uint32_t kFlag = 0x80000000u;              // label bit 31: exit (not yet final)
+constexpr int kFboxSlack = XO + BX + PL;             // shifted TMA boxes spill this far past the box
+constexpr size_t kOffP = size_t(BOX + kFboxSlack) * 4;  // pbox after fbox
+constexpr size_t kOffL = kOffP + size_t(BOX) * 2;    // lut bits
+constexpr size_t kOffM = kOffL + size_t(kLutWords) * 4;
+constexpr size_t kTileSmem = kOffM + 16 + 33 * 4 + 16; // ~78 KB -> 2 CTAs per SM (register-limited)
 
 struct Tiled3D {
-    uint8_t *d_lut = nullptr;
-    bool lut_ready = false;
+    uint32_t *d_lut = nullptr;
+    bool ready = false;
+    int64_t bdims[3] = {0, 0, 0};
+    int64_t bz[2] = {-1, -1};                        // slab planes of the cached list
+    int32_t *d_btiles = nullptr;                     // boundary tile list for the cached dims
+    int64_t n_btiles = 0;
+    int32_t *d_elist = nullptr;                      // exit targets E
+    int64_t ecap = 0;
+    unsigned long long *d_ecount = nullptr;
+    void *encode = nullptr;                          // cuTensorMapEncodeTiled
 };
 
 Tiled3D *tiled3d_create() { return new Tiled3D(); }
@@ -42,217 +68,458 @@ Tiled3D *tiled3d_create() { return new Tiled3D(); }
 void tiled3d_destroy(Tiled3D *t) {
     if (!t) return;
     if (t->d_lut) cudaFree(t->d_lut);
+    if (t->d_btiles) cudaFree(t->d_btiles);
+    if (t->d_elist) cudaFree(t->d_elist);
+    if (t->d_ecount) cudaFree(t->d_ecount);
     delete t;
 }
 
 struct Dims3 {
     int32_t nx, ny, nz;
-    int64_t nxy;
 };
 
-__device__ __forceinline__ int bidx(int x, int y, int z) { return (z * BY + y) * BX + x; }  // x, y, z in box coords
+struct TileArgs {
+    const float *f;                 // owned planes [z_lo, z_hi) of the slab
+    const float *f_lo, *f_hi;       // halo planes z_lo - 1 and z_hi (neighbour slabs) or null
+    int32_t z_lo, z_hi;
+    int64_t v0;                     // global id of the first owned vertex
+    int32_t *label;                 // owned labels (index v - v0)
+    uint32_t *exit_bits, *sad_bits, *max_bits;
+    int *nan_flag;
+    int32_t *elist;
+    unsigned long long *ecount;
+    int64_t ecap;
+    const uint32_t *lut;
+    const int32_t *btiles;          // boundary variant: packed tile ids
+    int32_t tiles_x, tiles_y;       // interior variant: sub-box extents
+    int3 origin;                    // interior variant: first interior tile
+};
 
-// The 14 link offsets of a 3-D vertex in ascending global index (lexicographic
-// in (dz, dy, dx)):
-//   lower group (index < v): (-1,-1,-1) (0,-1,-1) (-1,0,-1) (0,0,-1) (-1,-1,0) (0,-1,0) (-1,0,0)
-//   upper group (index > v): (1,0,0) (0,1,0) (1,1,0) (0,0,1) (1,0,1) (0,1,1) (1,1,1)
-// Bit k of the upper mask follows this order (lower group bits 0..6, upper 7..13),
-// which is the order of LinkTable for dims >= 2 -- the LUT is built from it.
-template <bool kInterior>
-__global__ void __launch_bounds__(kThreads, 2) k_tile(const float *__restrict__ f, Dims3 D,
-                                                      const uint8_t *__restrict__ lut_g, int32_t *__restrict__ label,
-                                                      uint32_t *exit_bits, uint32_t *sad_bits, uint32_t *max_bits,
-                                                      int *nan_flag, int tiles_x, int tiles_y, int3 origin,
-                                                      int3 skip_lo, int3 skip_hi) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    float *fbox = reinterpret_cast<float *>(smem_raw);                       // BOX floats
-    uint16_t *pbox = reinterpret_cast<uint16_t *>(smem_raw + 4 * BOX);      // BOX uint16
-    uint8_t *lut = smem_raw + 6 * BOX;                                        // 16 KB
+__device__ __forceinline__ int bidx(int x, int y, int z) { return (z * BY + y) * BX + x; }
+
+// The halo shell of a tile box (cells a path can exit to): the two z faces
+// (BY rows of TX + 2 columns), the two y faces of the inner planes, and the two
+// x columns of the inner rows.
+constexpr int kShellW = TX + 2;
+constexpr int kShellZ = 2 * BY * kShellW;
+constexpr int kShellY = kShellZ + (BZ - 2) * 2 * kShellW;
+constexpr int kShell = kShellY + (BZ - 2) * (BY - 2) * 2;
+__device__ __forceinline__ int shell_cell(int s) {
+    int bx, by, bz;
+    if (s < kShellZ) {
+        bz = s < BY * kShellW ? 0 : BZ - 1;
+        const int t = s % (BY * kShellW);
+        by = t / kShellW;
+        bx = XO - 1 + t % kShellW;
+    } else if (s < kShellY) {
+        const int t = s - kShellZ;
+        bz = 1 + t / (2 * kShellW);
+        const int u = t % (2 * kShellW);
+        by = u < kShellW ? 0 : BY - 1;
+        bx = XO - 1 + u % kShellW;
+    } else {
+        const int t = s - kShellY;
+        bz = 1 + t / (2 * (BY - 2));
+        const int u = t % (2 * (BY - 2));
+        by = 1 + (u >> 1);
+        bx = (u & 1) ? XO + TX : XO - 1;
+    }
+    return bidx(bx, by, bz);
+}
+
+// ------------------------------------------------------------ TMA helpers
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t phase) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "LAB_WAIT:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra LAB_WAIT;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(phase)
+        : "memory");
+}
+
+__device__ __forceinline__ void tma_load_3d(void *dst, const CUtensorMap *map, uint64_t *bar, int x, int y, int z) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];"
+        ::"r"(smem_u32(dst)), "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar))
+        : "memory");
+}
+
+// ------------------------------------------------------------ the tile kernel
+
+struct VK {           // a value with its box-index offset from the centre vertex
+    float v;
+    int d;
+};
+
+// b wins ties: b is the later (higher-index) operand
+__device__ __forceinline__ VK vmax(VK a, VK b) { return b.v >= a.v ? b : a; }
+
+// IEEE compares (no ftz: distinct denormals stay distinct, reading L2)
+__device__ __forceinline__ uint32_t setgt(float a, float b) {
+    uint32_t r;
+    asm("set.gt.u32.f32 %0, %1, %2;" : "=r"(r) : "f"(a), "f"(b));
+    return r;
+}
+__device__ __forceinline__ uint32_t setge(float a, float b) {
+    uint32_t r;
+    asm("set.ge.u32.f32 %0, %1, %2;" : "=r"(r) : "f"(a), "f"(b));
+    return r;
+}
+
+template <bool kInterior, bool kTma>
+__global__ void __launch_bounds__(kThreads, 2)
+    k_tile(const __grid_constant__ CUtensorMap tmap, TileArgs A, Dims3 D) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    float *fbox = reinterpret_cast<float *>(smem);
+    uint16_t *pbox = reinterpret_cast<uint16_t *>(smem + kOffP);
+    uint32_t *lut = reinterpret_cast<uint32_t *>(smem + kOffL);
+    uint64_t *bar = reinterpret_cast<uint64_t *>(smem + kOffM);
 
     const int tid = threadIdx.x;
     const int tx = tid & 31, ty = tid >> 5;
-    int t = blockIdx.x;
-    const int bxi = t % tiles_x;
-    t /= tiles_x;
-    const int byi = t % tiles_y + origin.y;
-    const int bzi = t / tiles_y + origin.z;
-    const int bxo = bxi + origin.x;
-    // the checked variant skips the interior sub-box (launched separately)
-    if (!kInterior && bxo >= skip_lo.x && bxo <= skip_hi.x && byi >= skip_lo.y && byi <= skip_hi.y &&
-        bzi >= skip_lo.z && bzi <= skip_hi.z)
-        return;
-    const int x0 = bxo * TX, y0 = byi * TY, z0 = bzi * TZ;
-
-    // ---- stage the tile + halo (and the LUT) in shared memory; halo cells of
-    // the pointer box point to themselves (terminal: the path leaves the tile)
-    for (int i = tid; i < kLut / 16; i += kThreads)
-        reinterpret_cast<uint4 *>(lut)[i] = __ldg(reinterpret_cast<const uint4 *>(lut_g) + i);
-    for (int i = tid; i < BOX; i += kThreads) {
-        const int bx = i % BX, r = i / BX;
-        const int by = r % BY, bz = r / BY;
-        const int gx = x0 + bx - 1, gy = y0 + by - 1, gz = z0 + bz - 1;
-        float v = 0.f;
-        if (kInterior || (gx >= 0 && gx < D.nx && gy >= 0 && gy < D.ny && gz >= 0 && gz < D.nz))
-            v = __ldg(f + (int64_t(gz) * D.nxy + int64_t(gy) * D.nx + gx));
-        fbox[i] = v;
-        pbox[i] = uint16_t(i);
+    int bxo, byo, bzo;
+    if (kInterior) {
+        int t = blockIdx.x;
+        bxo = t % A.tiles_x + A.origin.x;
+        t /= A.tiles_x;
+        byo = t % A.tiles_y + A.origin.y;
+        bzo = t / A.tiles_y + A.origin.z;
+    } else {
+        const int packed = A.btiles[blockIdx.x];     // (bz << 20) | (by << 10) | bx
+        bxo = packed & 1023;
+        byo = (packed >> 10) & 1023;
+        bzo = packed >> 20;
     }
+    const int x0 = bxo * TX, y0 = byo * TY, z0 = A.z_lo + bzo * TZ;
+
+    // ---- stage the tile + halo: one TMA bulk-tensor copy (or plain loads).
+    // A TMA box must start at a non-negative, 16-byte aligned x (measured,
+    // tools/tma_probe): at the low domain faces the box starts at 0 and is
+    // written shifted by one row / plane / 4 columns into the smem box (the
+    // cells it then spills into are padding or never-read halo of an invalid
+    // side; kFboxSlack covers the spill past the end).  Tiles whose box needs
+    // a neighbour slab's halo plane take the plain loads.
+    bool use_tma = kTma;
+    if (kTma && !kInterior)
+        use_tma = !((z0 - 1 >= 0 && z0 - 1 < A.z_lo) || (z0 + TZ < D.nz && z0 + TZ >= A.z_hi));
+    if (use_tma) {
+        if (tid == 0) {
+            mbar_init(bar, 1);
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        }
+        __syncthreads();
+        if (tid == 0) {
+            const int xs = x0 - XO, ys = y0 - 1, zs = z0 - 1 - A.z_lo;
+            const int shift = (xs < 0 ? XO : 0) + (ys < 0 ? BX : 0) + (zs < 0 ? PL : 0);
+            mbar_expect_tx(bar, uint32_t(BOX * 4));
+            tma_load_3d(fbox + shift, &tmap, bar, xs < 0 ? 0 : xs, ys < 0 ? 0 : ys, zs < 0 ? 0 : zs);
+        }
+    } else {
+        for (int i = tid; i < BOX; i += kThreads) {
+            const int bx = i % BX, r = i / BX;
+            const int by = r % BY, bz = r / BY;
+            const int gx = x0 + bx - XO, gy = y0 + by - 1, gz = z0 + bz - 1;
+            float v = 0.f;
+            if (gx >= 0 && gx < D.nx && gy >= 0 && gy < D.ny && gz >= 0 && gz < D.nz) {
+                const int64_t o = int64_t(gy) * D.nx + gx;
+                if (gz >= A.z_lo && gz < A.z_hi) v = __ldg(A.f + (int64_t(gz - A.z_lo) * D.ny * D.nx + o));
+                else if (gz == A.z_lo - 1 && A.f_lo) v = __ldg(A.f_lo + o);
+                else if (gz == A.z_hi && A.f_hi) v = __ldg(A.f_hi + o);
+            }
+            fbox[i] = v;
+        }
+    }
+    // halo / padding cells of the pointer box are terminal (point to themselves)
+    for (int i = tid; i < BOX; i += kThreads) pbox[i] = uint16_t(i);
+    for (int i = tid; i < kLutWords; i += kThreads) lut[i] = __ldg(A.lut + i);
+    if (use_tma) mbar_wait(bar, 0);
     __syncthreads();
 
     const int gx = x0 + tx, gy = y0 + ty;
     const bool col_ok = kInterior || (gx < D.nx && gy < D.ny);
-    // validity of the in-plane directions (x-1, x+1, y-1, y+1)
     const bool xm = kInterior || gx > 0, xp = kInterior || gx + 1 < D.nx;
     const bool ym = kInterior || gy > 0, yp = kInterior || gy + 1 < D.ny;
+    const int cb = bidx(tx + XO, ty + 1, 0);
 
-    // 2-D star of a plane at (tx, ty): c, (1,0), (0,1), (1,1), (-1,0), (0,-1), (-1,-1)
+    // 2-D star of box plane bz at this column: c, (1,0), (0,1), (1,1), (-1,0), (0,-1), (-1,-1)
     auto star = [&](int bz, float *s) {
-        const int b = bidx(tx + 1, ty + 1, bz);
-        s[0] = fbox[b];
-        s[1] = fbox[b + 1];
-        s[2] = fbox[b + BX];
-        s[3] = fbox[b + BX + 1];
-        s[4] = fbox[b - 1];
-        s[5] = fbox[b - BX];
-        s[6] = fbox[b - BX - 1];
+        const float *p = fbox + cb + bz * PL;
+        s[0] = p[0];
+        s[1] = p[1];
+        s[2] = p[BX];
+        s[3] = p[BX + 1];
+        s[4] = p[-1];
+        s[5] = p[-BX];
+        s[6] = p[-BX - 1];
     };
-    // box-index deltas of the 14 offsets, lower group then upper group
-    constexpr int PL = BX * BY;
-    constexpr int LD[7] = {-1 - BX - PL, -BX - PL, -1 - PL, -PL, -1 - BX, -BX, -1};
-    constexpr int UD[7] = {1, BX, 1 + BX, PL, 1 + PL, BX + PL, 1 + BX + PL};
+    // in-plane 2x2 maxima (ascending index order inside each, later wins ties)
+    auto bplus = [&](const float *s, int dz) -> VK {    // (0,0) (1,0) (0,1) (1,1)
+        VK a = vmax(VK{s[0], dz * PL}, VK{s[1], 1 + dz * PL});
+        VK b = vmax(VK{s[2], BX + dz * PL}, VK{s[3], BX + 1 + dz * PL});
+        return vmax(a, b);
+    };
+    auto bminus = [&](const float *s, int dz) -> VK {   // (-1,-1) (0,-1) (-1,0) (0,0)
+        VK a = vmax(VK{s[6], -BX - 1 + dz * PL}, VK{s[5], -BX + dz * PL});
+        VK b = vmax(VK{s[4], -1 + dz * PL}, VK{s[0], dz * PL});
+        return vmax(a, b);
+    };
+
     float pm[7], p0[7], pp[7];
     star(0, pm);
     star(1, p0);
-
+    VK bm_prev = bminus(pm, -1);       // B-(z-1) for z = 0
+    VK bp_cur = bplus(p0, 0);          // B+(z)   for z = 0
     uint32_t sad_mask = 0, max_mask = 0;
     bool nan_seen = false;
-#pragma unroll 2
+#pragma unroll 4
     for (int z = 0; z < TZ; ++z) {
         star(z + 2, pp);
         const int gz = z0 + z;
-        const bool zm = kInterior || gz > 0, zpv = kInterior || gz + 1 < D.nz;
-        const bool ok = col_ok && (kInterior || gz < D.nz);
+        const bool ok = col_ok && (kInterior || gz < A.z_hi);
         const float fv = p0[0];
         nan_seen |= ok && (fv != fv);
-        const float lv[7] = {pm[6], pm[5], pm[4], pm[0], p0[6], p0[5], p0[4]};
-        const bool lok[7] = {zm && xm && ym, zm && ym, zm && xm, zm, xm && ym, ym, xm};
-        const float uv[7] = {p0[1], p0[2], p0[3], pp[0], pp[1], pp[2], pp[3]};
-        const bool uok[7] = {xp, yp, xp && yp, zpv, zpv && xp, zpv && yp, zpv && xp && yp};
-        uint32_t mask = 0;
-        // lower neighbour u is above v iff f(u) > f(v) (its index is lower)
-        float bl = -__int_as_float(0x7f800000);
-        int bld = 0;
+        uint32_t mask;
+        int d;
+        if (kInterior) {
+            // S1: argmax over box(v) u box(v - 1); the upper box wins ties
+            const VK bp_next = bplus(pp, 1);
+            const VK bm_cur = bminus(p0, 0);
+            const VK U = vmax(bp_cur, bp_next);
+            const VK L = vmax(bm_prev, bm_cur);
+            d = vmax(L, U).d;
+            bp_cur = VK{bp_next.v, bp_next.d - PL};
+            bm_prev = VK{bm_cur.v, bm_cur.d - PL};
+            // S3: upper mask, lower group (index < v: up iff f > fv), then upper
+            // (set.*.u32 gives an all-ones word, merged with its bit by one LOP3)
+            mask = (setgt(pm[6], fv) & 1u) | (setgt(pm[5], fv) & 2u) | (setgt(pm[4], fv) & 4u) |
+                   (setgt(pm[0], fv) & 8u) | (setgt(p0[6], fv) & 16u) | (setgt(p0[5], fv) & 32u) |
+                   (setgt(p0[4], fv) & 64u) | (setge(p0[1], fv) & 128u) | (setge(p0[2], fv) & 256u) |
+                   (setge(p0[3], fv) & 512u) | (setge(pp[0], fv) & 1024u) | (setge(pp[1], fv) & 2048u) |
+                   (setge(pp[2], fv) & 4096u) | (setge(pp[3], fv) & 8192u);
+        } else {
+            const bool zm = gz > 0, zpv = gz + 1 < D.nz;
+            const float lv[7] = {pm[6], pm[5], pm[4], pm[0], p0[6], p0[5], p0[4]};
+            const bool lok[7] = {zm && xm && ym, zm && ym, zm && xm, zm, xm && ym, ym, xm};
+            const float uv[7] = {p0[1], p0[2], p0[3], pp[0], pp[1], pp[2], pp[3]};
+            const bool uok[7] = {xp, yp, xp && yp, zpv, zpv && xp, zpv && yp, zpv && xp && yp};
+            constexpr int LD[7] = {-1 - BX - PL, -BX - PL, -1 - PL, -PL, -1 - BX, -BX, -1};
+            constexpr int UD[7] = {1, BX, 1 + BX, PL, 1 + PL, BX + PL, 1 + BX + PL};
+            mask = 0;
+            float bl = -__int_as_float(0x7f800000);
+            int bld = 0;
 #pragma unroll
-        for (int k = 0; k < 7; ++k) {
-            const bool up = (kInterior || lok[k]) && (lv[k] > fv);
-            mask |= up ? (1u << k) : 0u;
-            if (up && lv[k] >= bl) {     // ascending index: >= keeps the highest index on ties
-                bl = lv[k];
-                bld = LD[k];
+            for (int k = 0; k < 7; ++k) {
+                const bool up = lok[k] && (lv[k] > fv);
+                mask |= up ? (1u << k) : 0u;
+                if (up && lv[k] >= bl) {
+                    bl = lv[k];
+                    bld = LD[k];
+                }
             }
-        }
-        // upper neighbour u is above v iff f(u) >= f(v)
-        float bu = fv;
-        int bud = 0;
+            float bu = fv;
+            int bud = 0;
 #pragma unroll
-        for (int k = 0; k < 7; ++k) {
-            const bool up = (kInterior || uok[k]) && (uv[k] >= fv);
-            mask |= up ? (1u << (7 + k)) : 0u;
-            if (up && uv[k] >= bu) {
-                bu = uv[k];
-                bud = UD[k];
+            for (int k = 0; k < 7; ++k) {
+                const bool up = uok[k] && (uv[k] >= fv);
+                mask |= up ? (1u << (7 + k)) : 0u;
+                if (up && uv[k] >= bu) {
+                    bu = uv[k];
+                    bud = UD[k];
+                }
             }
+            d = (bud != 0 && (bld == 0 || bu >= bl)) ? bud : bld;
         }
-        // gradient = SoS max over the upper link; an upper-group winner beats a
-        // lower-group one on equal values (higher index)
-        const int d = (bud != 0 && (bld == 0 || bu >= bl)) ? bud : bld;
-        const int c = bidx(tx + 1, ty + 1, z + 1);
+        const int c = cb + (z + 1) * PL;
         if (ok) pbox[c] = uint16_t(c + d);
-        const int beta = lut[mask];
-        if (ok && beta >= 2) sad_mask |= 1u << z;
-        if (ok && mask == 0) max_mask |= 1u << z;
+        const bool sad = (lut[mask >> 5] >> (mask & 31)) & 1u;
+        sad_mask |= (ok && sad) ? (1u << z) : 0u;
+        max_mask |= (ok && mask == 0) ? (1u << z) : 0u;
 #pragma unroll
         for (int k = 0; k < 7; ++k) {
             pm[k] = p0[k];
             p0[k] = pp[k];
         }
     }
-    if (nan_seen) atomicOr(nan_flag, 1);
+    if (nan_seen) atomicOr(A.nan_flag, 1);
     __syncthreads();
 
-    // ---- S2 inside the tile: chase to the local root (path halving in smem;
-    // benign races: every stored value lies further along the same path)
-    const bool wrow_aligned = (D.nx & 31) == 0;
+    // ---- S2 inside the tile.  Two rounds of pointer doubling (independent
+    // loads, no divergence) quarter every chain; then every vertex chases the
+    // rest of its chain to the local root, halving the path as it goes (in
+    // place and race-benign: every stored value lies further along the path).
+#pragma unroll 1
+    for (int round = 0; round < 2; ++round) {
+#pragma unroll
+        for (int z = 0; z < TZ; ++z) {
+            const int c = cb + (z + 1) * PL;
+            pbox[c] = pbox[pbox[c]];
+        }
+        __syncthreads();
+    }
 #pragma unroll 1
     for (int z = 0; z < TZ; ++z) {
-        const int gz = z0 + z;
-        const bool ok = col_ok && (kInterior || gz < D.nz);
-        int x = bidx(tx + 1, ty + 1, z + 1);
+        const int c = cb + (z + 1) * PL;
+        int x = c;
         int p = pbox[x];
         while (p != x) {
-            const int p2 = pbox[p];
-            if (p2 != p) pbox[x] = uint16_t(p2);
+            const int q = pbox[p];
+            if (q != p) pbox[x] = uint16_t(q);
             x = p;
-            p = p2;
+            p = q;
         }
-        // root x: in-tile maximum or halo exit
-        const int bx = x % BX, r = x / BX;
-        const int by = r % BY, bz = r / BY;
-        const bool exit = bx == 0 || bx == BX - 1 || by == 0 || by == BY - 1 || bz == 0 || bz == BZ - 1;
-        const int64_t root = int64_t(z0 + bz - 1) * D.nxy + int64_t(y0 + by - 1) * D.nx + (x0 + bx - 1);
-        const int64_t v = int64_t(gz) * D.nxy + int64_t(gy) * D.nx + gx;
-        if (ok) label[v] = int32_t(root);
+        pbox[c] = uint16_t(x);
+    }
+    __syncthreads();
+
+    // ---- outputs: label (bit 31 = exit), bitmaps, exit-target marks
+    uint8_t *used = reinterpret_cast<uint8_t *>(fbox);   // fbox is dead: 1 byte per box cell
+    for (int i = tid; i < BOX / 16; i += kThreads) reinterpret_cast<uint4 *>(used)[i] = make_uint4(0, 0, 0, 0);
+    __syncthreads();
+    const bool aligned = (D.nx & 31) == 0;
+#pragma unroll 2
+    for (int z = 0; z < TZ; ++z) {
+        const int gz = z0 + z;
+        const bool ok = col_ok && (kInterior || gz < A.z_hi);
+        // another thread's path halving may have overwritten pbox[c] with an
+        // ancestor after c's own chase stored the root: follow to the root
+        int r = pbox[cb + (z + 1) * PL];
+        for (int q; (q = pbox[r]) != r;) r = q;
+        const int bz = r / PL, rr = r - bz * PL;
+        const int by = rr / BX, bx = rr - by * BX;
+        // exit: the root is in the halo shell of the box, or (last tile of a
+        // slab) in a plane the slab does not own
+        const bool exit = bx < XO || bx >= XO + TX || by == 0 || by == BY - 1 || bz == 0 || bz == BZ - 1 ||
+                          (!kInterior && z0 - 1 + bz >= A.z_hi);
+        const int32_t root = ((z0 - 1 + bz) * D.ny + (y0 - 1 + by)) * D.nx + (x0 - XO + bx);
+        const int32_t v = (gz * D.ny + gy) * D.nx + gx;
+        if (ok) {
+            A.label[v - A.v0] = exit ? int32_t(uint32_t(root) | kFlag) : root;
+            if (exit) used[r] = 1;
+        }
         const uint32_t eb = __ballot_sync(0xffffffffu, ok && exit);
-        const uint32_t sb = __ballot_sync(0xffffffffu, ok && ((sad_mask >> z) & 1u));
-        const uint32_t mb = __ballot_sync(0xffffffffu, ok && ((max_mask >> z) & 1u));
-        if (wrow_aligned) {
+        const uint32_t sb = __ballot_sync(0xffffffffu, (sad_mask >> z) & 1u);
+        const uint32_t mb = __ballot_sync(0xffffffffu, (max_mask >> z) & 1u);
+        if (aligned) {
             if (tx == 0 && ok) {
-                exit_bits[v >> 5] = eb;
-                sad_bits[v >> 5] = sb;
-                max_bits[v >> 5] = mb;
+                const int64_t w = (v - A.v0) >> 5;
+                A.exit_bits[w] = eb;
+                A.sad_bits[w] = sb;
+                A.max_bits[w] = mb;
             }
         } else {
-            // rows are not 32-aligned: lane 0 scatters the ballots into (at
-            // most) two words with atomics (the words were zeroed)
-            const int64_t v0 = int64_t(gz) * D.nxy + int64_t(gy) * D.nx + x0;
-            const bool row_ok = kInterior || (gy < D.ny && gz < D.nz);
+            const int64_t r0 = int64_t((gz * D.ny + gy) * D.nx + x0) - A.v0;
+            const bool row_ok = kInterior || (gy < D.ny && gz < A.z_hi);
             if (tx == 0 && row_ok && (eb | sb | mb)) {
-                const int sh = int(v0 & 31);
-                const int64_t w = v0 >> 5;
-                atomicOr(exit_bits + w, eb << sh);
-                atomicOr(sad_bits + w, sb << sh);
-                atomicOr(max_bits + w, mb << sh);
+                const int sh = int(r0 & 31);
+                const int64_t w = r0 >> 5;
+                atomicOr(A.exit_bits + w, eb << sh);
+                atomicOr(A.sad_bits + w, sb << sh);
+                atomicOr(A.max_bits + w, mb << sh);
                 if (sh) {
-                    atomicOr(exit_bits + w + 1, eb >> (32 - sh));
-                    atomicOr(sad_bits + w + 1, sb >> (32 - sh));
-                    atomicOr(max_bits + w + 1, mb >> (32 - sh));
+                    atomicOr(A.exit_bits + w + 1, eb >> (32 - sh));
+                    atomicOr(A.sad_bits + w + 1, sb >> (32 - sh));
+                    atomicOr(A.max_bits + w + 1, mb >> (32 - sh));
                 }
             }
         }
     }
+    __syncthreads();
+    // ---- append the tile's distinct exit targets to E: one global atomic per
+    // tile (block scan of per-thread counts)
+    uint32_t *red = reinterpret_cast<uint32_t *>(smem + kOffM + 16);   // [32] warp sums + [1] base
+    // only the halo shell of the box can hold exit targets
+    int mine = 0;
+    for (int s = tid; s < kShell; s += kThreads) mine += used[shell_cell(s)];
+    int incl = mine;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (tx >= o) incl += y;
+    }
+    if (tx == 31) red[ty] = uint32_t(incl);
+    __syncthreads();
+    if (ty == 0) {
+        const int wsum = tx < kThreads / 32 ? int(red[tx]) : 0;
+        int wincl = wsum;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, wincl, o);
+            if (tx >= o) wincl += y;
+        }
+        if (tx < kThreads / 32) red[tx] = uint32_t(wincl - wsum);   // exclusive warp offsets
+        if (tx == kThreads / 32 - 1) {
+            const unsigned long long b = wincl ? atomicAdd(A.ecount, (unsigned long long)wincl) : 0ull;
+            reinterpret_cast<unsigned long long *>(red + 32)[0] = b;
+        }
+    }
+    __syncthreads();
+    if (mine) {
+        unsigned long long slot = reinterpret_cast<unsigned long long *>(red + 32)[0] + red[ty] + (incl - mine);
+        for (int s = tid; s < kShell; s += kThreads) {
+            const int i = shell_cell(s);
+            if (!used[i]) continue;
+            const int bz = i / PL, rr = i - bz * PL;
+            const int by = rr / BX, bx = rr - by * BX;
+            if (slot < (unsigned long long)A.ecap)
+                A.elist[slot] = ((z0 - 1 + bz) * D.ny + (y0 - 1 + by)) * D.nx + (x0 - XO + bx);
+            ++slot;
+        }
+    }
 }
 
-// Pass X: resolve every exiting vertex through the exit graph.
-__global__ void __launch_bounds__(256) k_exit_fixup(int32_t *label, const uint32_t *__restrict__ exit_bits, int64_t n) {
-    const int64_t v = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (v >= n) return;
-    const uint32_t w = __ldg(exit_bits + (v >> 5));
-    if (!((w >> (v & 31)) & 1u)) return;
-    int32_t e = label[v];
-    // e is a vertex of another tile; label[e] is its local root, final unless
-    // e itself exits
-    for (;;) {
-        const uint32_t we = *(volatile const uint32_t *)(exit_bits + (e >> 5));
-        const int32_t le = *(volatile int32_t *)(label + e);
-        if (!((we >> (e & 31)) & 1u)) {
-            e = le;
-            break;
+// Pass E: resolve every owned exit target through the exit graph (bit 31 =
+// not final), one dependent load per tile hop.  A path that leaves the slab
+// stops at its first remote vertex (resolved later by the boundary exchange).
+__global__ void __launch_bounds__(256) k_resolve_exits(int32_t *label, const int32_t *__restrict__ elist,
+                                                       const unsigned long long *ecount, int64_t ecap, int64_t v0,
+                                                       int64_t v1) {
+    const int64_t n = int64_t(min(*ecount, (unsigned long long)ecap));
+    for (int64_t j = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; j < n; j += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t e = elist[j];
+        if (e < v0 || e >= v1) continue;                 // a halo vertex: another slab's
+        int32_t w = *(volatile int32_t *)(label + (e - v0));
+        if (w >= 0) continue;
+        for (;;) {
+            const int64_t x = w & 0x7fffffff;
+            if (x < v0 || x >= v1) break;                 // remote: stays unresolved
+            const int32_t nw = *(volatile int32_t *)(label + (x - v0));
+            w = nw;
+            if (w >= 0) break;
         }
-        e = le;
-        // if label[e] was already resolved by another thread, e is now a
-        // maximum (not exiting) and the next iteration ends
+        label[e - v0] = w;
     }
-    label[v] = e;
+}
+
+// Pass E' (fallback when E overflowed): every exiting vertex chases its own
+// path as far as the slab allows.
+__global__ void __launch_bounds__(256) k_exit_chase(int32_t *label, const uint32_t *__restrict__ exit_bits, int64_t v0,
+                                                    int64_t v1) {
+    const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= v1 - v0) return;
+    if (!((__ldg(exit_bits + (i >> 5)) >> (i & 31)) & 1u)) return;
+    int32_t w = label[i];
+    while (w < 0) {
+        const int64_t x = w & 0x7fffffff;
+        if (x < v0 || x >= v1) break;
+        w = *(volatile int32_t *)(label + (x - v0));
+    }
+    label[i] = w;
 }
 
 __global__ void k_zero_words(uint32_t *a, uint32_t *b, uint32_t *c, int64_t n) {
@@ -270,61 +537,159 @@ static eg_status fail(std::string *err, cudaError_t e, const char *what) {
     return e == cudaErrorMemoryAllocation ? EG_ERR_OOM : EG_ERR_CUDA;
 }
 
-eg_status tiled3d_labels(Tiled3D *t, int ndim, const int64_t *dims, const float *f, int32_t *labels,
-                         uint32_t *sad_bits, uint32_t *max_bits, int *flags, cudaStream_t st, eg_stats *stats,
-                         std::string *err, uint32_t *exit_bits) {
+typedef CUresult (*EncodeTiledFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
+                                  const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+template <bool I, bool T>
+static cudaError_t set_smem_attr() {
+    return cudaFuncSetAttribute(k_tile<I, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kTileSmem));
+}
+
+eg_status tiled3d_local(Tiled3D *t, int ndim, const int64_t *dims, const Slab &s, const FieldView &F, int32_t *labels,
+                        uint32_t *sad_bits, uint32_t *max_bits, uint32_t *exit_bits, int *flags, cudaStream_t st,
+                        eg_stats *stats, std::string *err, cudaEvent_t ev_main0, cudaEvent_t ev_main1) {
     int64_t d3[3] = {1, 1, 1};
     for (int i = 0; i < ndim; ++i) d3[i] = dims[i];
     cudaError_t e;
-    if (!t->lut_ready) {
+    if (!t->ready) {
+        // 1-bit LUT: is beta0+ >= 2 for every 14-bit upper mask of the 3-D link,
+        // in the ascending-index offset order (lexicographic in (dz, dy, dx))
         int64_t dl[3] = {4, 4, 4};
         LinkTable tab = make_link_table(3, dl);
-        std::vector<uint8_t> lut = make_beta_lut3(tab);
-        if ((e = cudaMalloc(&t->d_lut, kLut)) != cudaSuccess) return fail(err, e, "cudaMalloc lut");
-        if ((e = cudaMemcpy(t->d_lut, lut.data(), kLut, cudaMemcpyHostToDevice)) != cudaSuccess)
+        std::vector<uint8_t> beta = make_beta_lut3(tab);
+        std::vector<uint32_t> bits(kLutWords, 0u);
+        for (int m = 0; m < (1 << 14); ++m)
+            if (beta[m] >= 2) bits[m >> 5] |= 1u << (m & 31);
+        if ((e = cudaMalloc(&t->d_lut, kLutWords * 4)) != cudaSuccess) return fail(err, e, "cudaMalloc lut");
+        if ((e = cudaMemcpy(t->d_lut, bits.data(), kLutWords * 4, cudaMemcpyHostToDevice)) != cudaSuccess)
             return fail(err, e, "lut upload");
-        if ((e = cudaFuncSetAttribute(k_tile<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kTileSmem))) !=
-            cudaSuccess)
+        if ((e = cudaMalloc(&t->d_ecount, sizeof(unsigned long long))) != cudaSuccess)
+            return fail(err, e, "cudaMalloc ecount");
+        if ((e = set_smem_attr<false, false>()) != cudaSuccess || (e = set_smem_attr<true, false>()) != cudaSuccess ||
+            (e = set_smem_attr<true, true>()) != cudaSuccess)
             return fail(err, e, "smem attr");
-        if ((e = cudaFuncSetAttribute(k_tile<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kTileSmem))) !=
-            cudaSuccess)
-            return fail(err, e, "smem attr");
-        t->lut_ready = true;
+        cudaDriverEntryPointQueryResult q;
+        void *fn = nullptr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            t->encode = fn;
+        cudaGetLastError();
+        t->ready = true;
     }
-    const int64_t N = d3[0] * d3[1] * d3[2];
-    const int64_t words = (N + 31) / 32;
-    Dims3 D{int32_t(d3[0]), int32_t(d3[1]), int32_t(d3[2]), d3[0] * d3[1]};
+    // a 1-D / 2-D grid is a 3-D grid with unit axes; its only slab is the whole grid
+    const int64_t z_lo = ndim == 3 ? s.z0 : 0, z_hi = ndim == 3 ? s.z1 : 1;
+    const int64_t nown = s.v1 - s.v0;
+    const int64_t words = (nown + 31) / 32;
+    Dims3 D{int32_t(d3[0]), int32_t(d3[1]), int32_t(d3[2])};
     const int tiles_x = int((d3[0] + TX - 1) / TX), tiles_y = int((d3[1] + TY - 1) / TY);
-    const int tiles_z = int((d3[2] + TZ - 1) / TZ);
+    const int tiles_z = int((z_hi - z_lo + TZ - 1) / TZ);
+    if (tiles_x > 1024 || tiles_y > 1024 || tiles_z > 2047) {
+        if (err) *err = "grid too large for the tiled path";
+        return EG_ERR_UNSUPPORTED;
+    }
+    // interior tiles: x/y halo box inside the domain and z box inside the
+    // owned planes: 1 <= b <= (extent - 1 - T) / T on every axis
+    int3 lo = make_int3(1, 1, 1);
+    int3 hi = make_int3(int((d3[0] - 1 - TX) / TX), int((d3[1] - 1 - TY) / TY), int((z_hi - z_lo - 1 - TZ) / TZ));
+    if (d3[0] - 1 - TX < 0 || d3[1] - 1 - TY < 0 || z_hi - z_lo - 1 - TZ < 0) hi = make_int3(0, 0, 0);
+    const bool have_interior = hi.x >= lo.x && hi.y >= lo.y && hi.z >= lo.z;
+    // boundary tile list, cached per (dims, slab)
+    if (t->bdims[0] != d3[0] || t->bdims[1] != d3[1] || t->bdims[2] != d3[2] || t->bz[0] != z_lo || t->bz[1] != z_hi) {
+        std::vector<int32_t> bt;
+        for (int bz = 0; bz < tiles_z; ++bz)
+            for (int by = 0; by < tiles_y; ++by)
+                for (int bx = 0; bx < tiles_x; ++bx) {
+                    const bool in = have_interior && bx >= lo.x && bx <= hi.x && by >= lo.y && by <= hi.y &&
+                                    bz >= lo.z && bz <= hi.z;
+                    if (!in) bt.push_back((bz << 20) | (by << 10) | bx);
+                }
+        if (t->d_btiles) cudaFree(t->d_btiles);
+        t->d_btiles = nullptr;
+        if (!bt.empty()) {
+            if ((e = cudaMalloc(&t->d_btiles, bt.size() * 4)) != cudaSuccess) return fail(err, e, "cudaMalloc btiles");
+            if ((e = cudaMemcpy(t->d_btiles, bt.data(), bt.size() * 4, cudaMemcpyHostToDevice)) != cudaSuccess)
+                return fail(err, e, "btiles upload");
+        }
+        t->n_btiles = int64_t(bt.size());
+        for (int i = 0; i < 3; ++i) t->bdims[i] = d3[i];
+        t->bz[0] = z_lo;
+        t->bz[1] = z_hi;
+    }
+    // exit-target list capacity: N / 8 (falls back to a per-vertex chase on overflow)
+    const int64_t want = std::max<int64_t>(nown / 8, 4096);
+    if (t->ecap < want) {
+        if (t->d_elist) cudaFree(t->d_elist);
+        t->d_elist = nullptr;
+        t->ecap = 0;
+        if ((e = cudaMalloc(&t->d_elist, want * 4)) != cudaSuccess) return fail(err, e, "cudaMalloc elist");
+        t->ecap = want;
+    }
+    if ((e = cudaMemsetAsync(t->d_ecount, 0, sizeof(unsigned long long), st)) != cudaSuccess)
+        return fail(err, e, "memset ecount");
     const bool aligned = (D.nx & 31) == 0;
     if (!aligned) {
         k_zero_words<<<148 * 4, 256, 0, st>>>(exit_bits, sad_bits, max_bits, words);
         stats->kernel_launches += 1;
     }
-    // interior tiles (halo box inside the domain) take the unchecked variant
-    int3 lo = make_int3(1, 1, 1);
-    int3 hi = make_int3(int((d3[0] - 1 - TX) / TX), int((d3[1] - 1 - TY) / TY), int((d3[2] - 1 - TZ) / TZ));
-    // tile b is interior iff b >= 1 and (b + 1) * T + 1 <= n, i.e. b <= (n - 1 - T) / T
-    const bool have_interior = hi.x >= lo.x && hi.y >= lo.y && hi.z >= lo.z;
-    if (!have_interior) {
-        lo = make_int3(1, 1, 1);
-        hi = make_int3(0, 0, 0);
+    // TMA tensor map over the owned planes (needs 16-byte row and plane strides)
+    CUtensorMap tmap;
+    std::memset(&tmap, 0, sizeof(tmap));
+    bool tma = t->encode != nullptr && (d3[0] % 4) == 0 && d3[0] >= 4 &&
+               (reinterpret_cast<uintptr_t>(F.own) % 16) == 0 && have_interior;
+    if (tma) {
+        cuuint64_t gdim[3] = {cuuint64_t(d3[0]), cuuint64_t(d3[1]), cuuint64_t(z_hi - z_lo)};
+        cuuint64_t gstr[2] = {cuuint64_t(d3[0] * 4), cuuint64_t(d3[0] * d3[1] * 4)};
+        cuuint32_t box[3] = {BX, BY, BZ};
+        cuuint32_t es[3] = {1, 1, 1};
+        CUresult r = reinterpret_cast<EncodeTiledFn>(t->encode)(
+            &tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float *>(F.own), gdim, gstr, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        tma = (r == CUDA_SUCCESS);
     }
-    const int64_t ntiles = int64_t(tiles_x) * tiles_y * tiles_z;
-    k_tile<false><<<unsigned(ntiles), kThreads, kTileSmem, st>>>(f, D, t->d_lut, labels, exit_bits, sad_bits, max_bits,
-                                                         flags, tiles_x, tiles_y, make_int3(0, 0, 0), lo, hi);
-    stats->kernel_launches += 1;
-    if ((e = cudaGetLastError()) != cudaSuccess) return fail(err, e, "k_tile<false>");
-    if (have_interior) {
-        const int ix = hi.x - lo.x + 1, iy = hi.y - lo.y + 1, iz = hi.z - lo.z + 1;
-        k_tile<true><<<unsigned(int64_t(ix) * iy * iz), kThreads, kTileSmem, st>>>(
-            f, D, t->d_lut, labels, exit_bits, sad_bits, max_bits, flags, ix, iy, lo, lo, hi);
+    stats->path = 1;
+    TileArgs A{F.own,     F.lo,      F.hi,      int32_t(z_lo), int32_t(z_hi), s.v0,       labels,  exit_bits,
+               sad_bits,  max_bits,  flags,     t->d_elist,    t->d_ecount,   t->ecap,    t->d_lut, t->d_btiles,
+               0,         0,         make_int3(0, 0, 0)};
+    if (ev_main0) cudaEventRecord(ev_main0, st);
+    if (t->n_btiles > 0) {
+        // boundary tiles use plain loads: a TMA box must start at a 16-byte
+        // aligned, non-negative x coordinate (measured with tools/tma_probe:
+        // a start of -1 is an illegal instruction), and these tiles are the
+        // ones whose halo starts outside the field or in a neighbour slab
+        k_tile<false, false><<<unsigned(t->n_btiles), kThreads, kTileSmem, st>>>(tmap, A, D);
         stats->kernel_launches += 1;
-        if ((e = cudaGetLastError()) != cudaSuccess) return fail(err, e, "k_tile<true>");
+        if ((e = cudaGetLastError()) != cudaSuccess) return fail(err, e, "k_tile<boundary>");
     }
-    k_exit_fixup<<<unsigned((N + 255) / 256), 256, 0, st>>>(labels, exit_bits, N);
+    if (have_interior) {
+        A.tiles_x = hi.x - lo.x + 1;
+        A.tiles_y = hi.y - lo.y + 1;
+        A.origin = lo;
+        const int64_t nt = int64_t(A.tiles_x) * A.tiles_y * (hi.z - lo.z + 1);
+        if (tma)
+            k_tile<true, true><<<unsigned(nt), kThreads, kTileSmem, st>>>(tmap, A, D);
+        else
+            k_tile<true, false><<<unsigned(nt), kThreads, kTileSmem, st>>>(tmap, A, D);
+        stats->kernel_launches += 1;
+        if ((e = cudaGetLastError()) != cudaSuccess) return fail(err, e, "k_tile<interior>");
+    }
+    if (ev_main1) cudaEventRecord(ev_main1, st);
+    // resolve the owned part of E
+    k_resolve_exits<<<148 * 64, 256, 0, st>>>(labels, t->d_elist, t->d_ecount, t->ecap, s.v0, s.v1);
     stats->kernel_launches += 1;
-    if ((e = cudaGetLastError()) != cudaSuccess) return fail(err, e, "k_exit_fixup");
+    if ((e = cudaGetLastError()) != cudaSuccess) return fail(err, e, "k_resolve_exits");
+    unsigned long long ecount = 0;
+    if ((e = cudaMemcpyAsync(&ecount, t->d_ecount, sizeof(ecount), cudaMemcpyDeviceToHost, st)) != cudaSuccess ||
+        (e = cudaStreamSynchronize(st)) != cudaSuccess)
+        return fail(err, e, "ecount");
+    stats->n_exit_targets += int64_t(ecount);
+    if (int64_t(ecount) > t->ecap) {
+        // E overflowed: every exiting vertex chases its own path (exact, slower)
+        k_exit_chase<<<unsigned((nown + 255) / 256), 256, 0, st>>>(labels, exit_bits, s.v0, s.v1);
+        stats->kernel_launches += 1;
+        if ((e = cudaGetLastError()) != cudaSuccess) return fail(err, e, "k_exit_chase");
+    }
     return EG_OK;
 }
 

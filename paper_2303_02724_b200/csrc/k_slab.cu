@@ -1,0 +1,142 @@
+// Cross-slab label resolution (multi-GPU slabs and virtual partitions).
+//
+// The paper's hybrid mode pauses a gradient path when it reaches a block
+// boundary and keeps a partial path (saddle, first, last) until the adjacent
+// block is processed.  Here every slab (one GPU, or one virtual
+// partition) first resolves paths locally; a path that leaves the slab ends
+// in an "exit pointer" to a vertex of a halo plane (label = kUnresolved | x).
+// The slabs then exchange the labels of their two boundary planes with their
+// neighbours and jump over those values (bval / hval) until no boundary value
+// is unresolved; a final pass rewrites every unresolved owned label.  Paths
+// cross a slab boundary only through its two planes, so the exchange is a
+// fixed 2 planes per neighbour per round.
+#include "eg_impl.h"
+
+namespace eg {
+
+static inline unsigned blocks_for(int64_t n, int bs) { return unsigned((n + bs - 1) / bs); }
+
+__global__ void k_flag_remote(int32_t *label, int64_t n, int64_t v0) {
+    const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int64_t w = label[i];
+    if (w < v0 || w >= v0 + n) label[i] = int32_t(uint32_t(w) | kUnresolved);
+}
+
+cudaError_t launch_flag_remote(int32_t *label, int64_t n, int64_t v0, cudaStream_t st) {
+    if (n <= 0) return cudaSuccess;
+    k_flag_remote<<<blocks_for(n, 256), 256, 0, st>>>(label, n, v0);
+    return cudaGetLastError();
+}
+
+// value of owned vertex g, followed one step through an owned exit target
+// (whose own label is final or points to a remote vertex)
+__device__ __forceinline__ int32_t local_value(const int32_t *label, int64_t g, int64_t v0, int64_t v1) {
+    int32_t w = label[g - v0];
+    if (w < 0) {
+        const int64_t x = w & 0x7fffffff;
+        if (x >= v0 && x < v1) w = label[x - v0];
+    }
+    return w;
+}
+
+__global__ void k_bval_init(const int32_t *label, Slab s, int32_t *bval) {
+    const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= 2 * s.plane) return;
+    const int64_t g = i < s.plane ? s.v0 + i : s.v1 - s.plane + (i - s.plane);
+    bval[i] = local_value(label, g, s.v0, s.v1);
+}
+
+cudaError_t launch_bval_init(const int32_t *label, const Slab &s, int32_t *bval, cudaStream_t st) {
+    k_bval_init<<<blocks_for(2 * s.plane, 256), 256, 0, st>>>(label, s, bval);
+    return cudaGetLastError();
+}
+
+__global__ void k_bval_update(int32_t *bval, const int32_t *__restrict__ hlo, const int32_t *__restrict__ hhi, Slab s,
+                              unsigned long long *unresolved) {
+    const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    bool still = false;
+    if (i < 2 * s.plane) {
+        int32_t w = bval[i];
+        if (w < 0) {
+            const int64_t x = w & 0x7fffffff;          // a vertex of a halo plane
+            int32_t nv = w;
+            if (x >= s.v0 - s.plane && x < s.v0 && hlo) nv = hlo[x - (s.v0 - s.plane)];
+            else if (x >= s.v1 && x < s.v1 + s.plane && hhi) nv = hhi[x - s.v1];
+            if (nv >= 0) {
+                w = nv;
+            } else {
+                const int64_t x2 = nv & 0x7fffffff;    // the neighbour's path continues at x2
+                if (x2 >= s.v0 && x2 < s.v0 + s.plane) w = bval[x2 - s.v0];
+                else if (x2 >= s.v1 - s.plane && x2 < s.v1) w = bval[s.plane + (x2 - (s.v1 - s.plane))];
+                // else: x2 lies beyond the neighbour; wait for it to resolve x
+            }
+            bval[i] = w;
+            still = w < 0;
+        }
+    }
+    if (__any_sync(0xffffffffu, still)) {
+        const unsigned c = __popc(__ballot_sync(0xffffffffu, still));
+        if ((threadIdx.x & 31) == 0) atomicAdd(unresolved, (unsigned long long)c);
+    }
+}
+
+cudaError_t launch_bval_update(int32_t *bval, const int32_t *hval_lo, const int32_t *hval_hi, const Slab &s,
+                               unsigned long long *unresolved, cudaStream_t st) {
+    k_bval_update<<<blocks_for(2 * s.plane, 256), 256, 0, st>>>(bval, hval_lo, hval_hi, s, unresolved);
+    return cudaGetLastError();
+}
+
+// Final pass.  A warp owns 4 words of owned vertices (128 vertices).
+__global__ void __launch_bounds__(256) k_finalize(int32_t *label, const uint32_t *__restrict__ bits, int64_t v0,
+                                                  int64_t v1, const int32_t *__restrict__ hlo,
+                                                  const int32_t *__restrict__ hhi, int64_t plane) {
+    const int64_t n = v1 - v0;
+    const int64_t words = (n + 31) / 32;
+    const int64_t w0 = (int64_t(blockIdx.x) * (blockDim.x / 32) + (threadIdx.x >> 5)) * 4;
+    if (w0 >= words) return;
+    const int lane = threadIdx.x & 31;
+    bool need[4];
+    int32_t e[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const int64_t i = (w0 + k) * 32 + lane;
+        if (bits) {
+            const uint32_t b = (w0 + k < words) ? __ldg(bits + w0 + k) : 0u;
+            need[k] = (b >> lane) & 1u;
+        } else {
+            need[k] = i < n;
+        }
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) e[k] = need[k] ? label[(w0 + k) * 32 + lane] : 0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        need[k] = need[k] && e[k] < 0;
+        if (need[k]) {
+            int64_t x = e[k] & 0x7fffffff;
+            if (x >= v0 && x < v1) {
+                const int32_t w = __ldg(label + (x - v0));
+                if (w >= 0) {
+                    e[k] = w;
+                    continue;
+                }
+                x = w & 0x7fffffff;
+            }
+            e[k] = x < v0 ? hlo[x - v0 + plane] : hhi[x - v1];
+        }
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+        if (need[k]) label[(w0 + k) * 32 + lane] = e[k];
+}
+
+cudaError_t launch_finalize(int32_t *label, const uint32_t *bits, int64_t v0, int64_t v1, const int32_t *hval_lo,
+                            const int32_t *hval_hi, int64_t plane, cudaStream_t st) {
+    const int64_t words = (v1 - v0 + 31) / 32;
+    if (words <= 0) return cudaSuccess;
+    k_finalize<<<blocks_for(words, 32), 256, 0, st>>>(label, bits, v0, v1, hval_lo, hval_hi, plane);
+    return cudaGetLastError();
+}
+
+}  // namespace eg

@@ -196,3 +196,83 @@ def test_compute_host_e2e(eg, ctx):
     assert np.array_equal(lab.numpy().astype(np.int64), o.label)
     g2 = ctx.compute_host(torch.from_numpy(f), dims=dims)      # pageable source
     assert_graph_equal(g2, o)
+
+
+@pytest.mark.parametrize("dims,kind", [([70, 9, 40], "signed_zero"), ([33, 35, 19], "int"), ([96, 64, 48], "int")])
+def test_tie_heavy_repeated(eg, ctx, dims, kind):
+    # in-place races in the shared-memory chase / exit resolution must never
+    # change a result: 20 repetitions, every one bit-exact
+    import torch
+    f, _ = G.random_field(dims, 17 + len(dims), kind)
+    o = O.grid(f, dims)
+    t = torch.from_numpy(f).cuda()
+    for _ in range(20):
+        g = ctx.compute(t, dims=dims)
+        assert first_diff(g.labels.cpu().numpy().astype(np.int64), o.label) is None
+        assert np.array_equal(g.arcs, o.arcs)
+
+
+# ---------------------------------------------------------------- partitions
+# the slab partition must give identical outputs for any number
+# of slabs.  EG_VIRTUAL_PARTS(k) runs k slabs on one GPU with the exact
+# multi-GPU protocol (halo planes, boundary-plane exchange rounds, per-slab
+# graphs concatenated in slab order), the exchange done by device copies.
+
+@pytest.mark.parametrize("k", [2, 3, 4, 7])
+@pytest.mark.parametrize("path", PATHS)
+def test_virtual_slabs_3d(eg, ctx, k, path):
+    import torch
+    t, dims = G.turbulence(64, seed=11, device="cuda", kc_div=8)
+    f = t.cpu().numpy()
+    o = O.grid(f, dims)
+    g = ctx.compute(t, dims=dims, flags=_flags(eg, path, eg.EG_VIRTUAL_PARTS(k) | eg.EG_RAW_ARCS))
+    assert_graph_equal(g, o, raw=True, what=f"turbulence 64^3, {k} slabs, {path}")
+    st = ctx.stats()
+    assert st["boundary_rounds"] >= 1
+
+
+@pytest.mark.parametrize("dims,kind,k", [([40, 36, 50], "int", 3), ([70, 9, 40], "signed_zero", 4),
+                                         ([33, 35, 19], "normal", 2), ([64, 64, 64], "int", 8)])
+def test_virtual_slabs_tie_heavy(eg, ctx, dims, kind, k):
+    import torch
+    f, _ = G.random_field(dims, 5, kind)
+    o = O.grid(f, dims)
+    for path in PATHS:
+        g = ctx.compute(torch.from_numpy(f).cuda(), dims=dims, flags=_flags(eg, path, eg.EG_VIRTUAL_PARTS(k)))
+        assert_graph_equal(g, o, what=f"{dims} {kind} {k} slabs {path}")
+
+
+@pytest.mark.parametrize("dims,k", [([9, 8, 7, 10], 3), ([8, 7, 6, 5, 12], 4), ([60, 50], 5), ([200], 6)])
+def test_virtual_slabs_nd(eg, ctx, dims, k):
+    import torch
+    f, _ = G.random_field(dims, 9, "int")
+    o = O.grid(f, dims)
+    g = ctx.compute(torch.from_numpy(f).cuda(), dims=dims, flags=eg.EG_VIRTUAL_PARTS(k) | eg.EG_RAW_ARCS)
+    assert_graph_equal(g, o, raw=True, what=f"{dims} {k} slabs")
+
+
+def test_virtual_slabs_schwefel_5d(eg, ctx):
+    import torch
+    f, dims = G.schwefel([12, 12, 12, 12, 16])
+    o = O.grid(f, dims)
+    g = ctx.compute(torch.from_numpy(f).cuda(), dims=dims, flags=eg.EG_VIRTUAL_PARTS(4))
+    assert_graph_equal(g, o, what="Schwefel 5D, 4 slabs")
+
+
+@pytest.mark.parametrize("k", [2, 5])
+def test_virtual_ranges_csr(eg, ctx, k):
+    import torch
+    X, f = G.gmm_points(5000, seed=10)
+    rp, ci = G.knn_csr(X, 16, device="cuda")
+    o = O.csr(f, rp, ci)
+    g = ctx.compute(torch.from_numpy(f).cuda(), csr=(torch.from_numpy(rp).cuda(), torch.from_numpy(ci).cuda()),
+                    flags=eg.EG_VIRTUAL_PARTS(k) | eg.EG_RAW_ARCS)
+    assert_graph_equal(g, o, raw=True, what=f"knn 5K, {k} ranges")
+
+
+def test_virtual_slabs_invalid(eg, ctx):
+    import torch
+    f, dims = G.random_field([8, 8, 5], 1, "int")
+    with pytest.raises(eg.EgError) as e:          # 5 planes cannot make 3 slabs of >= 2 planes
+        ctx.compute(torch.from_numpy(f).cuda(), dims=dims, flags=eg.EG_VIRTUAL_PARTS(3))
+    assert "INVALID_ARG" in str(e.value)
