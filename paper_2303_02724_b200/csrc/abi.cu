@@ -347,9 +347,12 @@ static eg_status generic_local(eg_ctx *c, const Problem &P, SlabState &S, bool m
 static eg_status grid_graph(eg_ctx *c, const Problem &P, SlabState &S, bool raw) {
     const int64_t n = S.s.v1 - S.s.v0;
     int64_t *cnt = c->counts.as<int64_t>();
-    CK(c->scratch.ensure(std::max(compact_scratch_bytes(std::max<int64_t>(n, 1)), size_t(1) << 16)));
-    CK(launch_count_bits(S.max_bits.as<uint32_t>(), n, c->scratch.p, cnt + 0, c->stream));
-    CK(launch_count_bits(S.sad_bits.as<uint32_t>(), n, c->scratch.p, cnt + 1, c->stream));
+    // two scratch regions: the chunk offsets of each bitmap survive until emission
+    const size_t half = (std::max(compact_scratch_bytes(std::max<int64_t>(n, 1)), size_t(1) << 16) + 255) / 256 * 256;
+    CK(c->scratch.ensure(2 * half));
+    char *scr_max = c->scratch.as<char>(), *scr_sad = c->scratch.as<char>() + half;
+    CK(launch_count_bits(S.max_bits.as<uint32_t>(), n, scr_max, cnt + 0, c->stream));
+    CK(launch_count_bits(S.sad_bits.as<uint32_t>(), n, scr_sad, cnt + 1, c->stream));
     c->stats.kernel_launches += 4;
     CK(c->h_counts.ensure(sizeof(int64_t) * 8));
     int64_t *hc = c->h_counts.as<int64_t>();
@@ -361,11 +364,11 @@ static eg_status grid_graph(eg_ctx *c, const Problem &P, SlabState &S, bool raw)
     CK(S.maxima64.ensure(sizeof(int64_t) * std::max<int64_t>(S.n_max, 1)));
     CK(S.saddles32.ensure(sizeof(int32_t) * std::max<int64_t>(ns, 1)));
     CK(S.saddles64.ensure(sizeof(int64_t) * std::max<int64_t>(ns, 1)));
-    CK(launch_compact_bits(S.max_bits.as<uint32_t>(), n, S.s.v0, c->scratch.p, nullptr, S.maxima64.as<int64_t>(),
-                           cnt + 0, c->stream));
-    CK(launch_compact_bits(S.sad_bits.as<uint32_t>(), n, S.s.v0, c->scratch.p, S.saddles32.as<int32_t>(),
-                           S.saddles64.as<int64_t>(), cnt + 1, c->stream));
-    c->stats.kernel_launches += 6;
+    CK(launch_emit_counted(S.max_bits.as<uint32_t>(), n, S.s.v0, scr_max, nullptr, S.maxima64.as<int64_t>(),
+                           c->stream));
+    CK(launch_emit_counted(S.sad_bits.as<uint32_t>(), n, S.s.v0, scr_sad, S.saddles32.as<int32_t>(),
+                           S.saddles64.as<int64_t>(), c->stream));
+    c->stats.kernel_launches += 2;
     CK(cudaEventRecord(c->ev[3], c->stream));
 
     // beta0+ per saddle and slot offsets (sum beta0+ = raw arcs)

@@ -99,6 +99,8 @@ size_t compact_scratch_bytes(int64_t n);
 cudaError_t launch_compact_bits(const uint32_t *bits, int64_t n, int64_t v0, void *scratch, int32_t *out32,
                                 int64_t *out64, int64_t *d_count, cudaStream_t st);
 cudaError_t launch_count_bits(const uint32_t *bits, int64_t n, void *scratch, int64_t *d_count, cudaStream_t st);
+cudaError_t launch_emit_counted(const uint32_t *bits, int64_t n, int64_t v0, const void *scratch, int32_t *out32,
+                                int64_t *out64, cudaStream_t st);
 
 // S4 for grids and CSR.
 cudaError_t launch_saddle_beta_grid(const LinkTable *d_tab, int ndim, FieldView F, const int32_t *saddles,

@@ -127,6 +127,19 @@ cudaError_t launch_compact_bits(const uint32_t *bits, int64_t n, int64_t v0, voi
     return cudaMemcpyAsync(d_count, off + chunks, sizeof(int64_t), cudaMemcpyDeviceToDevice, st);
 }
 
+// emission using the chunk offsets a previous launch_count_bits left in `scratch`
+cudaError_t launch_emit_counted(const uint32_t *bits, int64_t n, int64_t v0, const void *scratch, int32_t *out32,
+                                int64_t *out64, cudaStream_t st) {
+    const int64_t words = (n + 31) / 32;
+    const int64_t chunks = (words + kCompactBS - 1) / kCompactBS;
+    if (n <= 0) return cudaSuccess;
+    const char *p = static_cast<const char *>(scratch);
+    p += (size_t(chunks) * 4 + 15) / 16 * 16 + 16;
+    const int64_t *off = reinterpret_cast<const int64_t *>(p);
+    k_emit_bits<<<unsigned(chunks), kCompactBS, 0, st>>>(bits, words, n, v0, off, out32, out64);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_count_bits(const uint32_t *bits, int64_t n, void *scratch, int64_t *d_count, cudaStream_t st) {
     const int64_t words = (n + 31) / 32;
     const int64_t chunks = (words + kCompactBS - 1) / kCompactBS;

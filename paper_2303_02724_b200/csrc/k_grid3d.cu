@@ -231,18 +231,25 @@ __global__ void __launch_bounds__(kThreads, 2)
             tma_load_3d(fbox + shift, &tmap, bar, xs < 0 ? 0 : xs, ys < 0 ? 0 : ys, zs < 0 ? 0 : zs);
         }
     } else {
-        for (int i = tid; i < BOX; i += kThreads) {
-            const int bx = i % BX, r = i / BX;
-            const int by = r % BY, bz = r / BY;
-            const int gx = x0 + bx - XO, gy = y0 + by - 1, gz = z0 + bz - 1;
-            float v = 0.f;
-            if (gx >= 0 && gx < D.nx && gy >= 0 && gy < D.ny && gz >= 0 && gz < D.nz) {
-                const int64_t o = int64_t(gy) * D.nx + gx;
-                if (gz >= A.z_lo && gz < A.z_hi) v = __ldg(A.f + (int64_t(gz - A.z_lo) * D.ny * D.nx + o));
-                else if (gz == A.z_lo - 1 && A.f_lo) v = __ldg(A.f_lo + o);
-                else if (gz == A.z_hi && A.f_hi) v = __ldg(A.f_hi + o);
+        // one warp per box row: the row's source (owned planes, a halo plane
+        // of a neighbour slab, or nothing) is decided once per row
+        const int lane = tid & 31;
+        for (int row = tid >> 5; row < BY * BZ; row += kThreads / 32) {
+            const int by = row % BY, bz = row / BY;
+            const int gy = y0 + by - 1, gz = z0 + bz - 1;
+            const float *src = nullptr;
+            if (gy >= 0 && gy < D.ny && gz >= 0 && gz < D.nz) {
+                const int64_t o = int64_t(gy) * D.nx;
+                if (gz >= A.z_lo && gz < A.z_hi) src = A.f + (int64_t(gz - A.z_lo) * D.ny * D.nx + o);
+                else if (gz == A.z_lo - 1) src = A.f_lo ? A.f_lo + o : nullptr;
+                else if (gz == A.z_hi) src = A.f_hi ? A.f_hi + o : nullptr;
             }
-            fbox[i] = v;
+            float *dst = fbox + row * BX;
+#pragma unroll
+            for (int b = lane; b < BX; b += 32) {
+                const int gx = x0 + b - XO;
+                dst[b] = (src && gx >= 0 && gx < D.nx) ? __ldg(src + gx) : 0.f;
+            }
         }
     }
     // halo / padding cells of the pointer box are terminal (point to themselves)

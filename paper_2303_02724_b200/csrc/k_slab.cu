@@ -87,19 +87,22 @@ cudaError_t launch_bval_update(int32_t *bval, const int32_t *hval_lo, const int3
     return cudaGetLastError();
 }
 
-// Final pass.  A warp owns 4 words of owned vertices (128 vertices).
+// Final pass.  A warp owns kW words of owned vertices (32 kW vertices); the
+// loads of all of them are issued before any is used (memory-level
+// parallelism for the dependent gather).
+constexpr int kW = 8;
 __global__ void __launch_bounds__(256) k_finalize(int32_t *label, const uint32_t *__restrict__ bits, int64_t v0,
                                                   int64_t v1, const int32_t *__restrict__ hlo,
                                                   const int32_t *__restrict__ hhi, int64_t plane) {
     const int64_t n = v1 - v0;
     const int64_t words = (n + 31) / 32;
-    const int64_t w0 = (int64_t(blockIdx.x) * (blockDim.x / 32) + (threadIdx.x >> 5)) * 4;
+    const int64_t w0 = (int64_t(blockIdx.x) * (blockDim.x / 32) + (threadIdx.x >> 5)) * kW;
     if (w0 >= words) return;
     const int lane = threadIdx.x & 31;
-    bool need[4];
-    int32_t e[4];
+    bool need[kW];
+    int32_t e[kW];
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
+    for (int k = 0; k < kW; ++k) {
         const int64_t i = (w0 + k) * 32 + lane;
         if (bits) {
             const uint32_t b = (w0 + k < words) ? __ldg(bits + w0 + k) : 0u;
@@ -109,9 +112,19 @@ __global__ void __launch_bounds__(256) k_finalize(int32_t *label, const uint32_t
         }
     }
 #pragma unroll
-    for (int k = 0; k < 4; ++k) e[k] = need[k] ? label[(w0 + k) * 32 + lane] : 0;
+    for (int k = 0; k < kW; ++k) e[k] = need[k] ? label[(w0 + k) * 32 + lane] : 0;
+    if (!hlo && !hhi) {
+        // one slab: every exit target is owned and final
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
+        for (int k = 0; k < kW; ++k)
+            if (need[k] && e[k] < 0) e[k] = __ldg(label + ((e[k] & 0x7fffffff) - v0));
+#pragma unroll
+        for (int k = 0; k < kW; ++k)
+            if (need[k]) label[(w0 + k) * 32 + lane] = e[k];
+        return;
+    }
+#pragma unroll
+    for (int k = 0; k < kW; ++k) {
         need[k] = need[k] && e[k] < 0;
         if (need[k]) {
             int64_t x = e[k] & 0x7fffffff;
@@ -127,7 +140,7 @@ __global__ void __launch_bounds__(256) k_finalize(int32_t *label, const uint32_t
         }
     }
 #pragma unroll
-    for (int k = 0; k < 4; ++k)
+    for (int k = 0; k < kW; ++k)
         if (need[k]) label[(w0 + k) * 32 + lane] = e[k];
 }
 
@@ -135,7 +148,7 @@ cudaError_t launch_finalize(int32_t *label, const uint32_t *bits, int64_t v0, in
                             const int32_t *hval_hi, int64_t plane, cudaStream_t st) {
     const int64_t words = (v1 - v0 + 31) / 32;
     if (words <= 0) return cudaSuccess;
-    k_finalize<<<blocks_for(words, 32), 256, 0, st>>>(label, bits, v0, v1, hval_lo, hval_hi, plane);
+    k_finalize<<<blocks_for(words, 8 * kW), 256, 0, st>>>(label, bits, v0, v1, hval_lo, hval_hi, plane);
     return cudaGetLastError();
 }
 
