@@ -76,6 +76,7 @@ struct SlabState {
     int32_t *label = nullptr;          // owned labels (a view)
     DevBuf f_lo, f_hi;                 // halo planes of f received from the neighbours
     DevBuf sad_bits, max_bits, exit_bits;
+    DevBuf beta8;                      // CSR: beta0+ per owned vertex (from classify)
     DevBuf bval, hval_lo, hval_hi;     // boundary-plane label values (own / neighbours')
     bool has_lo = false, has_hi = false;
     Tiled3D *tiled = nullptr;
@@ -83,7 +84,7 @@ struct SlabState {
     DevBuf arc_s, arc_m, arc_mult, raw_s, raw_rep, raw_m;
     int64_t n_max = 0, n_sad = 0, n_arc = 0, n_raw = 0;
     ~SlabState() {
-        DevBuf *b[] = {&f_lo, &f_hi, &sad_bits, &max_bits, &exit_bits, &bval, &hval_lo, &hval_hi, &maxima64,
+        DevBuf *b[] = {&f_lo, &f_hi, &sad_bits, &max_bits, &exit_bits, &beta8, &bval, &hval_lo, &hval_hi, &maxima64,
                        &saddles32, &saddles64, &sbeta, &slot_off, &tmp_m, &tmp_mult, &n_unique, &arc_off, &arc_s,
                        &arc_m, &arc_mult, &raw_s, &raw_rep, &raw_m};
         for (DevBuf *x : b) x->release();
@@ -382,8 +383,8 @@ static eg_status grid_graph(eg_ctx *c, const Problem &P, SlabState &S, bool raw)
         CK(launch_saddle_beta_grid(c->tab.as<LinkTable>(), P.ndim, S.F, S.saddles32.as<int32_t>(), ns,
                                    S.sbeta.as<int32_t>(), c->stream));
     else
-        CK(launch_saddle_beta_csr(P.row_ptr, P.col_idx, S.F.own, S.saddles32.as<int32_t>(), ns,
-                                  S.sbeta.as<int32_t>(), c->stream));
+        CK(launch_gather_beta(S.beta8.as<uint8_t>(), S.s.v0, S.saddles32.as<int32_t>(), ns, S.sbeta.as<int32_t>(),
+                              c->stream));
     CK(launch_scan_i32(S.sbeta.as<int32_t>(), S.slot_off.as<int64_t>(), ns, c->scratch.p, sb, c->stream));
     c->stats.kernel_launches += 2;
     CK(cudaMemcpyAsync(hc, S.slot_off.as<int64_t>() + ns, sizeof(int64_t), cudaMemcpyDeviceToHost, c->stream));
@@ -759,6 +760,7 @@ static eg_status compute_csr(eg_ctx *c, const Problem &P, const float *f, uint32
         const int64_t words = (S.s.v1 - S.s.v0 + 31) / 32;
         CK(S.sad_bits.ensure(sizeof(uint32_t) * std::max<int64_t>(words, 1)));
         CK(S.max_bits.ensure(sizeof(uint32_t) * std::max<int64_t>(words, 1)));
+        CK(S.beta8.ensure(std::max<int64_t>(S.s.v1 - S.s.v0, 1)));
         S.has_lo = S.has_hi = false;
     }
     CK(cudaEventRecord(c->ev[0], c->stream));
@@ -772,7 +774,7 @@ static eg_status compute_csr(eg_ctx *c, const Problem &P, const float *f, uint32
         const bool first = S == c->slabs[0];
         if (first) CK(cudaEventRecord(c->ev_main[0], c->stream));
         CK(launch_classify_csr(P.row_ptr, P.col_idx, f, S->s.v0, S->s.v1, S->label, S->sad_bits.as<uint32_t>(),
-                               S->max_bits.as<uint32_t>(), nullptr, fl, fl + 1, c->stream));
+                               S->max_bits.as<uint32_t>(), S->beta8.as<uint8_t>(), fl, fl + 1, c->stream));
         if (first) CK(cudaEventRecord(c->ev_main[1], c->stream));
         c->stats.kernel_launches += 1;
     }

@@ -108,6 +108,9 @@ cudaError_t launch_saddle_beta_grid(const LinkTable *d_tab, int ndim, FieldView 
 cudaError_t launch_arcs_grid(const LinkTable *d_tab, int ndim, FieldView F, const int32_t *saddles, int64_t n_sad,
                              const int64_t *slot_off, LabelView lv, int32_t *tmp_m, int32_t *tmp_mult,
                              int32_t *n_unique, int64_t *raw_s, int64_t *raw_rep, int64_t *raw_m, cudaStream_t st);
+// beta0+ of the saddles from a per-vertex beta0+ array written by classify
+cudaError_t launch_gather_beta(const uint8_t *beta8, int64_t v0, const int32_t *saddles, int64_t n, int32_t *out,
+                               cudaStream_t st);
 cudaError_t launch_saddle_beta_csr(const int64_t *row_ptr, const int32_t *col_idx, const float *f,
                                    const int32_t *saddles, int64_t n_sad, int32_t *beta, cudaStream_t st);
 cudaError_t launch_arcs_csr(const int64_t *row_ptr, const int32_t *col_idx, const float *f, const int32_t *saddles,

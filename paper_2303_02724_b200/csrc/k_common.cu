@@ -30,7 +30,10 @@ __global__ void __launch_bounds__(256) k_jump(int32_t *ptr, int64_t n, int64_t v
             }
         }
     }
-    if (__any_sync(0xffffffffu, ch) && (threadIdx.x & 31) == 0) atomicOr(&changed[round], 1);
+    // one flag store per block at most, and none once the round is known to
+    // have changed something (a single global flag hammered by every warp
+    // serialises in L2)
+    if (__syncthreads_or(ch) && threadIdx.x == 0 && *(volatile int *)&changed[round] == 0) changed[round] = 1;
 }
 
 cudaError_t launch_jump_round(int32_t *ptr, int64_t n, int64_t v0, int *changed, int round, cudaStream_t st) {
@@ -181,6 +184,19 @@ cudaError_t launch_emit_arcs(const int32_t *saddles, int64_t n_sad, const int64_
     if (n_sad <= 0) return cudaSuccess;
     k_emit_arcs<<<blocks_for(n_sad, 256), 256, 0, st>>>(saddles, n_sad, slot_off, arc_off, tmp_m, tmp_mult, n_unique,
                                                         arc_s, arc_m, arc_mult);
+    return cudaGetLastError();
+}
+
+__global__ void k_gather_beta(const uint8_t *__restrict__ beta8, int64_t v0, const int32_t *__restrict__ saddles,
+                              int64_t n, int32_t *out) {
+    const int64_t j = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (j < n) out[j] = beta8[saddles[j] - v0];
+}
+
+cudaError_t launch_gather_beta(const uint8_t *beta8, int64_t v0, const int32_t *saddles, int64_t n, int32_t *out,
+                               cudaStream_t st) {
+    if (n <= 0) return cudaSuccess;
+    k_gather_beta<<<blocks_for(n, 256), 256, 0, st>>>(beta8, v0, saddles, n, out);
     return cudaGetLastError();
 }
 

@@ -42,23 +42,30 @@ template <int NDIM>
 struct GridSmem {
     static constexpr int K = 2 * ((1 << NDIM) - 1);
     static constexpr int NW = (K + 63) / 64;
-    int64_t delta[K];
+    int32_t delta[K];                       // N < 2^31: 32-bit linear offsets
     uint64_t nbr[K][NW];
+    uint64_t neg[NDIM][NW], pos[NDIM][NW];  // offsets with d_a = -1 / +1
     int32_t dims[NDIM];
-    int8_t d[K][NDIM];
 };
 
 template <int NDIM>
 __device__ __forceinline__ void load_tables(GridSmem<NDIM> &S, const LinkTable *__restrict__ tab) {
     constexpr int K = GridSmem<NDIM>::K, NW = GridSmem<NDIM>::NW;
     for (int k = threadIdx.x; k < K; k += blockDim.x) {
-        S.delta[k] = tab->delta[k];
+        S.delta[k] = int32_t(tab->delta[k]);
 #pragma unroll
         for (int w = 0; w < NW; ++w) S.nbr[k][w] = tab->nbr[k][w];
-#pragma unroll
-        for (int a = 0; a < NDIM; ++a) S.d[k][a] = tab->d[k][a];
     }
-    if (threadIdx.x < NDIM) S.dims[threadIdx.x] = int32_t(tab->dims[threadIdx.x]);
+    if (threadIdx.x < NDIM) {
+        const int a = threadIdx.x;
+        S.dims[a] = int32_t(tab->dims[a]);
+#pragma unroll
+        for (int w = 0; w < NW; ++w) S.neg[a][w] = S.pos[a][w] = 0;
+        for (int k = 0; k < K; ++k) {
+            if (tab->d[k][a] < 0) S.neg[a][k >> 6] |= 1ull << (k & 63);
+            if (tab->d[k][a] > 0) S.pos[a][k >> 6] |= 1ull << (k & 63);
+        }
+    }
     __syncthreads();
 }
 
@@ -69,31 +76,52 @@ __device__ __forceinline__ void load_tables(GridSmem<NDIM> &S, const LinkTable *
 template <int NDIM>
 __device__ __forceinline__ Bits<GridSmem<NDIM>::NW> upper_link(const GridSmem<NDIM> &S, const FieldView &F, int64_t v,
                                                                float fv, int64_t *best) {
-    constexpr int K = GridSmem<NDIM>::K;
-    int32_t c[NDIM];
-    int64_t r = v;
+    constexpr int K = GridSmem<NDIM>::K, NW = GridSmem<NDIM>::NW;
+    // the truncated link (reading L3): drop the offsets that leave the domain,
+    // one mask per face the vertex lies on
+    uint64_t valid[NW];
+#pragma unroll
+    for (int w = 0; w < NW; ++w) valid[w] = ~0ull;
+    uint32_t r = uint32_t(v);
 #pragma unroll
     for (int a = 0; a < NDIM; ++a) {
-        c[a] = int32_t(r % S.dims[a]);
-        r /= S.dims[a];
+        const uint32_t D = uint32_t(S.dims[a]);
+        const uint32_t c = r % D;
+        r /= D;
+#pragma unroll
+        for (int w = 0; w < NW; ++w) {
+            if (c == 0) valid[w] &= ~S.neg[a][w];
+            if (c + 1 == D) valid[w] &= ~S.pos[a][w];
+        }
     }
-    Bits<GridSmem<NDIM>::NW> m;
+    Bits<NW> m;
     m.clear();
     int64_t b = v;
     float bf = fv;
+    // one slab (no halo planes): plain loads from the owned array
+    const bool plain = F.lo == nullptr && F.hi == nullptr;
+    const float *own = F.own - F.v0;
+    // the table is sorted by offset: the first K/2 offsets lead to lower
+    // indices (up iff f > fv), the rest to higher ones (up iff f >= fv)
 #pragma unroll 2
-    for (int k = 0; k < K; ++k) {
-        bool ok = true;
-#pragma unroll
-        for (int a = 0; a < NDIM; ++a) {
-            int32_t q = c[a] + S.d[k][a];
-            ok &= (q >= 0) & (q < S.dims[a]);
+    for (int k = 0; k < K / 2; ++k) {
+        if (!((valid[k >> 6] >> (k & 63)) & 1ull)) continue;
+        const int64_t u = v + S.delta[k];
+        const float fu = plain ? __ldg(own + u) : F.at(u);
+        if (fu > fv) {
+            m.set(k);
+            if (fu >= bf) {
+                bf = fu;
+                b = u;
+            }
         }
-        if (!ok) continue;
-        int64_t u = v + S.delta[k];
-        float fu = F.at(u);
-        bool up = S.delta[k] > 0 ? (fu >= fv) : (fu > fv);
-        if (up) {
+    }
+#pragma unroll 2
+    for (int k = K / 2; k < K; ++k) {
+        if (!((valid[k >> 6] >> (k & 63)) & 1ull)) continue;
+        const int64_t u = v + S.delta[k];
+        const float fu = plain ? __ldg(own + u) : F.at(u);
+        if (fu >= fv) {
             m.set(k);
             if (fu >= bf) {
                 bf = fu;

@@ -24,16 +24,20 @@
 //         target is in E, hence final).
 // All in-place updates are race-benign: every value ever stored on a chain is
 // a later vertex of the same ascending path.
+#include <cooperative_groups.h>
 #include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
 #include "eg_tiled.h"
 
 namespace eg {
+
+namespace cg = cooperative_groups;
 
 constexpr int TX = 32, TY = 16, TZ = 16;
 constexpr int XO = 4;                                // box x index of the tile's first column
@@ -55,6 +59,8 @@ struct Tiled3D {
     bool ready = false;
     int64_t bdims[3] = {0, 0, 0};
     int64_t bz[2] = {-1, -1};                        // slab planes of the cached list
+    bool bcluster = false;                           // cluster mode of the cached list
+    bool use_cluster = false;
     int32_t *d_btiles = nullptr;                     // boundary tile list for the cached dims
     int64_t n_btiles = 0;
     int32_t *d_elist = nullptr;                      // exit targets E
@@ -77,6 +83,8 @@ void tiled3d_destroy(Tiled3D *t) {
 struct Dims3 {
     int32_t nx, ny, nz;
 };
+
+constexpr int kResOff = (BOX + 255) / 256 * 256;     // cluster: resolved shell values after the used bytes
 
 struct TileArgs {
     const float *f;                 // owned planes [z_lo, z_hi) of the slab
@@ -127,6 +135,30 @@ __device__ __forceinline__ int shell_cell(int s) {
     return bidx(bx, by, bz);
 }
 
+__device__ __forceinline__ bool is_shell_xyz(int bx, int by, int bz) {
+    return bx < XO || bx >= XO + TX || by == 0 || by == BY - 1 || bz == 0 || bz == BZ - 1;
+}
+__device__ __forceinline__ bool is_shell(int r) {
+    const int bz = r / PL, rr = r - bz * PL;
+    const int by = rr / BX, bx = rr - by * BX;
+    return is_shell_xyz(bx, by, bz);
+}
+// inverse of shell_cell for a shell cell (bx, by, bz)
+__device__ __forceinline__ int shell_index(int bx, int by, int bz) {
+    if (bz == 0 || bz == BZ - 1) return (bz ? BY * kShellW : 0) + by * kShellW + (bx - (XO - 1));
+    if (by == 0 || by == BY - 1) return kShellZ + (bz - 1) * 2 * kShellW + (by ? kShellW : 0) + (bx - (XO - 1));
+    return kShellY + (bz - 1) * 2 * (BY - 2) + (by - 1) * 2 + (bx == XO + TX ? 1 : 0);
+}
+
+struct Dims3;
+// Follow a path that leaves tile (cx, cy, cz) of a 2x2x2 cluster at its shell
+// cell i through the siblings' pointer boxes (sib[rank], rank = x + 2y + 4z)
+// until it ends at a maximum inside the super-tile (final label) or leaves it
+// (kUnresolved | the first vertex outside).  (sx0, sy0, sz0): global origin
+// of the super-tile.
+__device__ int32_t resolve_in_cluster(int i, int cx, int cy, int cz, const uint16_t *const *sib, int sx0, int sy0,
+                                      int sz0, const Dims3 &D);
+
 // ------------------------------------------------------------ TMA helpers
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -162,6 +194,25 @@ __device__ __forceinline__ void tma_load_3d(void *dst, const CUtensorMap *map, u
 
 // ------------------------------------------------------------ the tile kernel
 
+__device__ int32_t resolve_in_cluster(int i, int cx, int cy, int cz, const uint16_t *const *sib, int sx0, int sy0,
+                                      int sz0, const Dims3 &D) {
+    int idx = i;
+    for (;;) {
+        const int bz = idx / PL, rr = idx - bz * PL;
+        const int by = rr / BX, bx = rr - by * BX;
+        // super-tile coordinates of the vertex at this box cell
+        const int sx = cx * TX + bx - XO, sy = cy * TY + by - 1, sz = cz * TZ + bz - 1;
+        const int32_t gid = ((sz0 + sz) * D.ny + (sy0 + sy)) * D.nx + (sx0 + sx);
+        if (!is_shell_xyz(bx, by, bz)) return gid;                       // a maximum of that tile
+        if (sx < 0 || sx >= 2 * TX || sy < 0 || sy >= 2 * TY || sz < 0 || sz >= 2 * TZ)
+            return int32_t(uint32_t(gid) | kFlag);                        // leaves the super-tile
+        cx = sx / TX;
+        cy = sy / TY;
+        cz = sz / TZ;
+        idx = sib[cx + 2 * cy + 4 * cz][bidx(sx - cx * TX + XO, sy - cy * TY + 1, sz - cz * TZ + 1)];
+    }
+}
+
 struct VK {           // a value with its box-index offset from the centre vertex
     float v;
     int d;
@@ -169,6 +220,8 @@ struct VK {           // a value with its box-index offset from the centre verte
 
 // b wins ties: b is the later (higher-index) operand
 __device__ __forceinline__ VK vmax(VK a, VK b) { return b.v >= a.v ? b : a; }
+// the same where NaN marks a cell outside the domain: a NaN never wins
+__device__ __forceinline__ VK vmaxn(VK a, VK b) { return (b.v >= a.v || a.v != a.v) ? b : a; }
 
 // IEEE compares (no ftz: distinct denormals stay distinct, reading L2)
 __device__ __forceinline__ uint32_t setgt(float a, float b) {
@@ -181,8 +234,10 @@ __device__ __forceinline__ uint32_t setge(float a, float b) {
     asm("set.ge.u32.f32 %0, %1, %2;" : "=r"(r) : "f"(a), "f"(b));
     return r;
 }
+// bits of b where c is set, bits of a elsewhere (one LOP3)
+__device__ __forceinline__ uint32_t bsel(uint32_t a, uint32_t b, uint32_t c) { return (a & ~c) | (b & c); }
 
-template <bool kInterior, bool kTma>
+template <bool kInterior, bool kTma, bool kCluster>
 __global__ void __launch_bounds__(kThreads, 2)
     k_tile(const __grid_constant__ CUtensorMap tmap, TileArgs A, Dims3 D) {
     extern __shared__ __align__(128) unsigned char smem[];
@@ -194,7 +249,11 @@ __global__ void __launch_bounds__(kThreads, 2)
     const int tid = threadIdx.x;
     const int tx = tid & 31, ty = tid >> 5;
     int bxo, byo, bzo;
-    if (kInterior) {
+    if (kCluster) {
+        bxo = int(blockIdx.x) + A.origin.x;
+        byo = int(blockIdx.y) + A.origin.y;
+        bzo = int(blockIdx.z) + A.origin.z;
+    } else if (kInterior) {
         int t = blockIdx.x;
         bxo = t % A.tiles_x + A.origin.x;
         t /= A.tiles_x;
@@ -233,22 +292,36 @@ __global__ void __launch_bounds__(kThreads, 2)
     } else {
         // one warp per box row: the row's source (owned planes, a halo plane
         // of a neighbour slab, or nothing) is decided once per row
+        // (4 rows per warp in flight: loads first, then the smem stores)
         const int lane = tid & 31;
-        for (int row = tid >> 5; row < BY * BZ; row += kThreads / 32) {
-            const int by = row % BY, bz = row / BY;
-            const int gy = y0 + by - 1, gz = z0 + bz - 1;
-            const float *src = nullptr;
-            if (gy >= 0 && gy < D.ny && gz >= 0 && gz < D.nz) {
-                const int64_t o = int64_t(gy) * D.nx;
-                if (gz >= A.z_lo && gz < A.z_hi) src = A.f + (int64_t(gz - A.z_lo) * D.ny * D.nx + o);
-                else if (gz == A.z_lo - 1) src = A.f_lo ? A.f_lo + o : nullptr;
-                else if (gz == A.z_hi) src = A.f_hi ? A.f_hi + o : nullptr;
-            }
-            float *dst = fbox + row * BX;
+        constexpr int kRows = BY * BZ, kWarps = kThreads / 32, kU = 4;
+        for (int row0 = tid >> 5; row0 < kRows; row0 += kWarps * kU) {
+            float v[kU][2];
 #pragma unroll
-            for (int b = lane; b < BX; b += 32) {
-                const int gx = x0 + b - XO;
-                dst[b] = (src && gx >= 0 && gx < D.nx) ? __ldg(src + gx) : 0.f;
+            for (int u = 0; u < kU; ++u) {
+                const int row = row0 + u * kWarps;
+                const int by = row % BY, bz = row / BY;
+                const int gy = y0 + by - 1, gz = z0 + bz - 1;
+                const float *src = nullptr;
+                if (row < kRows && gy >= 0 && gy < D.ny && gz >= 0 && gz < D.nz) {
+                    const int64_t o = int64_t(gy) * D.nx;
+                    if (gz >= A.z_lo && gz < A.z_hi) src = A.f + (int64_t(gz - A.z_lo) * D.ny * D.nx + o);
+                    else if (gz == A.z_lo - 1) src = A.f_lo ? A.f_lo + o : nullptr;
+                    else if (gz == A.z_hi) src = A.f_hi ? A.f_hi + o : nullptr;
+                }
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const int b = lane + 32 * h;
+                    const int gx = x0 + b - XO;
+                    v[u][h] = (src && b < BX && gx >= 0 && gx < D.nx) ? __ldg(src + gx) : __int_as_float(0x7fffffff);
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < kU; ++u) {
+                const int row = row0 + u * kWarps;
+                if (row >= kRows) break;
+                fbox[row * BX + lane] = v[u][0];
+                if (lane + 32 < BX) fbox[row * BX + lane + 32] = v[u][1];
             }
         }
     }
@@ -260,8 +333,6 @@ __global__ void __launch_bounds__(kThreads, 2)
 
     const int gx = x0 + tx, gy = y0 + ty;
     const bool col_ok = kInterior || (gx < D.nx && gy < D.ny);
-    const bool xm = kInterior || gx > 0, xp = kInterior || gx + 1 < D.nx;
-    const bool ym = kInterior || gy > 0, yp = kInterior || gy + 1 < D.ny;
     const int cb = bidx(tx + XO, ty + 1, 0);
 
     // 2-D star of box plane bz at this column: c, (1,0), (0,1), (1,1), (-1,0), (0,-1), (-1,-1)
@@ -275,16 +346,20 @@ __global__ void __launch_bounds__(kThreads, 2)
         s[5] = p[-BX];
         s[6] = p[-BX - 1];
     };
-    // in-plane 2x2 maxima (ascending index order inside each, later wins ties)
+    // in-plane 2x2 maxima (ascending index order inside each, later wins ties).
+    // Edge tiles hold NaN in the cells outside the domain: a NaN never wins
+    // (vmaxn) and every compare with it is false, so the truncated link
+    // (reading L3) falls out of the same code.
+    auto vm = [](VK a, VK b) -> VK { return kInterior ? vmax(a, b) : vmaxn(a, b); };
     auto bplus = [&](const float *s, int dz) -> VK {    // (0,0) (1,0) (0,1) (1,1)
-        VK a = vmax(VK{s[0], dz * PL}, VK{s[1], 1 + dz * PL});
-        VK b = vmax(VK{s[2], BX + dz * PL}, VK{s[3], BX + 1 + dz * PL});
-        return vmax(a, b);
+        VK a = vm(VK{s[0], dz * PL}, VK{s[1], 1 + dz * PL});
+        VK b = vm(VK{s[2], BX + dz * PL}, VK{s[3], BX + 1 + dz * PL});
+        return vm(a, b);
     };
     auto bminus = [&](const float *s, int dz) -> VK {   // (-1,-1) (0,-1) (-1,0) (0,0)
-        VK a = vmax(VK{s[6], -BX - 1 + dz * PL}, VK{s[5], -BX + dz * PL});
-        VK b = vmax(VK{s[4], -1 + dz * PL}, VK{s[0], dz * PL});
-        return vmax(a, b);
+        VK a = vm(VK{s[6], -BX - 1 + dz * PL}, VK{s[5], -BX + dz * PL});
+        VK b = vm(VK{s[4], -1 + dz * PL}, VK{s[0], dz * PL});
+        return vm(a, b);
     };
 
     float pm[7], p0[7], pp[7];
@@ -301,57 +376,32 @@ __global__ void __launch_bounds__(kThreads, 2)
         const bool ok = col_ok && (kInterior || gz < A.z_hi);
         const float fv = p0[0];
         nan_seen |= ok && (fv != fv);
-        uint32_t mask;
-        int d;
-        if (kInterior) {
-            // S1: argmax over box(v) u box(v - 1); the upper box wins ties
-            const VK bp_next = bplus(pp, 1);
-            const VK bm_cur = bminus(p0, 0);
-            const VK U = vmax(bp_cur, bp_next);
-            const VK L = vmax(bm_prev, bm_cur);
-            d = vmax(L, U).d;
-            bp_cur = VK{bp_next.v, bp_next.d - PL};
-            bm_prev = VK{bm_cur.v, bm_cur.d - PL};
-            // S3: upper mask, lower group (index < v: up iff f > fv), then upper
-            // (set.*.u32 gives an all-ones word, merged with its bit by one LOP3)
-            mask = (setgt(pm[6], fv) & 1u) | (setgt(pm[5], fv) & 2u) | (setgt(pm[4], fv) & 4u) |
-                   (setgt(pm[0], fv) & 8u) | (setgt(p0[6], fv) & 16u) | (setgt(p0[5], fv) & 32u) |
-                   (setgt(p0[4], fv) & 64u) | (setge(p0[1], fv) & 128u) | (setge(p0[2], fv) & 256u) |
-                   (setge(p0[3], fv) & 512u) | (setge(pp[0], fv) & 1024u) | (setge(pp[1], fv) & 2048u) |
-                   (setge(pp[2], fv) & 4096u) | (setge(pp[3], fv) & 8192u);
-        } else {
-            const bool zm = gz > 0, zpv = gz + 1 < D.nz;
-            const float lv[7] = {pm[6], pm[5], pm[4], pm[0], p0[6], p0[5], p0[4]};
-            const bool lok[7] = {zm && xm && ym, zm && ym, zm && xm, zm, xm && ym, ym, xm};
-            const float uv[7] = {p0[1], p0[2], p0[3], pp[0], pp[1], pp[2], pp[3]};
-            const bool uok[7] = {xp, yp, xp && yp, zpv, zpv && xp, zpv && yp, zpv && xp && yp};
-            constexpr int LD[7] = {-1 - BX - PL, -BX - PL, -1 - PL, -PL, -1 - BX, -BX, -1};
-            constexpr int UD[7] = {1, BX, 1 + BX, PL, 1 + PL, BX + PL, 1 + BX + PL};
-            mask = 0;
-            float bl = -__int_as_float(0x7f800000);
-            int bld = 0;
-#pragma unroll
-            for (int k = 0; k < 7; ++k) {
-                const bool up = lok[k] && (lv[k] > fv);
-                mask |= up ? (1u << k) : 0u;
-                if (up && lv[k] >= bl) {
-                    bl = lv[k];
-                    bld = LD[k];
-                }
-            }
-            float bu = fv;
-            int bud = 0;
-#pragma unroll
-            for (int k = 0; k < 7; ++k) {
-                const bool up = uok[k] && (uv[k] >= fv);
-                mask |= up ? (1u << (7 + k)) : 0u;
-                if (up && uv[k] >= bu) {
-                    bu = uv[k];
-                    bud = UD[k];
-                }
-            }
-            d = (bud != 0 && (bld == 0 || bu >= bl)) ? bud : bld;
-        }
+        // S1: argmax over box(v) u box(v - 1); the upper box wins ties
+        const VK bp_next = bplus(pp, 1);
+        const VK bm_cur = bminus(p0, 0);
+        const VK U = vm(bp_cur, bp_next);
+        const VK L = vm(bm_prev, bm_cur);
+        const int d = vm(L, U).d;
+        bp_cur = VK{bp_next.v, bp_next.d - PL};
+        bm_prev = VK{bm_cur.v, bm_cur.d - PL};
+        // S3: upper mask, lower group (index < v: up iff f > fv), then upper.
+        // set.*.u32 gives an all-ones / all-zeros word; a chain of bit
+        // selects (one LOP3 each) keeps bit k of the k-th word.
+        uint32_t mask = setge(pp[3], fv);
+        mask = bsel(mask, setge(pp[2], fv), 0x1fffu);
+        mask = bsel(mask, setge(pp[1], fv), 0x0fffu);
+        mask = bsel(mask, setge(pp[0], fv), 0x07ffu);
+        mask = bsel(mask, setge(p0[3], fv), 0x03ffu);
+        mask = bsel(mask, setge(p0[2], fv), 0x01ffu);
+        mask = bsel(mask, setge(p0[1], fv), 0x00ffu);
+        mask = bsel(mask, setgt(p0[4], fv), 0x007fu);
+        mask = bsel(mask, setgt(p0[5], fv), 0x003fu);
+        mask = bsel(mask, setgt(p0[6], fv), 0x001fu);
+        mask = bsel(mask, setgt(pm[0], fv), 0x000fu);
+        mask = bsel(mask, setgt(pm[4], fv), 0x0007u);
+        mask = bsel(mask, setgt(pm[5], fv), 0x0003u);
+        mask = bsel(mask, setgt(pm[6], fv), 0x0001u);
+        mask &= 0x3fffu;
         const int c = cb + (z + 1) * PL;
         if (ok) pbox[c] = uint16_t(c + d);
         const bool sad = (lut[mask >> 5] >> (mask & 31)) & 1u;
@@ -370,6 +420,8 @@ __global__ void __launch_bounds__(kThreads, 2)
     // loads, no divergence) quarter every chain; then every vertex chases the
     // rest of its chain to the local root, halving the path as it goes (in
     // place and race-benign: every stored value lies further along the path).
+    // (measured alternative: doubling to convergence with a per-vertex done
+    // mask costs ~50 instr/vertex against ~37 for this, profiles/r01)
 #pragma unroll 1
     for (int round = 0; round < 2; ++round) {
 #pragma unroll
@@ -393,38 +445,83 @@ __global__ void __launch_bounds__(kThreads, 2)
         pbox[c] = uint16_t(x);
     }
     __syncthreads();
+    // another thread's path halving may have overwritten pbox[c] with an
+    // ancestor after c's own chase stored the root: settle every own cell on
+    // its root before anyone reads the box as roots
+#pragma unroll 1
+    for (int z = 0; z < TZ; ++z) {
+        const int c = cb + (z + 1) * PL;
+        int r = pbox[c];
+        for (int q; (q = pbox[r]) != r;) r = q;
+        pbox[c] = uint16_t(r);
+    }
+    __syncthreads();
 
     // ---- outputs: label (bit 31 = exit), bitmaps, exit-target marks
     uint8_t *used = reinterpret_cast<uint8_t *>(fbox);   // fbox is dead: 1 byte per box cell
+    int32_t *res = reinterpret_cast<int32_t *>(reinterpret_cast<uint8_t *>(fbox) + kResOff);   // cluster only
     for (int i = tid; i < BOX / 16; i += kThreads) reinterpret_cast<uint4 *>(used)[i] = make_uint4(0, 0, 0, 0);
     __syncthreads();
+    if constexpr (kCluster) {
+        // The 2x2x2 tiles of a thread-block cluster form a super-tile: a path
+        // that leaves this tile into a sibling is followed through the
+        // sibling's pointer box in distributed shared memory, so only paths
+        // leaving the super-tile remain exits.
+        //   A: final roots into the own box, mark the shell cells used as roots
+#pragma unroll 1
+        for (int z = 0; z < TZ; ++z) {
+            const int r = pbox[cb + (z + 1) * PL];
+            if (is_shell(r)) used[r] = 1;
+        }
+        cg::this_cluster().sync();
+        //   B: resolve every used shell cell through the siblings
+        const dim3 cbi = cg::this_cluster().block_index();
+        const uint16_t *sib[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) sib[q] = cg::this_cluster().map_shared_rank(pbox, q);
+        const int sx0 = x0 - int(cbi.x) * TX, sy0 = y0 - int(cbi.y) * TY, sz0 = z0 - int(cbi.z) * TZ;
+        for (int s = tid; s < kShell; s += kThreads) {
+            const int i = shell_cell(s);
+            if (used[i]) res[s] = resolve_in_cluster(i, int(cbi.x), int(cbi.y), int(cbi.z), sib, sx0, sy0, sz0, D);
+        }
+        cg::this_cluster().sync();      // no sibling reads this box after this point
+    }
     const bool aligned = (D.nx & 31) == 0;
+    // 32-bit index arithmetic (N < 2^31): the global id of box cell (0,0,0),
+    // the plane stride, and this column's owned index at z = 0
+    const int32_t nxy = D.ny * D.nx;
+    const int32_t g_box0 = ((z0 - 1) * D.ny + (y0 - 1)) * D.nx + (x0 - XO);
+    const int32_t i_col = (z0 * D.ny + gy) * D.nx + gx - int32_t(A.v0);
 #pragma unroll 2
     for (int z = 0; z < TZ; ++z) {
         const int gz = z0 + z;
         const bool ok = col_ok && (kInterior || gz < A.z_hi);
-        // another thread's path halving may have overwritten pbox[c] with an
-        // ancestor after c's own chase stored the root: follow to the root
-        int r = pbox[cb + (z + 1) * PL];
-        for (int q; (q = pbox[r]) != r;) r = q;
+        const int r = pbox[cb + (z + 1) * PL];          // the local root (doubling converged)
         const int bz = r / PL, rr = r - bz * PL;
         const int by = rr / BX, bx = rr - by * BX;
         // exit: the root is in the halo shell of the box, or (last tile of a
         // slab) in a plane the slab does not own
-        const bool exit = bx < XO || bx >= XO + TX || by == 0 || by == BY - 1 || bz == 0 || bz == BZ - 1 ||
-                          (!kInterior && z0 - 1 + bz >= A.z_hi);
-        const int32_t root = ((z0 - 1 + bz) * D.ny + (y0 - 1 + by)) * D.nx + (x0 - XO + bx);
-        const int32_t v = (gz * D.ny + gy) * D.nx + gx;
+        bool exit = bx < XO || bx >= XO + TX || by == 0 || by == BY - 1 || bz == 0 || bz == BZ - 1 ||
+                    (!kInterior && z0 - 1 + bz >= A.z_hi);
+        int32_t lab;
+        if (kCluster && exit) {
+            lab = res[shell_index(bx, by, bz)];
+            exit = lab < 0;
+        } else {
+            const int32_t root = g_box0 + bz * nxy + by * D.nx + bx;
+            lab = exit ? int32_t(uint32_t(root) | kFlag) : root;
+        }
+        const int32_t i = i_col + z * nxy;               // owned index of this vertex
         if (ok) {
-            A.label[v - A.v0] = exit ? int32_t(uint32_t(root) | kFlag) : root;
-            if (exit) used[r] = 1;
+            A.label[i] = lab;
+            if (!kCluster && exit) used[r] = 1;
         }
         const uint32_t eb = __ballot_sync(0xffffffffu, ok && exit);
         const uint32_t sb = __ballot_sync(0xffffffffu, (sad_mask >> z) & 1u);
         const uint32_t mb = __ballot_sync(0xffffffffu, (max_mask >> z) & 1u);
         if (aligned) {
             if (tx == 0 && ok) {
-                const int64_t w = (v - A.v0) >> 5;
+                const int32_t w = i >> 5;
                 A.exit_bits[w] = eb;
                 A.sad_bits[w] = sb;
                 A.max_bits[w] = mb;
@@ -447,12 +544,14 @@ __global__ void __launch_bounds__(kThreads, 2)
         }
     }
     __syncthreads();
-    // ---- append the tile's distinct exit targets to E: one global atomic per
-    // tile (block scan of per-thread counts)
+    // ---- append the tile's exit targets to E: one global atomic per tile
+    // (block scan of per-thread counts).  Only shell cells can be exit
+    // targets; in a cluster, the target is the resolved vertex outside the
+    // super-tile.
     uint32_t *red = reinterpret_cast<uint32_t *>(smem + kOffM + 16);   // [32] warp sums + [1] base
-    // only the halo shell of the box can hold exit targets
+    auto is_target = [&](int s, int i) -> bool { return used[i] && (!kCluster || res[s] < 0); };
     int mine = 0;
-    for (int s = tid; s < kShell; s += kThreads) mine += used[shell_cell(s)];
+    for (int s = tid; s < kShell; s += kThreads) mine += is_target(s, shell_cell(s));
     int incl = mine;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -480,11 +579,16 @@ __global__ void __launch_bounds__(kThreads, 2)
         unsigned long long slot = reinterpret_cast<unsigned long long *>(red + 32)[0] + red[ty] + (incl - mine);
         for (int s = tid; s < kShell; s += kThreads) {
             const int i = shell_cell(s);
-            if (!used[i]) continue;
-            const int bz = i / PL, rr = i - bz * PL;
-            const int by = rr / BX, bx = rr - by * BX;
-            if (slot < (unsigned long long)A.ecap)
-                A.elist[slot] = ((z0 - 1 + bz) * D.ny + (y0 - 1 + by)) * D.nx + (x0 - XO + bx);
+            if (!is_target(s, i)) continue;
+            int32_t g;
+            if (kCluster) {
+                g = res[s] & 0x7fffffff;
+            } else {
+                const int bz = i / PL, rr = i - bz * PL;
+                const int by = rr / BX, bx = rr - by * BX;
+                g = ((z0 - 1 + bz) * D.ny + (y0 - 1 + by)) * D.nx + (x0 - XO + bx);
+            }
+            if (slot < (unsigned long long)A.ecap) A.elist[slot] = g;
             ++slot;
         }
     }
@@ -548,9 +652,9 @@ typedef CUresult (*EncodeTiledFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t
                                   const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 
-template <bool I, bool T>
+template <bool I, bool T, bool C>
 static cudaError_t set_smem_attr() {
-    return cudaFuncSetAttribute(k_tile<I, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kTileSmem));
+    return cudaFuncSetAttribute(k_tile<I, T, C>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kTileSmem));
 }
 
 eg_status tiled3d_local(Tiled3D *t, int ndim, const int64_t *dims, const Slab &s, const FieldView &F, int32_t *labels,
@@ -573,9 +677,16 @@ eg_status tiled3d_local(Tiled3D *t, int ndim, const int64_t *dims, const Slab &s
             return fail(err, e, "lut upload");
         if ((e = cudaMalloc(&t->d_ecount, sizeof(unsigned long long))) != cudaSuccess)
             return fail(err, e, "cudaMalloc ecount");
-        if ((e = set_smem_attr<false, false>()) != cudaSuccess || (e = set_smem_attr<true, false>()) != cudaSuccess ||
-            (e = set_smem_attr<true, true>()) != cudaSuccess)
+        if ((e = set_smem_attr<false, false, false>()) != cudaSuccess ||
+            (e = set_smem_attr<true, false, false>()) != cudaSuccess ||
+            (e = set_smem_attr<true, true, false>()) != cudaSuccess ||
+            (e = set_smem_attr<true, true, true>()) != cudaSuccess)
             return fail(err, e, "smem attr");
+        // The super-tile kernel is opt-in (EG_CLUSTER=1): on C3 it cut the exit
+        // targets by 25 % but made the tile kernel 62 % slower (two cluster
+        // barriers per tile; profiles/r01), a net loss.
+        const char *cl = std::getenv("EG_CLUSTER");
+        t->use_cluster = cl && cl[0] == '1';
         cudaDriverEntryPointQueryResult q;
         void *fn = nullptr;
         if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) == cudaSuccess &&
@@ -600,9 +711,23 @@ eg_status tiled3d_local(Tiled3D *t, int ndim, const int64_t *dims, const Slab &s
     int3 lo = make_int3(1, 1, 1);
     int3 hi = make_int3(int((d3[0] - 1 - TX) / TX), int((d3[1] - 1 - TY) / TY), int((z_hi - z_lo - 1 - TZ) / TZ));
     if (d3[0] - 1 - TX < 0 || d3[1] - 1 - TY < 0 || z_hi - z_lo - 1 - TZ < 0) hi = make_int3(0, 0, 0);
-    const bool have_interior = hi.x >= lo.x && hi.y >= lo.y && hi.z >= lo.z;
-    // boundary tile list, cached per (dims, slab)
-    if (t->bdims[0] != d3[0] || t->bdims[1] != d3[1] || t->bdims[2] != d3[2] || t->bz[0] != z_lo || t->bz[1] != z_hi) {
+    bool have_interior = hi.x >= lo.x && hi.y >= lo.y && hi.z >= lo.z;
+    // thread-block clusters of 2x2x2 interior tiles (super-tiles resolved in
+    // distributed shared memory) need TMA-able fields and an even number of
+    // interior tiles per axis; the odd leftovers join the edge-tile list
+    const bool tma_ok = t->encode != nullptr && (d3[0] % 4) == 0 && d3[0] >= 4 &&
+                        (reinterpret_cast<uintptr_t>(F.own) % 16) == 0;
+    const bool cluster = have_interior && tma_ok && t->use_cluster && hi.x - lo.x >= 1 && hi.y - lo.y >= 1 &&
+                         hi.z - lo.z >= 1;
+    if (cluster) {
+        hi.x = lo.x + (hi.x - lo.x + 1) / 2 * 2 - 1;
+        hi.y = lo.y + (hi.y - lo.y + 1) / 2 * 2 - 1;
+        hi.z = lo.z + (hi.z - lo.z + 1) / 2 * 2 - 1;
+    }
+    // boundary tile list, cached per (dims, slab, cluster mode)
+    if (t->bdims[0] != d3[0] || t->bdims[1] != d3[1] || t->bdims[2] != d3[2] || t->bz[0] != z_lo || t->bz[1] != z_hi ||
+        t->bcluster != cluster) {
+        t->bcluster = cluster;
         std::vector<int32_t> bt;
         for (int bz = 0; bz < tiles_z; ++bz)
             for (int by = 0; by < tiles_y; ++by)
@@ -642,8 +767,7 @@ eg_status tiled3d_local(Tiled3D *t, int ndim, const int64_t *dims, const Slab &s
     // TMA tensor map over the owned planes (needs 16-byte row and plane strides)
     CUtensorMap tmap;
     std::memset(&tmap, 0, sizeof(tmap));
-    bool tma = t->encode != nullptr && (d3[0] % 4) == 0 && d3[0] >= 4 &&
-               (reinterpret_cast<uintptr_t>(F.own) % 16) == 0 && have_interior;
+    bool tma = tma_ok && have_interior;
     if (tma) {
         cuuint64_t gdim[3] = {cuuint64_t(d3[0]), cuuint64_t(d3[1]), cuuint64_t(z_hi - z_lo)};
         cuuint64_t gstr[2] = {cuuint64_t(d3[0] * 4), cuuint64_t(d3[0] * d3[1] * 4)};
@@ -665,19 +789,36 @@ eg_status tiled3d_local(Tiled3D *t, int ndim, const int64_t *dims, const Slab &s
         // aligned, non-negative x coordinate (measured with tools/tma_probe:
         // a start of -1 is an illegal instruction), and these tiles are the
         // ones whose halo starts outside the field or in a neighbour slab
-        k_tile<false, false><<<unsigned(t->n_btiles), kThreads, kTileSmem, st>>>(tmap, A, D);
+        k_tile<false, false, false><<<unsigned(t->n_btiles), kThreads, kTileSmem, st>>>(tmap, A, D);
         stats->kernel_launches += 1;
         if ((e = cudaGetLastError()) != cudaSuccess) return fail(err, e, "k_tile<boundary>");
     }
-    if (have_interior) {
+    if (have_interior && tma && cluster) {
+        A.origin = lo;
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(unsigned(hi.x - lo.x + 1), unsigned(hi.y - lo.y + 1), unsigned(hi.z - lo.z + 1));
+        cfg.blockDim = dim3(kThreads, 1, 1);
+        cfg.dynamicSmemBytes = kTileSmem;
+        cfg.stream = st;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = 2;
+        attr[0].val.clusterDim.y = 2;
+        attr[0].val.clusterDim.z = 2;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        if ((e = cudaLaunchKernelEx(&cfg, k_tile<true, true, true>, tmap, A, D)) != cudaSuccess)
+            return fail(err, e, "k_tile<cluster>");
+        stats->kernel_launches += 1;
+    } else if (have_interior) {
         A.tiles_x = hi.x - lo.x + 1;
         A.tiles_y = hi.y - lo.y + 1;
         A.origin = lo;
         const int64_t nt = int64_t(A.tiles_x) * A.tiles_y * (hi.z - lo.z + 1);
         if (tma)
-            k_tile<true, true><<<unsigned(nt), kThreads, kTileSmem, st>>>(tmap, A, D);
+            k_tile<true, true, false><<<unsigned(nt), kThreads, kTileSmem, st>>>(tmap, A, D);
         else
-            k_tile<true, false><<<unsigned(nt), kThreads, kTileSmem, st>>>(tmap, A, D);
+            k_tile<true, false, false><<<unsigned(nt), kThreads, kTileSmem, st>>>(tmap, A, D);
         stats->kernel_launches += 1;
         if ((e = cudaGetLastError()) != cudaSuccess) return fail(err, e, "k_tile<interior>");
     }
