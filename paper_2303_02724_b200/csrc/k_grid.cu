@@ -1,171 +1,190 @@
 // Generic n-D grid kernels (n = 1..6): S1 steepest-ascent pointer, S3 upper-
 // link components, and the per-saddle part of S4.  One thread per vertex, the
 // way the paper's classification kernel is organised ("launching a CUDA
-// thread for each vertex"), but with the link's edge set replaced by constant
-// bitmasks over the 2 (2^n - 1) link offsets: beta0+ is a bitset flood fill
-// (every upper link vertex is visited once) instead of P:184's union-find.
-// This path serves every n; n <= 3 grids normally take the tiled kernel in
+// thread for each vertex"); n <= 3 grids normally take the tiled kernel in
 // k_grid3d.cu instead.
+//
+// beta0+ without a union-find (P:184 uses one).  The link offsets of the
+// Freudenthal triangulation are +d and -e for nonempty subsets d, e of the n
+// axes (d, e read as n-bit masks), and two link vertices are adjacent iff the
+// difference of their offsets is again an offset:
+//     +d1 ~ +d2  iff  d1 is a proper subset of d2 or vice versa,
+//     -e1 ~ -e2  likewise,
+//     +d  ~ -e   iff  d and e are disjoint (e is a subset of ~d).
+// So a set of link vertices is a pair of 2^n-bit words P, N (bit d of P =
+// offset +d), and one flood-fill step over ALL adjacencies at once is a
+// subset / superset closure of a 2^n-bit word -- n shift-and-or steps each:
+//     P' = U+ & (up(P) | down(P | rev(N))),   N' = U- & (up(N) | down(N | rev(P)))
+// where rev(x) maps bit d to bit ~d.  A component is the fixed point from one
+// seed bit; beta0+ is the number of seeds needed to exhaust U+ and U-.  The
+// adjacency rule is pinned against the oracle's explicit link graph by the
+// n = 1..6 parity tests.
 #include <cstdio>
+#include <type_traits>
 
 #include "eg_impl.h"
 
 namespace eg {
 
-template <int NW>
-struct Bits {
-    uint64_t w[NW];
-    __device__ __forceinline__ void clear() {
-#pragma unroll
-        for (int i = 0; i < NW; ++i) w[i] = 0;
+template <int NDIM>
+struct Lattice {
+    static constexpr int M = 1 << NDIM;  // subsets of the n axes
+    using W = std::conditional_t<(M <= 32), uint32_t, uint64_t>;
+    static constexpr int WB = 8 * sizeof(W);
+    __host__ __device__ static constexpr W full() { return M == WB ? ~W(0) : ((W(1) << M) - 1); }
+    // bits of the subsets that do not contain axis a
+    __host__ __device__ static constexpr W without(int a) {
+        W x = 0;
+        for (int i = 0; i < M; ++i)
+            if (!((i >> a) & 1)) x |= W(1) << i;
+        return x;
     }
-    __device__ __forceinline__ bool any() const {
-        uint64_t x = 0;
+    __device__ __forceinline__ static W up(W x) {  // all supersets of members
 #pragma unroll
-        for (int i = 0; i < NW; ++i) x |= w[i];
-        return x != 0;
+        for (int a = 0; a < NDIM; ++a) x |= (x & without(a)) << (1 << a);
+        return x;
     }
-    __device__ __forceinline__ void set(int k) { w[k >> 6] |= 1ull << (k & 63); }
-    __device__ __forceinline__ int pop_lowest() {  // index of the lowest set bit, cleared; -1 if none
+    __device__ __forceinline__ static W down(W x) {  // all subsets of members
 #pragma unroll
-        for (int i = 0; i < NW; ++i)
-            if (w[i]) {
-                int b = __ffsll((long long)w[i]) - 1;
-                w[i] &= w[i] - 1;
-                return i * 64 + b;
-            }
-        return -1;
+        for (int a = 0; a < NDIM; ++a) x |= (x >> (1 << a)) & without(a);
+        return x;
+    }
+    __device__ __forceinline__ static W rev(W x) {  // bit d -> bit (M-1-d) = ~d
+        if constexpr (WB == 32) return __brev(x) >> (32 - M);
+        else return W(__brevll(x));
+    }
+    __device__ __forceinline__ static W lowest(W x) { return x & (~x + 1); }
+    __device__ __forceinline__ static int pop(W &x) {
+        int b;
+        if constexpr (WB == 32) b = __ffs(x) - 1;
+        else b = __ffsll(x) - 1;
+        x &= x - 1;
+        return b;
     }
 };
 
 template <int NDIM>
 struct GridSmem {
-    static constexpr int K = 2 * ((1 << NDIM) - 1);
-    static constexpr int NW = (K + 63) / 64;
-    int32_t delta[K];                       // N < 2^31: 32-bit linear offsets
-    uint64_t nbr[K][NW];
-    uint64_t neg[NDIM][NW], pos[NDIM][NW];  // offsets with d_a = -1 / +1
+    int32_t dpos[1 << NDIM];  // linear offset of +d (N < 2^31)
     int32_t dims[NDIM];
 };
 
 template <int NDIM>
 __device__ __forceinline__ void load_tables(GridSmem<NDIM> &S, const LinkTable *__restrict__ tab) {
-    constexpr int K = GridSmem<NDIM>::K, NW = GridSmem<NDIM>::NW;
-    for (int k = threadIdx.x; k < K; k += blockDim.x) {
-        S.delta[k] = int32_t(tab->delta[k]);
-#pragma unroll
-        for (int w = 0; w < NW; ++w) S.nbr[k][w] = tab->nbr[k][w];
+    for (int d = threadIdx.x; d < (1 << NDIM); d += blockDim.x) {
+        int64_t x = 0;
+        for (int a = 0; a < NDIM; ++a)
+            if ((d >> a) & 1) x += tab->stride[a];
+        S.dpos[d] = int32_t(x);
     }
-    if (threadIdx.x < NDIM) {
-        const int a = threadIdx.x;
-        S.dims[a] = int32_t(tab->dims[a]);
-#pragma unroll
-        for (int w = 0; w < NW; ++w) S.neg[a][w] = S.pos[a][w] = 0;
-        for (int k = 0; k < K; ++k) {
-            if (tab->d[k][a] < 0) S.neg[a][k >> 6] |= 1ull << (k & 63);
-            if (tab->d[k][a] > 0) S.pos[a][k >> 6] |= 1ull << (k & 63);
-        }
-    }
+    if (threadIdx.x < NDIM) S.dims[threadIdx.x] = int32_t(tab->dims[threadIdx.x]);
     __syncthreads();
 }
 
-// Upper mask and gradient of global vertex v.  Offsets are
-// scanned in ascending global index, so `>=` keeps the highest index among
-// equal values (simulated perturbation, reading L1).  Returns the mask; *best
-// is the gradient (v for a maximum).
+// The upper link of v as (U+, U-) and its gradient.  The
+// offsets are scanned in ascending global index (-e for e = M-1 .. 1, then +d
+// for d = 1 .. M-1: the linear offset of a mask is monotone in the mask over
+// the axes of extent >= 2), so `>=` keeps the highest index among equal values
+// (simulated perturbation, reading L1).  The link is truncated at the domain
+// boundary (reading L3): +d is dropped when v sits on the upper face of an
+// axis in d, -e on the lower face.  *best = v for a maximum.
 template <int NDIM>
-__device__ __forceinline__ Bits<GridSmem<NDIM>::NW> upper_link(const GridSmem<NDIM> &S, const FieldView &F, int64_t v,
-                                                               float fv, int64_t *best) {
-    constexpr int K = GridSmem<NDIM>::K, NW = GridSmem<NDIM>::NW;
-    // the truncated link (reading L3): drop the offsets that leave the domain,
-    // one mask per face the vertex lies on
-    uint64_t valid[NW];
-#pragma unroll
-    for (int w = 0; w < NW; ++w) valid[w] = ~0ull;
+__device__ __forceinline__ void upper_link(const GridSmem<NDIM> &S, const FieldView &F, int64_t v, float fv,
+                                           typename Lattice<NDIM>::W &Up, typename Lattice<NDIM>::W &Un,
+                                           int64_t *best) {
+    using L = Lattice<NDIM>;
+    using W = typename L::W;
+    constexpr int M = L::M;
+    W vp = L::full() & ~W(1), vn = vp;
     uint32_t r = uint32_t(v);
 #pragma unroll
     for (int a = 0; a < NDIM; ++a) {
         const uint32_t D = uint32_t(S.dims[a]);
         const uint32_t c = r % D;
         r /= D;
-#pragma unroll
-        for (int w = 0; w < NW; ++w) {
-            if (c == 0) valid[w] &= ~S.neg[a][w];
-            if (c + 1 == D) valid[w] &= ~S.pos[a][w];
-        }
+        if (c == 0) vn &= L::without(a);
+        if (c + 1 == D) vp &= L::without(a);
     }
-    Bits<NW> m;
-    m.clear();
+    const bool plain = F.lo == nullptr && F.hi == nullptr;  // one slab, no halo planes
+    const float *own = F.own - F.v0;
+    W up = 0, un = 0;
     int64_t b = v;
     float bf = fv;
-    // one slab (no halo planes): plain loads from the owned array
-    const bool plain = F.lo == nullptr && F.hi == nullptr;
-    const float *own = F.own - F.v0;
-    // the table is sorted by offset: the first K/2 offsets lead to lower
-    // indices (up iff f > fv), the rest to higher ones (up iff f >= fv)
-#pragma unroll 2
-    for (int k = 0; k < K / 2; ++k) {
-        if (!((valid[k >> 6] >> (k & 63)) & 1ull)) continue;
-        const int64_t u = v + S.delta[k];
+#pragma unroll
+    for (int e = M - 1; e >= 1; --e) {  // lower indices: up iff f > fv
+        const bool ok = (vn >> e) & 1;
+        const int64_t u = v - (ok ? S.dpos[e] : 0);
         const float fu = plain ? __ldg(own + u) : F.at(u);
-        if (fu > fv) {
-            m.set(k);
+        if (ok && fu > fv) {
+            un |= W(1) << e;
             if (fu >= bf) {
                 bf = fu;
                 b = u;
             }
         }
     }
-#pragma unroll 2
-    for (int k = K / 2; k < K; ++k) {
-        if (!((valid[k >> 6] >> (k & 63)) & 1ull)) continue;
-        const int64_t u = v + S.delta[k];
+#pragma unroll
+    for (int d = 1; d < M; ++d) {  // higher indices: up iff f >= fv
+        const bool ok = (vp >> d) & 1;
+        const int64_t u = v + (ok ? S.dpos[d] : 0);
         const float fu = plain ? __ldg(own + u) : F.at(u);
-        if (fu >= fv) {
-            m.set(k);
+        if (ok && fu >= fv) {
+            up |= W(1) << d;
             if (fu >= bf) {
                 bf = fu;
                 b = u;
             }
         }
     }
+    Up = up;
+    Un = un;
     *best = b;
-    return m;
 }
 
-// beta0+: components of the upper link by bitset flood fill over
-// the constant link adjacency.  If reps != null, also the highest vertex of
-// every component (UpperLinkRep), in component order.
+// beta0+  by lattice closure, see the file comment.  If reps !=
+// null, also the highest vertex of every component (UpperLinkRep), in
+// component order.
 template <int NDIM>
-__device__ __forceinline__ int components(const GridSmem<NDIM> &S, Bits<GridSmem<NDIM>::NW> rem, const FieldView &F,
-                                          int64_t v, int32_t *reps) {
-    constexpr int NW = GridSmem<NDIM>::NW;
+__device__ __forceinline__ int components(const GridSmem<NDIM> &S, typename Lattice<NDIM>::W Up,
+                                          typename Lattice<NDIM>::W Un, const FieldView &F, int64_t v,
+                                          int32_t *reps) {
+    using L = Lattice<NDIM>;
+    using W = typename L::W;
+    W P = Up, N = Un;  // not yet assigned to a component
     int beta = 0;
-    while (rem.any()) {
-        Bits<NW> front;
-        front.clear();
-        int seed = rem.pop_lowest();
-        front.set(seed);
-        int64_t rep = -1;
-        float rf = 0.f;
-        int k;
-        while ((k = front.pop_lowest()) >= 0) {
-            if (reps) {
-                int64_t u = v + S.delta[k];
-                float fu = F.at(u);
+    while (P | N) {
+        W cp = P ? L::lowest(P) : W(0);
+        W cn = P ? W(0) : L::lowest(N);
+        for (;;) {
+            const W np = Up & (L::up(cp) | L::down(cp | L::rev(cn)));
+            const W nn = Un & (L::up(cn) | L::down(cn | L::rev(cp)));
+            if (np == cp && nn == cn) break;
+            cp = np;
+            cn = nn;
+        }
+        P &= ~cp;
+        N &= ~cn;
+        if (reps) {
+            int64_t rep = -1;
+            float rf = 0.f;
+            while (cn) {
+                const int64_t u = v - S.dpos[L::pop(cn)];
+                const float fu = F.at(u);
                 if (rep < 0 || fu > rf || (fu == rf && u > rep)) {
                     rep = u;
                     rf = fu;
                 }
             }
-#pragma unroll
-            for (int w = 0; w < NW; ++w) {
-                uint64_t nb = S.nbr[k][w] & rem.w[w];
-                rem.w[w] &= ~nb;
-                front.w[w] |= nb;
+            while (cp) {
+                const int64_t u = v + S.dpos[L::pop(cp)];
+                const float fu = F.at(u);
+                if (rep < 0 || fu > rf || (fu == rf && u > rep)) {
+                    rep = u;
+                    rf = fu;
+                }
             }
+            reps[beta] = int32_t(rep);
         }
-        if (reps) reps[beta] = int32_t(rep);
         ++beta;
     }
     return beta;
@@ -173,9 +192,8 @@ __device__ __forceinline__ int components(const GridSmem<NDIM> &S, Bits<GridSmem
 
 template <int NDIM>
 __global__ void __launch_bounds__(256) k_classify_grid(const LinkTable *__restrict__ tab, FieldView F, Slab s,
-                                                       int32_t *ptr,
-                                                       uint32_t *sad_bits, uint32_t *max_bits, uint8_t *beta_out,
-                                                       int *nan_flag) {
+                                                       int32_t *ptr, uint32_t *sad_bits, uint32_t *max_bits,
+                                                       uint8_t *beta_out, int *nan_flag) {
     __shared__ GridSmem<NDIM> S;
     load_tables<NDIM>(S, tab);
     const int64_t nown = s.v1 - s.v0;
@@ -187,9 +205,10 @@ __global__ void __launch_bounds__(256) k_classify_grid(const LinkTable *__restri
         const float fv = F.at(v);
         if (fv != fv) atomicOr(nan_flag, 1);
         int64_t best;
-        auto m = upper_link<NDIM>(S, F, v, fv, &best);
-        is_max = !m.any();
-        int beta = is_max ? 0 : components<NDIM>(S, m, F, v, nullptr);
+        typename Lattice<NDIM>::W up, un;
+        upper_link<NDIM>(S, F, v, fv, up, un, &best);
+        is_max = (up | un) == 0;
+        const int beta = is_max ? 0 : components<NDIM>(S, up, un, F, v, nullptr);
         is_sad = beta >= 2;
         ptr[i] = int32_t(best);
         if (beta_out) beta_out[i] = uint8_t(beta > 255 ? 255 : beta);
@@ -213,10 +232,10 @@ __global__ void __launch_bounds__(256) k_saddle_beta_grid(const LinkTable *__res
     const int64_t v = saddles[j];
     const float fv = F.at(v);
     int64_t best;
-    auto m = upper_link<NDIM>(S, F, v, fv, &best);
-    beta[j] = components<NDIM>(S, m, F, v, nullptr);
+    typename Lattice<NDIM>::W up, un;
+    upper_link<NDIM>(S, F, v, fv, up, un, &best);
+    beta[j] = components<NDIM>(S, up, un, F, v, nullptr);
 }
-
 
 // Per saddle: for every component, m = label[rep]; sort the (<= K) m values
 // and reduce to unique (m, multiplicity) (reading L7).  Writes into the
@@ -224,7 +243,7 @@ __global__ void __launch_bounds__(256) k_saddle_beta_grid(const LinkTable *__res
 __device__ __forceinline__ void reduce_arcs(int32_t *ms, int b, int64_t off, int32_t *tmp_m, int32_t *tmp_mult,
                                             int32_t *n_unique_j) {
     for (int a = 1; a < b; ++a) {  // insertion sort (b <= link size)
-        int32_t x = ms[a];
+        const int32_t x = ms[a];
         int c = a - 1;
         while (c >= 0 && ms[c] > x) {
             ms[c + 1] = ms[c];
@@ -246,7 +265,7 @@ __device__ __forceinline__ void reduce_arcs(int32_t *ms, int b, int64_t off, int
 
 __device__ __forceinline__ void sort_reps(int32_t *reps, int b) {
     for (int a = 1; a < b; ++a) {
-        int32_t x = reps[a];
+        const int32_t x = reps[a];
         int c = a - 1;
         while (c >= 0 && reps[c] > x) {
             reps[c + 1] = reps[c];
@@ -266,13 +285,14 @@ __global__ void __launch_bounds__(128) k_arcs_grid(const LinkTable *__restrict__
     load_tables<NDIM>(S, tab);
     const int64_t j = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (j >= n_sad) return;
-    constexpr int K = GridSmem<NDIM>::K;
+    constexpr int K = 2 * ((1 << NDIM) - 1);
     int32_t reps[K];
     const int64_t v = saddles[j];
     const float fv = F.at(v);
     int64_t best;
-    auto m = upper_link<NDIM>(S, F, v, fv, &best);
-    int b = components<NDIM>(S, m, F, v, reps);
+    typename Lattice<NDIM>::W up, un;
+    upper_link<NDIM>(S, F, v, fv, up, un, &best);
+    const int b = components<NDIM>(S, up, un, F, v, reps);
     sort_reps(reps, b);
     const int64_t off = slot_off[j];
     int32_t ms[K];
@@ -305,7 +325,8 @@ cudaError_t launch_classify_grid(const LinkTable *d_tab, int ndim, FieldView F, 
                                  cudaStream_t st) {
     const int64_t n = s.v1 - s.v0;
     if (n <= 0) return cudaSuccess;
-#define CALL(D) k_classify_grid<D><<<blocks_for(n, 256), 256, 0, st>>>(d_tab, F, s, ptr, sad_bits, max_bits, beta_out, nan_flag)
+#define CALL(D) \
+    k_classify_grid<D><<<blocks_for(n, 256), 256, 0, st>>>(d_tab, F, s, ptr, sad_bits, max_bits, beta_out, nan_flag)
     EG_DISPATCH_NDIM(ndim, CALL)
 #undef CALL
     return cudaGetLastError();
@@ -321,13 +342,12 @@ cudaError_t launch_saddle_beta_grid(const LinkTable *d_tab, int ndim, FieldView 
 }
 
 cudaError_t launch_arcs_grid(const LinkTable *d_tab, int ndim, FieldView F, const int32_t *saddles, int64_t n_sad,
-                             const int64_t *slot_off, LabelView lv,
-                             int32_t *tmp_m, int32_t *tmp_mult, int32_t *n_unique, int64_t *raw_s, int64_t *raw_rep,
-                             int64_t *raw_m, cudaStream_t st) {
+                             const int64_t *slot_off, LabelView lv, int32_t *tmp_m, int32_t *tmp_mult,
+                             int32_t *n_unique, int64_t *raw_s, int64_t *raw_rep, int64_t *raw_m, cudaStream_t st) {
     if (n_sad <= 0) return cudaSuccess;
-#define CALL(D)                                                                                            \
-    k_arcs_grid<D><<<blocks_for(n_sad, 128), 128, 0, st>>>(d_tab, F, saddles, n_sad, slot_off, lv, \
-                                                           tmp_m, tmp_mult, n_unique, raw_s, raw_rep, raw_m)
+#define CALL(D)                                                                                              \
+    k_arcs_grid<D><<<blocks_for(n_sad, 128), 128, 0, st>>>(d_tab, F, saddles, n_sad, slot_off, lv, tmp_m, \
+                                                           tmp_mult, n_unique, raw_s, raw_rep, raw_m)
     EG_DISPATCH_NDIM(ndim, CALL)
 #undef CALL
     return cudaGetLastError();
