@@ -308,7 +308,7 @@ static eg_status generic_local(eg_ctx *c, const Problem &P, SlabState &S, bool m
     const int64_t n = S.s.v1 - S.s.v0;
     int *flags = c->flags.as<int>();
     if (timed) CK(cudaEventRecord(c->ev_main[0], c->stream));
-    CK(launch_classify_grid(c->tab.as<LinkTable>(), P.ndim, S.F, S.s, S.label, S.sad_bits.as<uint32_t>(),
+    CK(launch_classify_grid(c->host_tab, P.ndim, S.F, S.s, S.label, S.sad_bits.as<uint32_t>(),
                             S.max_bits.as<uint32_t>(), nullptr, flags, c->stream));
     if (timed) CK(cudaEventRecord(c->ev_main[1], c->stream));
     c->stats.kernel_launches += 1;
@@ -318,7 +318,7 @@ static eg_status generic_local(eg_ctx *c, const Problem &P, SlabState &S, bool m
     int *changed = flags + 2;
     CK(cudaMemsetAsync(changed, 0, sizeof(int) * 64, c->stream));
     int rounds = 0;
-    const int kBatch = 6;
+    const int kBatch = 3;   // bounded chains: one or two rounds usually finish
     int hflag[64];
     for (int r0 = 0; r0 < 60; r0 += kBatch) {
         const int r1 = std::min(60, r0 + kBatch);
@@ -380,7 +380,7 @@ static eg_status grid_graph(eg_ctx *c, const Problem &P, SlabState &S, bool raw)
     const size_t sb = scan_scratch_bytes(std::max<int64_t>(ns, 1));
     CK(c->scratch.ensure(sb));
     if (P.grid)
-        CK(launch_saddle_beta_grid(c->tab.as<LinkTable>(), P.ndim, S.F, S.saddles32.as<int32_t>(), ns,
+        CK(launch_saddle_beta_grid(c->host_tab, P.ndim, S.F, S.saddles32.as<int32_t>(), ns,
                                    S.sbeta.as<int32_t>(), c->stream));
     else
         CK(launch_gather_beta(S.beta8.as<uint8_t>(), S.s.v0, S.saddles32.as<int32_t>(), ns, S.sbeta.as<int32_t>(),
@@ -406,7 +406,7 @@ static eg_status grid_graph(eg_ctx *c, const Problem &P, SlabState &S, bool raw)
         lv.lo = S.has_lo ? S.hval_lo.as<int32_t>() : nullptr;
         lv.hi = S.has_hi ? S.hval_hi.as<int32_t>() : nullptr;
         lv.plane = S.s.plane;
-        CK(launch_arcs_grid(c->tab.as<LinkTable>(), P.ndim, S.F, S.saddles32.as<int32_t>(), ns,
+        CK(launch_arcs_grid(c->host_tab, P.ndim, S.F, S.saddles32.as<int32_t>(), ns,
                             S.slot_off.as<int64_t>(), lv, S.tmp_m.as<int32_t>(), S.tmp_mult.as<int32_t>(),
                             S.n_unique.as<int32_t>(), raw ? S.raw_s.as<int64_t>() : nullptr,
                             raw ? S.raw_rep.as<int64_t>() : nullptr, raw ? S.raw_m.as<int64_t>() : nullptr, c->stream));
@@ -798,8 +798,8 @@ static eg_status compute_csr(eg_ctx *c, const Problem &P, const float *f, uint32
         int *changed = fl + 2;
         CK(cudaMemsetAsync(changed, 0, sizeof(int) * 64, c->stream));
         int hflag[64], rounds = 0;
-        for (int r0 = 0; r0 < 60; r0 += 6) {
-            const int r1 = std::min(60, r0 + 6);
+        for (int r0 = 0; r0 < 60; r0 += 3) {
+            const int r1 = std::min(60, r0 + 3);
             for (int r = r0; r < r1; ++r) {
                 CK(launch_jump_round(whole.label, P.N, 0, changed, r, c->stream));
                 c->stats.kernel_launches += 1;
@@ -996,7 +996,7 @@ eg_status eg_gradient(eg_ctx *c, const eg_domain *d, const float *d_field, int32
         ST(ensure_table(c, P));
         const Slab s{0, P.D, P.plane, 0, P.N};
         const FieldView F{d_field, nullptr, nullptr, 0, P.N, P.plane};
-        CK(launch_classify_grid(c->tab.as<LinkTable>(), P.ndim, F, s, d_ptr, S.sad_bits.as<uint32_t>(),
+        CK(launch_classify_grid(c->host_tab, P.ndim, F, s, d_ptr, S.sad_bits.as<uint32_t>(),
                                 S.max_bits.as<uint32_t>(), d_beta, c->flags.as<int>(), c->stream));
     } else {
         CK(launch_classify_csr(P.row_ptr, P.col_idx, d_field, P.v0, P.v1, d_ptr, S.sad_bits.as<uint32_t>(),

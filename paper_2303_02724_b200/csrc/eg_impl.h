@@ -81,7 +81,7 @@ struct LabelView {
 
 // S1 + S3, generic n: ptr[i] (global id) for owned i, saddle / maximum bits
 // (bit i of word i/32), optional beta0+ per vertex.
-cudaError_t launch_classify_grid(const LinkTable *d_tab, int ndim, FieldView F, const Slab &s, int32_t *ptr,
+cudaError_t launch_classify_grid(const LinkTable &tab, int ndim, FieldView F, const Slab &s, int32_t *ptr,
                                  uint32_t *sad_bits, uint32_t *max_bits, uint8_t *beta_out, int *nan_flag,
                                  cudaStream_t st);
 cudaError_t launch_classify_csr(const int64_t *row_ptr, const int32_t *col_idx, const float *f, int64_t v0,
@@ -103,9 +103,9 @@ cudaError_t launch_emit_counted(const uint32_t *bits, int64_t n, int64_t v0, con
                                 int64_t *out64, cudaStream_t st);
 
 // S4 for grids and CSR.
-cudaError_t launch_saddle_beta_grid(const LinkTable *d_tab, int ndim, FieldView F, const int32_t *saddles,
+cudaError_t launch_saddle_beta_grid(const LinkTable &tab, int ndim, FieldView F, const int32_t *saddles,
                                     int64_t n_sad, int32_t *beta, cudaStream_t st);
-cudaError_t launch_arcs_grid(const LinkTable *d_tab, int ndim, FieldView F, const int32_t *saddles, int64_t n_sad,
+cudaError_t launch_arcs_grid(const LinkTable &tab, int ndim, FieldView F, const int32_t *saddles, int64_t n_sad,
                              const int64_t *slot_off, LabelView lv, int32_t *tmp_m, int32_t *tmp_mult,
                              int32_t *n_unique, int64_t *raw_s, int64_t *raw_rep, int64_t *raw_m, cudaStream_t st);
 // beta0+ of the saddles from a per-vertex beta0+ array written by classify

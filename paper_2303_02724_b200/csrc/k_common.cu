@@ -1,5 +1,7 @@
 // Shared device passes: pointer jumping (S2), stable bitmap compaction of
 // maxima / saddles (S3 node lists), scans and arc emission (S4).
+#include <algorithm>
+
 #include <cub/cub.cuh>
 #include <thrust/iterator/counting_iterator.h>
 #include <thrust/iterator/transform_iterator.h>
@@ -11,34 +13,64 @@ namespace eg {
 static inline unsigned blocks_for(int64_t n, int bs) { return unsigned((n + bs - 1) / bs); }
 
 // ----------------------------------------------------------- S2 jumping
-// ptr <- ptr[ptr] in place.  Concurrent updates are benign: every value ever
-// written is a vertex further along the same ascending path, so any
-// interleaving converges to the path's end (the maximum Alg. 2 reaches,
-// P:205-208).  Targets outside [v0, v0 + n) are terminal (remote vertices).
+// Each round follows every vertex's pointer chain for up to kHops links and
+// stores where it got to (P:205-208's path following, bounded).  Concurrent
+// rounds are benign: a vertex's own entry is the only one it writes, and
+// every value ever stored is a vertex further along the same ascending path,
+// so a stale or a fresh read both lead to the path's end; entries already
+// finished by other threads shortcut the walk.  Targets outside
+// [v0, v0 + n) are terminal (remote vertices).  changed[round] is set when
+// some chain was cut at kHops; a round after one that cut nothing exits at
+// once (the chains are all terminal: max or remote).  Bounding the walk keeps
+// a long monotone path from serialising one thread (the next round restarts
+// from the stored ancestor, so the rounds still halve-or-better every chain).
+constexpr int kHops = 32;
+
 __global__ void __launch_bounds__(256) k_jump(int32_t *ptr, int64_t n, int64_t v0, int *changed, int round) {
-    if (round > 0 && *(volatile int *)&changed[round - 1] == 0) return;   // converged earlier
-    const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    bool ch = false;
-    if (i < n) {
-        const int32_t p = ptr[i];
-        const int64_t pi = int64_t(p) - v0;
-        if (pi >= 0 && pi < n) {
-            const int32_t pp = ptr[pi];
-            if (pp != p) {
-                ptr[i] = pp;
-                ch = true;
+    // converged earlier?  changed[round - 1] was written by the previous launch,
+    // so a cached read is coherent (a volatile read from every thread would
+    // queue ~N/32 requests on one L2 line)
+    if (round > 0 && __ldg(&changed[round - 1]) == 0) return;
+    bool cut = false;
+    // grid-stride over a resident grid: a round that has nothing to do costs
+    // one launch, not N/256 block launches
+    for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
+        const int32_t p0 = ptr[i];
+        int32_t p = p0;
+        bool c = true;
+#pragma unroll 1
+        for (int h = 0; h < kHops; ++h) {
+            const int64_t pi = int64_t(p) - v0;
+            if (pi < 0 || pi >= n) {
+                c = false;
+                break;
             }
+            const int32_t pp = __ldcg(ptr + pi);
+            if (pp == p) {
+                c = false;
+                break;
+            }
+            p = pp;
         }
+        if (p != p0) ptr[i] = p;
+        cut |= c;
     }
-    // one flag store per block at most, and none once the round is known to
-    // have changed something (a single global flag hammered by every warp
-    // serialises in L2)
-    if (__syncthreads_or(ch) && threadIdx.x == 0 && *(volatile int *)&changed[round] == 0) changed[round] = 1;
+    // one flag store per block at most (a single global flag hammered by
+    // every warp serialises in L2)
+    if (__syncthreads_or(cut) && threadIdx.x == 0 && *(volatile int *)&changed[round] == 0) changed[round] = 1;
 }
 
 cudaError_t launch_jump_round(int32_t *ptr, int64_t n, int64_t v0, int *changed, int round, cudaStream_t st) {
     if (n <= 0) return cudaSuccess;
-    k_jump<<<blocks_for(n, 256), 256, 0, st>>>(ptr, n, v0, changed, round);
+    static int sms = 0;
+    if (sms == 0) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    }
+    // 8 blocks of 256 = 2048 threads: a full SM at this kernel's register count
+    k_jump<<<unsigned(std::min<int64_t>(blocks_for(n, 256), int64_t(sms) * 8)), 256, 0, st>>>(ptr, n, v0, changed,
+                                                                                               round);
     return cudaGetLastError();
 }
 

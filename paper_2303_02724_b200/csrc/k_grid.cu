@@ -19,6 +19,7 @@
 // seed bit; beta0+ is the number of seeds needed to exhaust U+ and U-.  The
 // adjacency rule is pinned against the oracle's explicit link graph by the
 // n = 1..6 parity tests.
+#include <algorithm>
 #include <cstdio>
 #include <type_traits>
 
@@ -63,33 +64,64 @@ struct Lattice {
     }
 };
 
+// Per-grid constants, passed by value: every access with an unrolled (compile-
+// time) index becomes a constant-bank operand.
 template <int NDIM>
-struct GridSmem {
+struct GridConst {
     int32_t dpos[1 << NDIM];  // linear offset of +d (N < 2^31)
-    int32_t dims[NDIM];
+    int32_t dneg[1 << NDIM];  // -dpos
+    uint32_t dims[NDIM];
+    uint32_t mag[NDIM];       // r / dims[a] = umulhi(r, mag[a]) >> sh[a] for r < 2^31
+    int32_t sh[NDIM];
 };
 
 template <int NDIM>
-__device__ __forceinline__ void load_tables(GridSmem<NDIM> &S, const LinkTable *__restrict__ tab) {
-    for (int d = threadIdx.x; d < (1 << NDIM); d += blockDim.x) {
+static GridConst<NDIM> make_grid_const(const LinkTable &t) {
+    GridConst<NDIM> S{};
+    for (int d = 0; d < (1 << NDIM); ++d) {
         int64_t x = 0;
         for (int a = 0; a < NDIM; ++a)
-            if ((d >> a) & 1) x += tab->stride[a];
+            if ((d >> a) & 1) x += t.stride[a];
         S.dpos[d] = int32_t(x);
+        S.dneg[d] = -int32_t(x);
     }
-    if (threadIdx.x < NDIM) S.dims[threadIdx.x] = int32_t(tab->dims[threadIdx.x]);
-    __syncthreads();
+    for (int a = 0; a < NDIM; ++a) {
+        // round-up reciprocal: with l = ceil(log2 D) and m = ceil(2^(31+l) / D),
+        // floor(r m / 2^(31+l)) = floor(r / D) for every r < 2^31, since
+        // m D - 2^(31+l) < D <= 2^l.  D = 1 is flagged by sh = -1.
+        const uint32_t D = uint32_t(t.dims[a]);
+        S.dims[a] = D;
+        if (D <= 1) {
+            S.mag[a] = 0u;
+            S.sh[a] = -1;
+        } else {
+            int l = 0;
+            while ((uint64_t(1) << l) < D) ++l;
+            S.mag[a] = uint32_t(((uint64_t(1) << (31 + l)) + D - 1u) / D);
+            S.sh[a] = l - 1;
+        }
+    }
+    return S;
 }
 
+__device__ __forceinline__ float nan_f() { return __int_as_float(0x7fffffff); }
+
 // The upper link of v as (U+, U-) and its gradient.  The
-// offsets are scanned in ascending global index (-e for e = M-1 .. 1, then +d
-// for d = 1 .. M-1: the linear offset of a mask is monotone in the mask over
-// the axes of extent >= 2), so `>=` keeps the highest index among equal values
-// (simulated perturbation, reading L1).  The link is truncated at the domain
-// boundary (reading L3): +d is dropped when v sits on the upper face of an
-// axis in d, -e on the lower face.  *best = v for a maximum.
-template <int NDIM>
-__device__ __forceinline__ void upper_link(const GridSmem<NDIM> &S, const FieldView &F, int64_t v, float fv,
+// link is truncated at the domain boundary (reading L3): +d is dropped when v
+// sits on the upper face of an axis in d, -e on the lower face; a dropped
+// offset reads as NaN, which compares false both ways.  The gradient is the
+// highest link vertex in simulated-perturbation order (reading L1) -- if any
+// link vertex is above v, the highest one is -- so it is tracked over the
+// whole link: the offsets are scanned in ascending global index (-e for
+// e = M-1 .. 1, then +d for d = 1 .. M-1; the linear offset of a mask is
+// monotone in the mask over the axes of extent >= 2), and `>=` keeps the
+// highest index among equal values.  *best = v for a maximum.
+//
+// kPlain: the field is one array holding the whole domain (one slab, no halo
+// planes); a vertex whose whole link box lies inside it loads without
+// clamping the dropped offsets.
+template <int NDIM, bool kPlain>
+__device__ __forceinline__ void upper_link(const GridConst<NDIM> &S, const FieldView &F, int64_t v, float fv,
                                            typename Lattice<NDIM>::W &Up, typename Lattice<NDIM>::W &Un,
                                            int64_t *best) {
     using L = Lattice<NDIM>;
@@ -99,53 +131,75 @@ __device__ __forceinline__ void upper_link(const GridSmem<NDIM> &S, const FieldV
     uint32_t r = uint32_t(v);
 #pragma unroll
     for (int a = 0; a < NDIM; ++a) {
-        const uint32_t D = uint32_t(S.dims[a]);
-        const uint32_t c = r % D;
-        r /= D;
+        const uint32_t D = S.dims[a];
+        const uint32_t q = S.sh[a] < 0 ? r : (__umulhi(r, S.mag[a]) >> S.sh[a]);
+        const uint32_t c = r - q * D;
+        r = q;
         if (c == 0) vn &= L::without(a);
         if (c + 1 == D) vp &= L::without(a);
     }
-    const bool plain = F.lo == nullptr && F.hi == nullptr;  // one slab, no halo planes
-    const float *own = F.own - F.v0;
     W up = 0, un = 0;
-    int64_t b = v;
-    float bf = fv;
+    float bf = -INFINITY;
+    int bk = 0;  // -e or +d of the highest link vertex so far
+    // kSafe: every offset's address is inside the array, so the loads are
+    // unconditional and a dropped offset is replaced by NaN afterwards
+    auto scan = [&](auto load, auto safe) {
+        constexpr bool kSafe = decltype(safe)::value;
 #pragma unroll
-    for (int e = M - 1; e >= 1; --e) {  // lower indices: up iff f > fv
-        const bool ok = (vn >> e) & 1;
-        const int64_t u = v - (ok ? S.dpos[e] : 0);
-        const float fu = plain ? __ldg(own + u) : F.at(u);
-        if (ok && fu > fv) {
-            un |= W(1) << e;
+        for (int e = M - 1; e >= 1; --e) {  // lower indices: above v iff f > fv
+            const bool ok = (vn >> e) & 1;
+            float fu;
+            if constexpr (kSafe) {
+                fu = load(S.dneg[e]);
+                if (!ok) fu = nan_f();
+            } else {
+                fu = ok ? load(S.dneg[e]) : nan_f();
+            }
+            if (fu > fv) un |= W(1) << e;
             if (fu >= bf) {
                 bf = fu;
-                b = u;
+                bk = -e;
             }
         }
-    }
 #pragma unroll
-    for (int d = 1; d < M; ++d) {  // higher indices: up iff f >= fv
-        const bool ok = (vp >> d) & 1;
-        const int64_t u = v + (ok ? S.dpos[d] : 0);
-        const float fu = plain ? __ldg(own + u) : F.at(u);
-        if (ok && fu >= fv) {
-            up |= W(1) << d;
+        for (int d = 1; d < M; ++d) {  // higher indices: above v iff f >= fv
+            const bool ok = (vp >> d) & 1;
+            float fu;
+            if constexpr (kSafe) {
+                fu = load(S.dpos[d]);
+                if (!ok) fu = nan_f();
+            } else {
+                fu = ok ? load(S.dpos[d]) : nan_f();
+            }
+            if (fu >= fv) up |= W(1) << d;
             if (fu >= bf) {
                 bf = fu;
-                b = u;
+                bk = d;
             }
         }
+    };
+    if constexpr (kPlain) {
+        // an opaque base keeps each address one wide multiply-add off it
+        const float *p = F.own + (v - F.v0);
+        asm("" : "+l"(p));
+        const int64_t reach = S.dpos[M - 1];
+        if (v - reach >= F.v0 && v + reach < F.v1)
+            scan([&](int32_t off) { return __ldg(p + off); }, std::true_type{});
+        else
+            scan([&](int32_t off) { return __ldg(p + off); }, std::false_type{});
+    } else {
+        scan([&](int32_t off) { return F.at(v + off); }, std::false_type{});
     }
     Up = up;
     Un = un;
-    *best = b;
+    *best = (up | un) ? v + (bk < 0 ? -S.dpos[-bk] : S.dpos[bk]) : v;
 }
 
 // beta0+  by lattice closure, see the file comment.  If reps !=
 // null, also the highest vertex of every component (UpperLinkRep), in
 // component order.
 template <int NDIM>
-__device__ __forceinline__ int components(const GridSmem<NDIM> &S, typename Lattice<NDIM>::W Up,
+__device__ __forceinline__ int components(const GridConst<NDIM> &S, typename Lattice<NDIM>::W Up,
                                           typename Lattice<NDIM>::W Un, const FieldView &F, int64_t v,
                                           int32_t *reps) {
     using L = Lattice<NDIM>;
@@ -190,12 +244,10 @@ __device__ __forceinline__ int components(const GridSmem<NDIM> &S, typename Latt
     return beta;
 }
 
-template <int NDIM>
-__global__ void __launch_bounds__(256) k_classify_grid(const LinkTable *__restrict__ tab, FieldView F, Slab s,
+template <int NDIM, bool kPlain>
+__global__ void __launch_bounds__(256) k_classify_grid(const __grid_constant__ GridConst<NDIM> S, FieldView F, Slab s,
                                                        int32_t *ptr, uint32_t *sad_bits, uint32_t *max_bits,
                                                        uint8_t *beta_out, int *nan_flag) {
-    __shared__ GridSmem<NDIM> S;
-    load_tables<NDIM>(S, tab);
     const int64_t nown = s.v1 - s.v0;
     const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     const bool active = i < nown;
@@ -206,7 +258,7 @@ __global__ void __launch_bounds__(256) k_classify_grid(const LinkTable *__restri
         if (fv != fv) atomicOr(nan_flag, 1);
         int64_t best;
         typename Lattice<NDIM>::W up, un;
-        upper_link<NDIM>(S, F, v, fv, up, un, &best);
+        upper_link<NDIM, kPlain>(S, F, v, fv, up, un, &best);
         is_max = (up | un) == 0;
         const int beta = is_max ? 0 : components<NDIM>(S, up, un, F, v, nullptr);
         is_sad = beta >= 2;
@@ -215,25 +267,23 @@ __global__ void __launch_bounds__(256) k_classify_grid(const LinkTable *__restri
     }
     const uint32_t sb = __ballot_sync(0xffffffffu, is_sad);
     const uint32_t mb = __ballot_sync(0xffffffffu, is_max);
-    if ((threadIdx.x & 31) == 0 && i < nown) {
+    if ((threadIdx.x & 31) == 0 && active) {
         sad_bits[i >> 5] = sb;
         max_bits[i >> 5] = mb;
     }
 }
 
 template <int NDIM>
-__global__ void __launch_bounds__(256) k_saddle_beta_grid(const LinkTable *__restrict__ tab, FieldView F,
+__global__ void __launch_bounds__(256) k_saddle_beta_grid(const __grid_constant__ GridConst<NDIM> S, FieldView F,
                                                           const int32_t *__restrict__ saddles, int64_t n_sad,
                                                           int32_t *beta) {
-    __shared__ GridSmem<NDIM> S;
-    load_tables<NDIM>(S, tab);
     const int64_t j = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (j >= n_sad) return;
     const int64_t v = saddles[j];
     const float fv = F.at(v);
     int64_t best;
     typename Lattice<NDIM>::W up, un;
-    upper_link<NDIM>(S, F, v, fv, up, un, &best);
+    upper_link<NDIM, false>(S, F, v, fv, up, un, &best);
     beta[j] = components<NDIM>(S, up, un, F, v, nullptr);
 }
 
@@ -276,13 +326,11 @@ __device__ __forceinline__ void sort_reps(int32_t *reps, int b) {
 }
 
 template <int NDIM>
-__global__ void __launch_bounds__(128) k_arcs_grid(const LinkTable *__restrict__ tab, FieldView F,
+__global__ void __launch_bounds__(128) k_arcs_grid(const __grid_constant__ GridConst<NDIM> S, FieldView F,
                                                    const int32_t *__restrict__ saddles, int64_t n_sad,
                                                    const int64_t *__restrict__ slot_off, LabelView lv,
                                                    int32_t *tmp_m, int32_t *tmp_mult, int32_t *n_unique,
                                                    int64_t *raw_s, int64_t *raw_rep, int64_t *raw_m) {
-    __shared__ GridSmem<NDIM> S;
-    load_tables<NDIM>(S, tab);
     const int64_t j = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (j >= n_sad) return;
     constexpr int K = 2 * ((1 << NDIM) - 1);
@@ -291,7 +339,7 @@ __global__ void __launch_bounds__(128) k_arcs_grid(const LinkTable *__restrict__
     const float fv = F.at(v);
     int64_t best;
     typename Lattice<NDIM>::W up, un;
-    upper_link<NDIM>(S, F, v, fv, up, un, &best);
+    upper_link<NDIM, false>(S, F, v, fv, up, un, &best);
     const int b = components<NDIM>(S, up, un, F, v, reps);
     sort_reps(reps, b);
     const int64_t off = slot_off[j];
@@ -320,33 +368,39 @@ __global__ void __launch_bounds__(128) k_arcs_grid(const LinkTable *__restrict__
 
 static inline unsigned blocks_for(int64_t n, int bs) { return unsigned((n + bs - 1) / bs); }
 
-cudaError_t launch_classify_grid(const LinkTable *d_tab, int ndim, FieldView F, const Slab &s, int32_t *ptr,
+cudaError_t launch_classify_grid(const LinkTable &tab, int ndim, FieldView F, const Slab &s, int32_t *ptr,
                                  uint32_t *sad_bits, uint32_t *max_bits, uint8_t *beta_out, int *nan_flag,
                                  cudaStream_t st) {
     const int64_t n = s.v1 - s.v0;
     if (n <= 0) return cudaSuccess;
-#define CALL(D) \
-    k_classify_grid<D><<<blocks_for(n, 256), 256, 0, st>>>(d_tab, F, s, ptr, sad_bits, max_bits, beta_out, nan_flag)
+    const bool plain = F.lo == nullptr && F.hi == nullptr;
+#define CALL(D)                                                                                           \
+    if (plain)                                                                                            \
+        k_classify_grid<D, true><<<blocks_for(n, 256), 256, 0, st>>>(             \
+            make_grid_const<D>(tab), F, s, ptr, sad_bits, max_bits, beta_out, nan_flag);                                    \
+    else                                                                                                  \
+        k_classify_grid<D, false><<<blocks_for(n, 256), 256, 0, st>>>(           \
+            make_grid_const<D>(tab), F, s, ptr, sad_bits, max_bits, beta_out, nan_flag)
     EG_DISPATCH_NDIM(ndim, CALL)
 #undef CALL
     return cudaGetLastError();
 }
 
-cudaError_t launch_saddle_beta_grid(const LinkTable *d_tab, int ndim, FieldView F, const int32_t *saddles,
+cudaError_t launch_saddle_beta_grid(const LinkTable &tab, int ndim, FieldView F, const int32_t *saddles,
                                     int64_t n_sad, int32_t *beta, cudaStream_t st) {
     if (n_sad <= 0) return cudaSuccess;
-#define CALL(D) k_saddle_beta_grid<D><<<blocks_for(n_sad, 256), 256, 0, st>>>(d_tab, F, saddles, n_sad, beta)
+#define CALL(D) k_saddle_beta_grid<D><<<blocks_for(n_sad, 256), 256, 0, st>>>(make_grid_const<D>(tab), F, saddles, n_sad, beta)
     EG_DISPATCH_NDIM(ndim, CALL)
 #undef CALL
     return cudaGetLastError();
 }
 
-cudaError_t launch_arcs_grid(const LinkTable *d_tab, int ndim, FieldView F, const int32_t *saddles, int64_t n_sad,
+cudaError_t launch_arcs_grid(const LinkTable &tab, int ndim, FieldView F, const int32_t *saddles, int64_t n_sad,
                              const int64_t *slot_off, LabelView lv, int32_t *tmp_m, int32_t *tmp_mult,
                              int32_t *n_unique, int64_t *raw_s, int64_t *raw_rep, int64_t *raw_m, cudaStream_t st) {
     if (n_sad <= 0) return cudaSuccess;
 #define CALL(D)                                                                                              \
-    k_arcs_grid<D><<<blocks_for(n_sad, 128), 128, 0, st>>>(d_tab, F, saddles, n_sad, slot_off, lv, tmp_m, \
+    k_arcs_grid<D><<<blocks_for(n_sad, 128), 128, 0, st>>>(make_grid_const<D>(tab), F, saddles, n_sad, slot_off, lv, tmp_m, \
                                                            tmp_mult, n_unique, raw_s, raw_rep, raw_m)
     EG_DISPATCH_NDIM(ndim, CALL)
 #undef CALL

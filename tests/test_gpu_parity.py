@@ -81,6 +81,9 @@ CASES = [
     ([33, 35, 19], "int"), ([65, 33, 17], "normal"), ([70, 9, 40], "signed_zero"), ([31, 64, 33], "const"),
     ([7, 6, 5, 4], "int"), ([9, 8, 7, 6], "normal"), ([6, 5, 4, 3, 3], "int"), ([8, 7, 6, 5, 4], "normal"),
     ([4, 3, 3, 2, 3, 3], "int"), ([5, 4, 4, 3, 3, 2], "normal"),
+    # extents of 1 and 2 on inner axes (the generic kernel's coordinate division and truncated link)
+    ([5, 1, 4, 3], "int"), ([3, 4, 1, 2, 5], "int"), ([2, 1, 3, 1, 2, 3], "int"), ([1, 7, 1, 6, 1], "normal"),
+    ([37, 3, 2, 2, 3], "signed_zero"),
 ]
 
 
