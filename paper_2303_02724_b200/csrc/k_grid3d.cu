@@ -52,7 +52,8 @@ constexpr int kFboxSlack = XO + BX + PL;             // shifted TMA boxes spill 
 constexpr size_t kOffP = size_t(BOX + kFboxSlack) * 4;  // pbox after fbox
 constexpr size_t kOffL = kOffP + size_t(BOX) * 2;    // lut bits
 constexpr size_t kOffM = kOffL + size_t(kLutWords) * 4;
-constexpr size_t kTileSmem = kOffM + 16 + 33 * 4 + 16; // ~78 KB -> 2 CTAs per SM (register-limited)
+constexpr size_t kOffT = kOffM + 16 + 33 * 4 + 16;  // plane table (PL int32)
+constexpr size_t kTileSmem = kOffT + size_t(PL) * 4; // ~81 KB -> 2 CTAs per SM (register-limited)
 
 struct Tiled3D {
     uint32_t *d_lut = nullptr;
@@ -61,7 +62,10 @@ struct Tiled3D {
     int64_t bz[2] = {-1, -1};                        // slab planes of the cached list
     bool bcluster = false;                           // cluster mode of the cached list
     bool use_cluster = false;
+    int rounds = 2;
     int32_t *d_btiles = nullptr;                     // boundary tile list for the cached dims
+    int32_t *d_ptab = nullptr;                       // plane table for nx = ptab_nx
+    int64_t ptab_nx = -1;
     int64_t n_btiles = 0;
     int32_t *d_elist = nullptr;                      // exit targets E
     int64_t ecap = 0;
@@ -75,6 +79,7 @@ void tiled3d_destroy(Tiled3D *t) {
     if (!t) return;
     if (t->d_lut) cudaFree(t->d_lut);
     if (t->d_btiles) cudaFree(t->d_btiles);
+    if (t->d_ptab) cudaFree(t->d_ptab);
     if (t->d_elist) cudaFree(t->d_elist);
     if (t->d_ecount) cudaFree(t->d_ecount);
     delete t;
@@ -85,6 +90,9 @@ struct Dims3 {
 };
 
 constexpr int kResOff = (BOX + 255) / 256 * 256;     // cluster: resolved shell values after the used bytes
+constexpr int kUbitWords = (BOX + 31) / 32;          // exit-target bitmap
+constexpr int kTlistOff = kUbitWords * 4;            // exit-target list (uint16 box cells) after it
+static_assert(kTlistOff + BOX * 2 <= (BOX + kFboxSlack) * 4, "target list fits the dead field box");
 
 struct TileArgs {
     const float *f;                 // owned planes [z_lo, z_hi) of the slab
@@ -98,9 +106,11 @@ struct TileArgs {
     unsigned long long *ecount;
     int64_t ecap;
     const uint32_t *lut;
+    const int32_t *ptab;            // per box-plane cell: by * nx + bx, bit 31 = in-plane shell
     const int32_t *btiles;          // boundary variant: packed tile ids
     int32_t tiles_x, tiles_y;       // interior variant: sub-box extents
     int3 origin;                    // interior variant: first interior tile
+    int32_t rounds;                 // pointer-doubling rounds before the chase
 };
 
 __device__ __forceinline__ int bidx(int x, int y, int z) { return (z * BY + y) * BX + x; }
@@ -325,9 +335,14 @@ __global__ void __launch_bounds__(kThreads, 2)
             }
         }
     }
-    // halo / padding cells of the pointer box are terminal (point to themselves)
-    for (int i = tid; i < BOX; i += kThreads) pbox[i] = uint16_t(i);
+    // halo / padding cells of the pointer box are terminal (point to themselves);
+    // two cells per store
+    static_assert(BOX % 2 == 0 && kOffP % 4 == 0, "paired pbox init");
+    for (int i = tid; i < BOX / 2; i += kThreads)
+        reinterpret_cast<uint32_t *>(pbox)[i] = uint32_t(2 * i) | (uint32_t(2 * i + 1) << 16);
     for (int i = tid; i < kLutWords; i += kThreads) lut[i] = __ldg(A.lut + i);
+    int32_t *ptab = reinterpret_cast<int32_t *>(smem + kOffT);
+    for (int i = tid; i < PL; i += kThreads) ptab[i] = __ldg(A.ptab + i);
     if (use_tma) mbar_wait(bar, 0);
     __syncthreads();
 
@@ -416,14 +431,33 @@ __global__ void __launch_bounds__(kThreads, 2)
     if (nan_seen) atomicOr(A.nan_flag, 1);
     __syncthreads();
 
+    // fbox is dead from here.  Cluster: 1 byte per box cell marks the shell
+    // cells used as roots, resolved values after them.  Otherwise: a bitmap of
+    // the exit targets (the first vertex to set a bit appends the cell to a
+    // list of the tile's targets, so E needs no scan of the box).
+    uint8_t *used = reinterpret_cast<uint8_t *>(fbox);
+    int32_t *res = reinterpret_cast<int32_t *>(reinterpret_cast<uint8_t *>(fbox) + kResOff);   // cluster only
+    uint32_t *ubits = reinterpret_cast<uint32_t *>(fbox);
+    uint16_t *tlist = reinterpret_cast<uint16_t *>(reinterpret_cast<uint8_t *>(fbox) + kTlistOff);
+    uint32_t *tcount = reinterpret_cast<uint32_t *>(smem + kOffM + 16 + 33 * 4 + 8);
+    if constexpr (kCluster) {
+        static_assert(BOX % 16 == 0, "uint4 clear of the used bytes");
+        for (int i = tid; i < BOX / 16; i += kThreads) reinterpret_cast<uint4 *>(used)[i] = make_uint4(0, 0, 0, 0);
+    } else {
+        for (int i = tid; i < kUbitWords; i += kThreads) ubits[i] = 0u;
+        if (tid == 0) *tcount = 0u;
+    }
+
     // ---- S2 inside the tile.  Two rounds of pointer doubling (independent
-    // loads, no divergence) quarter every chain; then every vertex chases the
-    // rest of its chain to the local root, halving the path as it goes (in
-    // place and race-benign: every stored value lies further along the path).
-    // (measured alternative: doubling to convergence with a per-vertex done
-    // mask costs ~50 instr/vertex against ~37 for this, profiles/r01)
+    // loads, no divergence) quarter every chain; then every vertex follows the
+    // rest of its chain to the local root and stores the root in its own cell
+    // only.  Any other thread reads that cell as either the old pointer or the
+    // root -- both lie on the same ascending path -- so nothing needs settling,
+    // and chains that run into a finished cell end one hop later.
+    // (measured alternatives, profiles/r01: doubling to convergence with a
+    // per-vertex done mask ~50 instr/vertex; path halving + a settle pass ~45)
 #pragma unroll 1
-    for (int round = 0; round < 2; ++round) {
+    for (int round = 0; round < A.rounds; ++round) {
 #pragma unroll
         for (int z = 0; z < TZ; ++z) {
             const int c = cb + (z + 1) * PL;
@@ -431,43 +465,29 @@ __global__ void __launch_bounds__(kThreads, 2)
         }
         __syncthreads();
     }
-#pragma unroll 1
-    for (int z = 0; z < TZ; ++z) {
-        const int c = cb + (z + 1) * PL;
-        int x = c;
-        int p = pbox[x];
-        while (p != x) {
-            const int q = pbox[p];
-            if (q != p) pbox[x] = uint16_t(q);
-            x = p;
-            p = q;
-        }
+    auto chase = [&](int c) -> int {
+        int x = pbox[c];
+        for (int q; (q = pbox[x]) != x;) x = q;
         pbox[c] = uint16_t(x);
-    }
-    __syncthreads();
-    // another thread's path halving may have overwritten pbox[c] with an
-    // ancestor after c's own chase stored the root: settle every own cell on
-    // its root before anyone reads the box as roots
-#pragma unroll 1
-    for (int z = 0; z < TZ; ++z) {
-        const int c = cb + (z + 1) * PL;
-        int r = pbox[c];
-        for (int q; (q = pbox[r]) != r;) r = q;
-        pbox[c] = uint16_t(r);
-    }
-    __syncthreads();
+        return x;
+    };
 
     // ---- outputs: label (bit 31 = exit), bitmaps, exit-target marks
-    uint8_t *used = reinterpret_cast<uint8_t *>(fbox);   // fbox is dead: 1 byte per box cell
-    int32_t *res = reinterpret_cast<int32_t *>(reinterpret_cast<uint8_t *>(fbox) + kResOff);   // cluster only
-    for (int i = tid; i < BOX / 16; i += kThreads) reinterpret_cast<uint4 *>(used)[i] = make_uint4(0, 0, 0, 0);
-    __syncthreads();
+    const bool aligned = (D.nx & 31) == 0;
+    // 32-bit index arithmetic (N < 2^31): the global id of box cell (0,0,0),
+    // the plane stride, and this column's owned index at z = 0
+    const int32_t nxy = D.ny * D.nx;
+    const int32_t g_box0 = ((z0 - 1) * D.ny + (y0 - 1)) * D.nx + (x0 - XO);
+    const int32_t i_col = (z0 * D.ny + gy) * D.nx + gx - int32_t(A.v0);
     if constexpr (kCluster) {
         // The 2x2x2 tiles of a thread-block cluster form a super-tile: a path
         // that leaves this tile into a sibling is followed through the
         // sibling's pointer box in distributed shared memory, so only paths
         // leaving the super-tile remain exits.
         //   A: final roots into the own box, mark the shell cells used as roots
+#pragma unroll 1
+        for (int z = 0; z < TZ; ++z) chase(cb + (z + 1) * PL);
+        __syncthreads();
 #pragma unroll 1
         for (int z = 0; z < TZ; ++z) {
             const int r = pbox[cb + (z + 1) * PL];
@@ -486,35 +506,33 @@ __global__ void __launch_bounds__(kThreads, 2)
         }
         cg::this_cluster().sync();      // no sibling reads this box after this point
     }
-    const bool aligned = (D.nx & 31) == 0;
-    // 32-bit index arithmetic (N < 2^31): the global id of box cell (0,0,0),
-    // the plane stride, and this column's owned index at z = 0
-    const int32_t nxy = D.ny * D.nx;
-    const int32_t g_box0 = ((z0 - 1) * D.ny + (y0 - 1)) * D.nx + (x0 - XO);
-    const int32_t i_col = (z0 * D.ny + gy) * D.nx + gx - int32_t(A.v0);
 #pragma unroll 2
     for (int z = 0; z < TZ; ++z) {
         const int gz = z0 + z;
         const bool ok = col_ok && (kInterior || gz < A.z_hi);
-        const int r = pbox[cb + (z + 1) * PL];          // the local root (doubling converged)
+        const int c = cb + (z + 1) * PL;
+        const int r = kCluster ? int(pbox[c]) : chase(c);   // the local root
         const int bz = r / PL, rr = r - bz * PL;
-        const int by = rr / BX, bx = rr - by * BX;
+        const int32_t t = ptab[rr];
         // exit: the root is in the halo shell of the box, or (last tile of a
         // slab) in a plane the slab does not own
-        bool exit = bx < XO || bx >= XO + TX || by == 0 || by == BY - 1 || bz == 0 || bz == BZ - 1 ||
-                    (!kInterior && z0 - 1 + bz >= A.z_hi);
+        bool exit = t < 0 || bz == 0 || bz == BZ - 1 || (!kInterior && z0 - 1 + bz >= A.z_hi);
         int32_t lab;
         if (kCluster && exit) {
+            const int by = rr / BX, bx = rr - by * BX;
             lab = res[shell_index(bx, by, bz)];
             exit = lab < 0;
         } else {
-            const int32_t root = g_box0 + bz * nxy + by * D.nx + bx;
+            const int32_t root = g_box0 + bz * nxy + (t & 0x7fffffff);
             lab = exit ? int32_t(uint32_t(root) | kFlag) : root;
         }
         const int32_t i = i_col + z * nxy;               // owned index of this vertex
         if (ok) {
             A.label[i] = lab;
-            if (!kCluster && exit) used[r] = 1;
+            if (!kCluster && exit) {
+                const uint32_t bit = 1u << (r & 31);
+                if (!(atomicOr(ubits + (r >> 5), bit) & bit)) tlist[atomicAdd(tcount, 1u)] = uint16_t(r);
+            }
         }
         const uint32_t eb = __ballot_sync(0xffffffffu, ok && exit);
         const uint32_t sb = __ballot_sync(0xffffffffu, (sad_mask >> z) & 1u);
@@ -545,51 +563,54 @@ __global__ void __launch_bounds__(kThreads, 2)
     }
     __syncthreads();
     // ---- append the tile's exit targets to E: one global atomic per tile
-    // (block scan of per-thread counts).  Only shell cells can be exit
-    // targets; in a cluster, the target is the resolved vertex outside the
-    // super-tile.
-    uint32_t *red = reinterpret_cast<uint32_t *>(smem + kOffM + 16);   // [32] warp sums + [1] base
-    auto is_target = [&](int s, int i) -> bool { return used[i] && (!kCluster || res[s] < 0); };
-    int mine = 0;
-    for (int s = tid; s < kShell; s += kThreads) mine += is_target(s, shell_cell(s));
-    int incl = mine;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const int y = __shfl_up_sync(0xffffffffu, incl, o);
-        if (tx >= o) incl += y;
-    }
-    if (tx == 31) red[ty] = uint32_t(incl);
-    __syncthreads();
-    if (ty == 0) {
-        const int wsum = tx < kThreads / 32 ? int(red[tx]) : 0;
-        int wincl = wsum;
+    if constexpr (kCluster) {
+        // block scan of per-thread counts over the shell cells whose path
+        // leaves the super-tile; E gets the resolved vertex outside
+        uint32_t *red = reinterpret_cast<uint32_t *>(smem + kOffM + 16);   // [32] warp sums + [1] base
+        auto is_target = [&](int s, int i) -> bool { return used[i] && res[s] < 0; };
+        int mine = 0;
+        for (int s = tid; s < kShell; s += kThreads) mine += is_target(s, shell_cell(s));
+        int incl = mine;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
-            const int y = __shfl_up_sync(0xffffffffu, wincl, o);
-            if (tx >= o) wincl += y;
+            const int y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (tx >= o) incl += y;
         }
-        if (tx < kThreads / 32) red[tx] = uint32_t(wincl - wsum);   // exclusive warp offsets
-        if (tx == kThreads / 32 - 1) {
-            const unsigned long long b = wincl ? atomicAdd(A.ecount, (unsigned long long)wincl) : 0ull;
-            reinterpret_cast<unsigned long long *>(red + 32)[0] = b;
-        }
-    }
-    __syncthreads();
-    if (mine) {
-        unsigned long long slot = reinterpret_cast<unsigned long long *>(red + 32)[0] + red[ty] + (incl - mine);
-        for (int s = tid; s < kShell; s += kThreads) {
-            const int i = shell_cell(s);
-            if (!is_target(s, i)) continue;
-            int32_t g;
-            if (kCluster) {
-                g = res[s] & 0x7fffffff;
-            } else {
-                const int bz = i / PL, rr = i - bz * PL;
-                const int by = rr / BX, bx = rr - by * BX;
-                g = ((z0 - 1 + bz) * D.ny + (y0 - 1 + by)) * D.nx + (x0 - XO + bx);
+        if (tx == 31) red[ty] = uint32_t(incl);
+        __syncthreads();
+        if (ty == 0) {
+            const int wsum = tx < kThreads / 32 ? int(red[tx]) : 0;
+            int wincl = wsum;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(0xffffffffu, wincl, o);
+                if (tx >= o) wincl += y;
             }
-            if (slot < (unsigned long long)A.ecap) A.elist[slot] = g;
-            ++slot;
+            if (tx < kThreads / 32) red[tx] = uint32_t(wincl - wsum);   // exclusive warp offsets
+            if (tx == kThreads / 32 - 1) {
+                const unsigned long long b = wincl ? atomicAdd(A.ecount, (unsigned long long)wincl) : 0ull;
+                reinterpret_cast<unsigned long long *>(red + 32)[0] = b;
+            }
+        }
+        __syncthreads();
+        if (mine) {
+            unsigned long long slot = reinterpret_cast<unsigned long long *>(red + 32)[0] + red[ty] + (incl - mine);
+            for (int s = tid; s < kShell; s += kThreads) {
+                if (!is_target(s, shell_cell(s))) continue;
+                if (slot < (unsigned long long)A.ecap) A.elist[slot] = res[s] & 0x7fffffff;
+                ++slot;
+            }
+        }
+    } else {
+        unsigned long long *base = reinterpret_cast<unsigned long long *>(smem + kOffM + 16);
+        const uint32_t nt = *tcount;
+        if (tid == 0) *base = nt ? atomicAdd(A.ecount, (unsigned long long)nt) : 0ull;
+        __syncthreads();
+        const unsigned long long b0 = *base;
+        for (uint32_t j = tid; j < nt; j += kThreads) {
+            const int i = tlist[j];
+            const int bz = i / PL, rr = i - bz * PL;
+            if (b0 + j < (unsigned long long)A.ecap) A.elist[b0 + j] = g_box0 + bz * nxy + (ptab[rr] & 0x7fffffff);
         }
     }
 }
@@ -687,6 +708,8 @@ eg_status tiled3d_local(Tiled3D *t, int ndim, const int64_t *dims, const Slab &s
         // barriers per tile; profiles/r01), a net loss.
         const char *cl = std::getenv("EG_CLUSTER");
         t->use_cluster = cl && cl[0] == '1';
+        const char *rs = std::getenv("EG_TILE_ROUNDS");   // tuning knob (default 2)
+        if (rs && rs[0] >= '0' && rs[0] <= '6') t->rounds = rs[0] - '0';
         cudaDriverEntryPointQueryResult q;
         void *fn = nullptr;
         if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) == cudaSuccess &&
@@ -748,6 +771,20 @@ eg_status tiled3d_local(Tiled3D *t, int ndim, const int64_t *dims, const Slab &s
         t->bz[0] = z_lo;
         t->bz[1] = z_hi;
     }
+    // plane table: box-plane cell (bx, by) -> by * nx + bx, bit 31 if the cell
+    // is on the in-plane shell (x or y halo)
+    if (t->ptab_nx != d3[0]) {
+        std::vector<int32_t> pt(PL);
+        for (int rr = 0; rr < PL; ++rr) {
+            const int by = rr / BX, bx = rr % BX;
+            const bool sh = bx < XO || bx >= XO + TX || by == 0 || by == BY - 1;
+            pt[rr] = int32_t(uint32_t(by * int32_t(d3[0]) + bx) | (sh ? kFlag : 0u));
+        }
+        if (!t->d_ptab && (e = cudaMalloc(&t->d_ptab, PL * 4)) != cudaSuccess) return fail(err, e, "cudaMalloc ptab");
+        if ((e = cudaMemcpy(t->d_ptab, pt.data(), PL * 4, cudaMemcpyHostToDevice)) != cudaSuccess)
+            return fail(err, e, "ptab upload");
+        t->ptab_nx = d3[0];
+    }
     // exit-target list capacity: N / 8 (falls back to a per-vertex chase on overflow)
     const int64_t want = std::max<int64_t>(nown / 8, 4096);
     if (t->ecap < want) {
@@ -780,9 +817,9 @@ eg_status tiled3d_local(Tiled3D *t, int ndim, const int64_t *dims, const Slab &s
         tma = (r == CUDA_SUCCESS);
     }
     stats->path = 1;
-    TileArgs A{F.own,     F.lo,      F.hi,      int32_t(z_lo), int32_t(z_hi), s.v0,       labels,  exit_bits,
-               sad_bits,  max_bits,  flags,     t->d_elist,    t->d_ecount,   t->ecap,    t->d_lut, t->d_btiles,
-               0,         0,         make_int3(0, 0, 0)};
+    TileArgs A{F.own,     F.lo,     F.hi,  int32_t(z_lo), int32_t(z_hi), s.v0,    labels,   exit_bits,
+               sad_bits,  max_bits, flags, t->d_elist,    t->d_ecount,   t->ecap, t->d_lut, t->d_ptab,
+               t->d_btiles, 0,      0,     make_int3(0, 0, 0), t->rounds};
     if (ev_main0) cudaEventRecord(ev_main0, st);
     if (t->n_btiles > 0) {
         // boundary tiles use plain loads: a TMA box must start at a 16-byte
