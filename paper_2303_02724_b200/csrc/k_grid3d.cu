@@ -233,19 +233,16 @@ __device__ __forceinline__ VK vmax(VK a, VK b) { return b.v >= a.v ? b : a; }
 // the same where NaN marks a cell outside the domain: a NaN never wins
 __device__ __forceinline__ VK vmaxn(VK a, VK b) { return (b.v >= a.v || a.v != a.v) ? b : a; }
 
-// IEEE compares (no ftz: distinct denormals stay distinct, reading L2)
-__device__ __forceinline__ uint32_t setgt(float a, float b) {
-    uint32_t r;
-    asm("set.gt.u32.f32 %0, %1, %2;" : "=r"(r) : "f"(a), "f"(b));
-    return r;
+// IEEE compares (no ftz: distinct denormals stay distinct, reading L2; a NaN
+// compares false): m |= kBit if a > b (a >= b), one FSETP + one predicated LOP3
+template <uint32_t kBit>
+__device__ __forceinline__ void or_if_gt(uint32_t &m, float a, float b) {
+    asm("{\n\t.reg .pred p;\n\tsetp.gt.f32 p, %1, %2;\n\t@p or.b32 %0, %0, %3;\n\t}" : "+r"(m) : "f"(a), "f"(b), "n"(kBit));
 }
-__device__ __forceinline__ uint32_t setge(float a, float b) {
-    uint32_t r;
-    asm("set.ge.u32.f32 %0, %1, %2;" : "=r"(r) : "f"(a), "f"(b));
-    return r;
+template <uint32_t kBit>
+__device__ __forceinline__ void or_if_ge(uint32_t &m, float a, float b) {
+    asm("{\n\t.reg .pred p;\n\tsetp.ge.f32 p, %1, %2;\n\t@p or.b32 %0, %0, %3;\n\t}" : "+r"(m) : "f"(a), "f"(b), "n"(kBit));
 }
-// bits of b where c is set, bits of a elsewhere (one LOP3)
-__device__ __forceinline__ uint32_t bsel(uint32_t a, uint32_t b, uint32_t c) { return (a & ~c) | (b & c); }
 
 template <bool kInterior, bool kTma, bool kCluster>
 __global__ void __launch_bounds__(kThreads, 2)
@@ -399,24 +396,23 @@ __global__ void __launch_bounds__(kThreads, 2)
         const int d = vm(L, U).d;
         bp_cur = VK{bp_next.v, bp_next.d - PL};
         bm_prev = VK{bm_cur.v, bm_cur.d - PL};
-        // S3: upper mask, lower group (index < v: up iff f > fv), then upper.
-        // set.*.u32 gives an all-ones / all-zeros word; a chain of bit
-        // selects (one LOP3 each) keeps bit k of the k-th word.
-        uint32_t mask = setge(pp[3], fv);
-        mask = bsel(mask, setge(pp[2], fv), 0x1fffu);
-        mask = bsel(mask, setge(pp[1], fv), 0x0fffu);
-        mask = bsel(mask, setge(pp[0], fv), 0x07ffu);
-        mask = bsel(mask, setge(p0[3], fv), 0x03ffu);
-        mask = bsel(mask, setge(p0[2], fv), 0x01ffu);
-        mask = bsel(mask, setge(p0[1], fv), 0x00ffu);
-        mask = bsel(mask, setgt(p0[4], fv), 0x007fu);
-        mask = bsel(mask, setgt(p0[5], fv), 0x003fu);
-        mask = bsel(mask, setgt(p0[6], fv), 0x001fu);
-        mask = bsel(mask, setgt(pm[0], fv), 0x000fu);
-        mask = bsel(mask, setgt(pm[4], fv), 0x0007u);
-        mask = bsel(mask, setgt(pm[5], fv), 0x0003u);
-        mask = bsel(mask, setgt(pm[6], fv), 0x0001u);
-        mask &= 0x3fffu;
+        // S3: upper mask, bit k = k-th link vertex in ascending index order:
+        // lower group (index < v: up iff f > fv), then the upper group (>=).
+        uint32_t mask = 0u;
+        or_if_ge<1u << 13>(mask, pp[3], fv);
+        or_if_ge<1u << 12>(mask, pp[2], fv);
+        or_if_ge<1u << 11>(mask, pp[1], fv);
+        or_if_ge<1u << 10>(mask, pp[0], fv);
+        or_if_ge<1u << 9>(mask, p0[3], fv);
+        or_if_ge<1u << 8>(mask, p0[2], fv);
+        or_if_ge<1u << 7>(mask, p0[1], fv);
+        or_if_gt<1u << 6>(mask, p0[4], fv);
+        or_if_gt<1u << 5>(mask, p0[5], fv);
+        or_if_gt<1u << 4>(mask, p0[6], fv);
+        or_if_gt<1u << 3>(mask, pm[0], fv);
+        or_if_gt<1u << 2>(mask, pm[4], fv);
+        or_if_gt<1u << 1>(mask, pm[5], fv);
+        or_if_gt<1u << 0>(mask, pm[6], fv);
         const int c = cb + (z + 1) * PL;
         if (ok) pbox[c] = uint16_t(c + d);
         const bool sad = (lut[mask >> 5] >> (mask & 31)) & 1u;
