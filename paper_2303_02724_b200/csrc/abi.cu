@@ -75,16 +75,17 @@ struct SlabState {
     FieldView F{};
     int32_t *label = nullptr;          // owned labels (a view)
     DevBuf f_lo, f_hi;                 // halo planes of f received from the neighbours
-    DevBuf sad_bits, max_bits, exit_bits;
+    DevBuf sad_bits, max_bits;
     DevBuf beta8;                      // CSR: beta0+ per owned vertex (from classify)
     DevBuf bval, hval_lo, hval_hi;     // boundary-plane label values (own / neighbours')
     bool has_lo = false, has_hi = false;
     Tiled3D *tiled = nullptr;
+    bool tiled_lists = false;          // maxima / saddles come from the tiled path's lists
     DevBuf maxima64, saddles32, saddles64, sbeta, slot_off, tmp_m, tmp_mult, n_unique, arc_off;
     DevBuf arc_s, arc_m, arc_mult, raw_s, raw_rep, raw_m;
     int64_t n_max = 0, n_sad = 0, n_arc = 0, n_raw = 0;
     ~SlabState() {
-        DevBuf *b[] = {&f_lo, &f_hi, &sad_bits, &max_bits, &exit_bits, &beta8, &bval, &hval_lo, &hval_hi, &maxima64,
+        DevBuf *b[] = {&f_lo, &f_hi, &sad_bits, &max_bits, &beta8, &bval, &hval_lo, &hval_hi, &maxima64,
                        &saddles32, &saddles64, &sbeta, &slot_off, &tmp_m, &tmp_mult, &n_unique, &arc_off, &arc_s,
                        &arc_m, &arc_mult, &raw_s, &raw_rep, &raw_m};
         for (DevBuf *x : b) x->release();
@@ -348,28 +349,44 @@ static eg_status generic_local(eg_ctx *c, const Problem &P, SlabState &S, bool m
 static eg_status grid_graph(eg_ctx *c, const Problem &P, SlabState &S, bool raw) {
     const int64_t n = S.s.v1 - S.s.v0;
     int64_t *cnt = c->counts.as<int64_t>();
-    // two scratch regions: the chunk offsets of each bitmap survive until emission
-    const size_t half = (std::max(compact_scratch_bytes(std::max<int64_t>(n, 1)), size_t(1) << 16) + 255) / 256 * 256;
-    CK(c->scratch.ensure(2 * half));
-    char *scr_max = c->scratch.as<char>(), *scr_sad = c->scratch.as<char>() + half;
-    CK(launch_count_bits(S.max_bits.as<uint32_t>(), n, scr_max, cnt + 0, c->stream));
-    CK(launch_count_bits(S.sad_bits.as<uint32_t>(), n, scr_sad, cnt + 1, c->stream));
-    c->stats.kernel_launches += 4;
     CK(c->h_counts.ensure(sizeof(int64_t) * 8));
     int64_t *hc = c->h_counts.as<int64_t>();
-    CK(cudaMemcpyAsync(hc, cnt, sizeof(int64_t) * 2, cudaMemcpyDeviceToHost, c->stream));
-    CK(cudaStreamSynchronize(c->stream));
-    S.n_max = hc[0];
-    S.n_sad = hc[1];
+    if (S.tiled && S.tiled_lists) {
+        // the tile kernels appended the maxima / saddles to lists: sort them
+        S.n_max = tiled3d_count(S.tiled, 0);
+        S.n_sad = tiled3d_count(S.tiled, 1);
+        CK(S.maxima64.ensure(sizeof(int64_t) * std::max<int64_t>(S.n_max, 1)));
+        CK(S.saddles32.ensure(sizeof(int32_t) * std::max<int64_t>(S.n_sad, 1)));
+        CK(S.saddles64.ensure(sizeof(int64_t) * std::max<int64_t>(S.n_sad, 1)));
+        eg_status st = tiled3d_lists(S.tiled, S.maxima64.as<int64_t>(), S.saddles32.as<int32_t>(),
+                                     S.saddles64.as<int64_t>(), c->stream, &c->stats, &c->err);
+        if (st != EG_OK) {
+            if (st == EG_ERR_CUDA) c->poisoned = true;
+            return st;
+        }
+    } else {
+        // two scratch regions: the chunk offsets of each bitmap survive until emission
+        const size_t half =
+            (std::max(compact_scratch_bytes(std::max<int64_t>(n, 1)), size_t(1) << 16) + 255) / 256 * 256;
+        CK(c->scratch.ensure(2 * half));
+        char *scr_max = c->scratch.as<char>(), *scr_sad = c->scratch.as<char>() + half;
+        CK(launch_count_bits(S.max_bits.as<uint32_t>(), n, scr_max, cnt + 0, c->stream));
+        CK(launch_count_bits(S.sad_bits.as<uint32_t>(), n, scr_sad, cnt + 1, c->stream));
+        c->stats.kernel_launches += 4;
+        CK(cudaMemcpyAsync(hc, cnt, sizeof(int64_t) * 2, cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        S.n_max = hc[0];
+        S.n_sad = hc[1];
+        CK(S.maxima64.ensure(sizeof(int64_t) * std::max<int64_t>(S.n_max, 1)));
+        CK(S.saddles32.ensure(sizeof(int32_t) * std::max<int64_t>(S.n_sad, 1)));
+        CK(S.saddles64.ensure(sizeof(int64_t) * std::max<int64_t>(S.n_sad, 1)));
+        CK(launch_emit_counted(S.max_bits.as<uint32_t>(), n, S.s.v0, scr_max, nullptr, S.maxima64.as<int64_t>(),
+                               c->stream));
+        CK(launch_emit_counted(S.sad_bits.as<uint32_t>(), n, S.s.v0, scr_sad, S.saddles32.as<int32_t>(),
+                               S.saddles64.as<int64_t>(), c->stream));
+        c->stats.kernel_launches += 2;
+    }
     const int64_t ns = S.n_sad;
-    CK(S.maxima64.ensure(sizeof(int64_t) * std::max<int64_t>(S.n_max, 1)));
-    CK(S.saddles32.ensure(sizeof(int32_t) * std::max<int64_t>(ns, 1)));
-    CK(S.saddles64.ensure(sizeof(int64_t) * std::max<int64_t>(ns, 1)));
-    CK(launch_emit_counted(S.max_bits.as<uint32_t>(), n, S.s.v0, scr_max, nullptr, S.maxima64.as<int64_t>(),
-                           c->stream));
-    CK(launch_emit_counted(S.sad_bits.as<uint32_t>(), n, S.s.v0, scr_sad, S.saddles32.as<int32_t>(),
-                           S.saddles64.as<int64_t>(), c->stream));
-    c->stats.kernel_launches += 2;
     CK(cudaEventRecord(c->ev[3], c->stream));
 
     // beta0+ per saddle and slot offsets (sum beta0+ = raw arcs)
@@ -646,12 +663,12 @@ static eg_status compute_grid(eg_ctx *c, const Problem &P, const float *f, uint3
         S.F.plane = P.plane;
         S.has_lo = multi && S.s.z0 > 0;
         S.has_hi = multi && S.s.z1 < P.D;
-        CK(S.sad_bits.ensure(sizeof(uint32_t) * std::max<int64_t>(words, 1)));
-        CK(S.max_bits.ensure(sizeof(uint32_t) * std::max<int64_t>(words, 1)));
-        if (tiled) {
-            CK(S.exit_bits.ensure(sizeof(uint32_t) * std::max<int64_t>(words, 1)));
-            if (!S.tiled) S.tiled = tiled3d_create();
+        if (!tiled) {
+            CK(S.sad_bits.ensure(sizeof(uint32_t) * std::max<int64_t>(words, 1)));
+            CK(S.max_bits.ensure(sizeof(uint32_t) * std::max<int64_t>(words, 1)));
         }
+        if (tiled && !S.tiled) S.tiled = tiled3d_create();
+        S.tiled_lists = tiled;
         if (multi) {
             CK(S.f_lo.ensure(sizeof(float) * P.plane));
             CK(S.f_hi.ensure(sizeof(float) * P.plane));
@@ -690,8 +707,7 @@ static eg_status compute_grid(eg_ctx *c, const Problem &P, const float *f, uint3
     for (SlabState *S : c->slabs) {
         const bool first = S == c->slabs[0];
         if (tiled) {
-            eg_status s = tiled3d_local(S->tiled, P.ndim, P.dims, S->s, S->F, S->label, S->sad_bits.as<uint32_t>(),
-                                        S->max_bits.as<uint32_t>(), S->exit_bits.as<uint32_t>(), c->flags.as<int>(),
+            eg_status s = tiled3d_local(S->tiled, P.ndim, P.dims, S->s, S->F, S->label, c->flags.as<int>(),
                                         c->stream, &c->stats, &c->err, first ? c->ev_main[0] : nullptr,
                                         first ? c->ev_main[1] : nullptr);
             if (s != EG_OK) {
@@ -712,7 +728,7 @@ static eg_status compute_grid(eg_ctx *c, const Problem &P, const float *f, uint3
     }
     for (SlabState *S : c->slabs) {
         if (!tiled && !multi) continue;           // generic single slab: already final
-        CK(launch_finalize(S->label, tiled ? S->exit_bits.as<uint32_t>() : nullptr, S->s.v0, S->s.v1,
+        CK(launch_finalize(S->label, nullptr, S->s.v0, S->s.v1,
                            S->has_lo ? S->hval_lo.as<int32_t>() : nullptr,
                            S->has_hi ? S->hval_hi.as<int32_t>() : nullptr, P.plane, c->stream));
         c->stats.kernel_launches += 1;
@@ -760,6 +776,7 @@ static eg_status compute_csr(eg_ctx *c, const Problem &P, const float *f, uint32
         const int64_t words = (S.s.v1 - S.s.v0 + 31) / 32;
         CK(S.sad_bits.ensure(sizeof(uint32_t) * std::max<int64_t>(words, 1)));
         CK(S.max_bits.ensure(sizeof(uint32_t) * std::max<int64_t>(words, 1)));
+        S.tiled_lists = false;
         CK(S.beta8.ensure(std::max<int64_t>(S.s.v1 - S.s.v0, 1)));
         S.has_lo = S.has_hi = false;
     }

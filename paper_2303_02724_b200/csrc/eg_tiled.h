@@ -10,12 +10,17 @@ Tiled3D *tiled3d_create();
 void tiled3d_destroy(Tiled3D *t);
 // S1 + S3 and the slab-local part of S2 for the owned planes of slab `s` of an
 // n <= 3 grid: labels (owned, index v - s.v0) final or kUnresolved | x (see
-// eg_impl.h), saddle / maximum / exit bitmaps over the owned vertices, NaN
-// flag in flags[0].  Exiting vertices still point at their exit target: the
-// caller finishes them with launch_finalize (after the boundary exchange when
-// there are several slabs).
+// eg_impl.h), the maxima and saddles of the owned vertices (kept in `t`, see
+// tiled3d_lists), NaN flag in flags[0].  Exiting vertices still point at
+// their exit target: the caller finishes them with launch_finalize (after the
+// boundary exchange when there are several slabs).
 eg_status tiled3d_local(Tiled3D *t, int ndim, const int64_t *dims, const Slab &s, const FieldView &F, int32_t *labels,
-                        uint32_t *sad_bits, uint32_t *max_bits, uint32_t *exit_bits, int *flags, cudaStream_t st,
-                        eg_stats *stats, std::string *err, cudaEvent_t ev_main0 = nullptr,
-                        cudaEvent_t ev_main1 = nullptr);
+                        int *flags, cudaStream_t st, eg_stats *stats, std::string *err,
+                        cudaEvent_t ev_main0 = nullptr, cudaEvent_t ev_main1 = nullptr);
+// number of maxima (which = 0) / saddles (which = 1) found by the last tiled3d_local
+int64_t tiled3d_count(const Tiled3D *t, int which);
+// the maxima (int64) and saddles (int32 and int64) of the last tiled3d_local,
+// ascending; outputs sized by tiled3d_count
+eg_status tiled3d_lists(Tiled3D *t, int64_t *max64, int32_t *sad32, int64_t *sad64, cudaStream_t st,
+                        eg_stats *stats, std::string *err);
 }  // namespace eg

@@ -89,7 +89,7 @@ cudaError_t launch_bval_update(int32_t *bval, const int32_t *hval_lo, const int3
 
 // Final pass.  A warp owns kW words of owned vertices (32 kW vertices); the
 // loads of all of them are issued before any is used (memory-level
-// parallelism for the dependent gather).
+// parallelism for the dependent gather), and only changed labels are stored.
 constexpr int kW = 8;
 __global__ void __launch_bounds__(256) k_finalize(int32_t *label, const uint32_t *__restrict__ bits, int64_t v0,
                                                   int64_t v1, const int32_t *__restrict__ hlo,
@@ -113,11 +113,13 @@ __global__ void __launch_bounds__(256) k_finalize(int32_t *label, const uint32_t
     }
 #pragma unroll
     for (int k = 0; k < kW; ++k) e[k] = need[k] ? label[(w0 + k) * 32 + lane] : 0;
+#pragma unroll
+    for (int k = 0; k < kW; ++k) need[k] = need[k] && e[k] < 0;
     if (!hlo && !hhi) {
         // one slab: every exit target is owned and final
 #pragma unroll
         for (int k = 0; k < kW; ++k)
-            if (need[k] && e[k] < 0) e[k] = __ldg(label + ((e[k] & 0x7fffffff) - v0));
+            if (need[k]) e[k] = __ldg(label + ((e[k] & 0x7fffffff) - v0));
 #pragma unroll
         for (int k = 0; k < kW; ++k)
             if (need[k]) label[(w0 + k) * 32 + lane] = e[k];
@@ -125,7 +127,6 @@ __global__ void __launch_bounds__(256) k_finalize(int32_t *label, const uint32_t
     }
 #pragma unroll
     for (int k = 0; k < kW; ++k) {
-        need[k] = need[k] && e[k] < 0;
         if (need[k]) {
             int64_t x = e[k] & 0x7fffffff;
             if (x >= v0 && x < v1) {

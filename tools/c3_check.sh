@@ -3,7 +3,7 @@
 # usage: tools/c3_check.sh <tag> [full]
 tag=${1:-run}
 mkdir -p gpurun_out
-python -m pytest tests/test_gpu_parity.py tests/test_gpu_cluster.py tests/test_gpu_configs.py -x -q 2>&1 | tail -3
+python -m pytest tests -m gpu -x -q 2>&1 | tail -3
 for i in 1 2; do
   timeout 600 python bench.py --config C3 --steps 10 --warmup 3 --no-cpu --no-e2e 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(d['ms_per_step'], d['phases_us'], d['graph'], d['parity_sample'], d['roofline']['frac'])"
 done
