@@ -12,7 +12,7 @@
 //               so the argmax is 2x2 in-plane maxima combined across z;
 //           S3  the 14-bit upper mask -> "beta0+ >= 2" from a 2 KB bit LUT
 //               (Table 1; maximum iff the mask is empty).
-//         The gradients are stored as 16-bit indices into a pointer box and
+//         The gradients are stored as 16-bit byte offsets into a pointer box and
 //         compressed in shared memory (S2 inside the tile): every vertex ends
 //         at an in-tile maximum (its final label) or at the first halo vertex
 //         on its path (an exit: the path leaves the tile, the paper's partial
@@ -45,7 +45,7 @@ constexpr int BY = TY + 2, BZ = TZ + 2;
 constexpr int PL = BX * BY;                          // 720 cells per plane of the field box
 constexpr int BOX = PL * BZ;                         // 12960 field-box cells = one TMA box
 constexpr int PS = 1024;                             // pointer-box plane stride: cell r = bz * PS + by * BX + bx
-constexpr int PBOX = BZ * PS;                        // 18432 < 65536: 16-bit pointer-box indices
+constexpr int PBOX = BZ * PS;                        // 18432 cells; pointers are byte offsets 2 r < 65536 (16 bits)
 constexpr int kThreads = TX * TY;                    // one z-column per thread
 constexpr int kWarps = kThreads / 32;
 constexpr int kLutWords = (1 << 14) / 32;            // 1 bit per 14-bit upper mask: beta0+ >= 2
@@ -60,7 +60,7 @@ constexpr size_t kOffL = kOffP + size_t(PBOX) * 2;
 constexpr size_t kOffM = kOffL + size_t(kLutWords) * 4;
 constexpr size_t kOffT = kOffM + 256;
 constexpr size_t kTileSmem = kOffT + size_t(PL) * 4;   // ~92 KB -> 2 CTAs per SM
-static_assert(PBOX <= BOX * 4, "exit marks (1 byte per pointer-box cell) fit the dead field box");
+static_assert(2 * PBOX <= BOX * 4, "exit marks (1 byte per pointer-box byte offset) fit the dead field box");
 static_assert(TZ == 16, "saddle / maximum column masks pack into one 32-bit word");
 
 struct Tiled3D {
@@ -122,7 +122,7 @@ struct TileArgs {
     int64_t ecap;
     const uint32_t *lut;
     const int32_t *ptab;            // per box-plane cell: by * nx + bx, bit 31 = in-plane shell
-    const uint16_t *shell;          // kShell pointer-box indices
+    const uint16_t *shell;          // kShell pointer-box byte offsets
     const int32_t *btiles;          // boundary variant: packed tile ids
     int32_t tiles_x, tiles_y;       // interior variant: sub-box extents
     int3 origin;                    // interior variant: first interior tile
@@ -173,8 +173,16 @@ struct VK {           // a value with its pointer-box offset from the centre ver
     int d;
 };
 
-// b wins ties: b is the later (higher-index) operand
-__device__ __forceinline__ VK vmax(VK a, VK b) { return b.v >= a.v ? b : a; }
+// b wins ties: b is the later (higher-index) operand.  Both selects are
+// integer SELs (full rate; FSEL issues at half rate on sm_100, measured with
+// tools/pipe_probe).
+__device__ __forceinline__ VK vmax(VK a, VK b) {
+    VK r;
+    asm("{\n\t.reg .pred p;\n\tsetp.ge.f32 p, %2, %3;\n\tselp.b32 %0, %2, %3, p;\n\tselp.b32 %1, %4, %5, p;\n\t}"
+        : "=f"(r.v), "=r"(r.d)
+        : "f"(b.v), "f"(a.v), "r"(b.d), "r"(a.d));
+    return r;
+}
 // the same where NaN marks a cell outside the domain: a NaN never wins
 __device__ __forceinline__ VK vmaxn(VK a, VK b) { return (b.v >= a.v || a.v != a.v) ? b : a; }
 
@@ -207,7 +215,15 @@ __global__ void __launch_bounds__(kThreads, 2)
     k_tile(const __grid_constant__ CUtensorMap tmap, TileArgs A, Dims3 D) {
     extern __shared__ __align__(128) unsigned char smem[];
     float *fbox = reinterpret_cast<float *>(smem);
-    uint16_t *pbox = reinterpret_cast<uint16_t *>(smem + kOffP);
+    unsigned char *pb = smem + kOffP;
+    // the pointer box holds byte offsets: a chase step is one load at base + value
+    auto P = [pb](int b) -> uint16_t & { return *reinterpret_cast<uint16_t *>(pb + b); };
+    const uint32_t pbase = smem_u32(pb);
+    auto ld16 = [](uint32_t a) -> uint32_t {
+        uint32_t v;
+        asm volatile("ld.shared.u16 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
+        return v;
+    };
     uint32_t *lut = reinterpret_cast<uint32_t *>(smem + kOffL);
     uint64_t *bar = reinterpret_cast<uint64_t *>(smem + kOffM);
     uint32_t *red = reinterpret_cast<uint32_t *>(smem + kOffM + 16);                 // [kWarps] warp offsets
@@ -281,7 +297,7 @@ __global__ void __launch_bounds__(kThreads, 2)
     // shell cells of the pointer box are terminal (point to themselves)
     for (int s = tid; s < kShell; s += kThreads) {
         const int i = __ldg(A.shell + s);
-        pbox[i] = uint16_t(i);
+        P(i) = uint16_t(i);
     }
     for (int i = tid; i < kLutWords; i += kThreads) lut[i] = __ldg(A.lut + i);
     for (int i = tid; i < PL; i += kThreads) ptab[i] = __ldg(A.ptab + i);
@@ -299,6 +315,7 @@ __global__ void __launch_bounds__(kThreads, 2)
     const int gx = x0 + tx, gy = y0 + ty;
     const bool col_ok = kInterior || (gx < D.nx && gy < D.ny);
     const int cf = (ty + 1) * BX + tx + XO;          // this column's in-plane cell (both boxes)
+    const int cfb = 2 * cf;                          // ... as a pointer-box byte offset
 
     // 2-D star of box plane bz at this column: c, (1,0), (0,1), (1,1), (-1,0), (0,-1), (-1,-1)
     auto star = [&](int bz, float *s) {
@@ -312,18 +329,18 @@ __global__ void __launch_bounds__(kThreads, 2)
         s[6] = p[-BX - 1];
     };
     // in-plane 2x2 maxima (ascending index order inside each, later wins
-    // ties), offsets in pointer-box units.  Edge tiles hold NaN in the cells
+    // ties), offsets in pointer-box bytes.  Edge tiles hold NaN in the cells
     // outside the domain: a NaN never wins (vmaxn) and every compare with it
     // is false, so the truncated link (reading L3) falls out of the same code.
     auto vm = [](VK a, VK b) -> VK { return kInterior ? vmax(a, b) : vmaxn(a, b); };
     auto bplus = [&](const float *s, int dz) -> VK {    // (0,0) (1,0) (0,1) (1,1)
-        VK a = vm(VK{s[0], dz * PS}, VK{s[1], 1 + dz * PS});
-        VK b = vm(VK{s[2], BX + dz * PS}, VK{s[3], BX + 1 + dz * PS});
+        VK a = vm(VK{s[0], 2 * (dz * PS)}, VK{s[1], 2 * (1 + dz * PS)});
+        VK b = vm(VK{s[2], 2 * (BX + dz * PS)}, VK{s[3], 2 * (BX + 1 + dz * PS)});
         return vm(a, b);
     };
     auto bminus = [&](const float *s, int dz) -> VK {   // (-1,-1) (0,-1) (-1,0) (0,0)
-        VK a = vm(VK{s[6], -BX - 1 + dz * PS}, VK{s[5], -BX + dz * PS});
-        VK b = vm(VK{s[4], -1 + dz * PS}, VK{s[0], dz * PS});
+        VK a = vm(VK{s[6], 2 * (-BX - 1 + dz * PS)}, VK{s[5], 2 * (-BX + dz * PS)});
+        VK b = vm(VK{s[4], 2 * (-1 + dz * PS)}, VK{s[0], 2 * (dz * PS)});
         return vm(a, b);
     };
 
@@ -344,8 +361,8 @@ __global__ void __launch_bounds__(kThreads, 2)
         const VK U = vm(bp_cur, bp_next);
         const VK L = vm(bm_prev, bm_cur);
         int d = vm(L, U).d;
-        bp_cur = VK{bp_next.v, bp_next.d - PS};
-        bm_prev = VK{bm_cur.v, bm_cur.d - PS};
+        bp_cur = VK{bp_next.v, bp_next.d - 2 * PS};
+        bm_prev = VK{bm_cur.v, bm_cur.d - 2 * PS};
         // S3: upper mask, bit k = k-th link vertex in ascending index order:
         // lower group (index < v: up iff f > fv), then the upper group (>=).
         uint32_t mask = 0u;
@@ -366,8 +383,8 @@ __global__ void __launch_bounds__(kThreads, 2)
         // an empty upper link points to itself; this also makes a NaN vertex
         // (every compare false) terminal, so no pointer cycle can form
         d = mask ? d : 0;
-        const int c = cf + (z + 1) * PS;
-        pbox[c] = uint16_t(kInterior || ok ? c + d : c);
+        const int c = cfb + 2 * (z + 1) * PS;
+        P(c) = uint16_t(kInterior || ok ? c + d : c);
         const uint32_t sad = (lut[mask >> 5] >> (mask & 31)) & 1u;
         sad_mask |= ((kInterior || ok) ? sad : 0u) << z;
         max_mask |= ((kInterior || ok) && mask == 0) ? (1u << z) : 0u;
@@ -394,13 +411,13 @@ __global__ void __launch_bounds__(kThreads, 2)
     // so nothing needs settling, and chains that run into a finished cell end
     // one hop later.
     uint8_t *used = reinterpret_cast<uint8_t *>(fbox);
-    for (int i = tid; i < PBOX / 16; i += kThreads) reinterpret_cast<uint4 *>(used)[i] = make_uint4(0, 0, 0, 0);
+    for (int i = tid; i < 2 * PBOX / 16; i += kThreads) reinterpret_cast<uint4 *>(used)[i] = make_uint4(0, 0, 0, 0);
 #pragma unroll 1
     for (int round = 0; round < A.rounds; ++round) {
 #pragma unroll
         for (int z = 0; z < TZ; ++z) {
-            const int c = cf + (z + 1) * PS;
-            pbox[c] = pbox[pbox[c]];
+            const int c = cfb + 2 * (z + 1) * PS;
+            P(c) = P(P(c));
         }
         __syncthreads();
     }
@@ -415,12 +432,19 @@ __global__ void __launch_bounds__(kThreads, 2)
 #pragma unroll 2
     for (int z = 0; z < TZ; ++z) {
         const bool ok = col_ok && (kInterior || z0 + z < A.z_hi);
-        const int c = cf + (z + 1) * PS;
-        int r = pbox[c];
-        for (int q; (q = pbox[r]) != r;) r = q;
-        pbox[c] = uint16_t(r);
-        const int bz = r >> 10;
-        const int32_t t = ptab[r & (PS - 1)];
+        const int c = cfb + 2 * (z + 1) * PS;
+        // chase to the root (a cell that points to itself), two hops per
+        // loop turn so that no register copies are needed
+        uint32_t r = ld16(pbase + c);
+        for (;;) {
+            const uint32_t q = ld16(pbase + r);
+            if (q == r) break;
+            r = ld16(pbase + q);
+            if (r == q) break;
+        }
+        P(c) = uint16_t(r);
+        const int bz = r >> 11;
+        const int32_t t = *reinterpret_cast<const int32_t *>(reinterpret_cast<const char *>(ptab) + ((r & (2 * PS - 2)) << 1));
         // exit: the root is in the halo shell of the box, or (last tile of a
         // slab) in a plane the slab does not own
         bool exit = t < 0 || unsigned(bz - 1) >= unsigned(TZ);
@@ -492,7 +516,7 @@ __global__ void __launch_bounds__(kThreads, 2)
         const uint32_t b = __ballot_sync(0xffffffffu, m);
         if (m) {
             const unsigned long long j = slot + __popc(b & lt);
-            if (j < (unsigned long long)A.ecap) A.elist[j] = g_box0 + (i >> 10) * nxy + (ptab[i & (PS - 1)] & 0x7fffffff);
+            if (j < (unsigned long long)A.ecap) A.elist[j] = g_box0 + (i >> 11) * nxy + (ptab[(i >> 1) & (PS - 1)] & 0x7fffffff);
         }
         slot += __popc(b);
     }
@@ -592,7 +616,7 @@ eg_status tiled3d_local(Tiled3D *t, int ndim, const int64_t *dims, const Slab &s
             for (int by = 0; by < BY; ++by)
                 for (int bx = XO - 1; bx <= XO + TX; ++bx)
                     if (bz == 0 || bz == BZ - 1 || by == 0 || by == BY - 1 || bx == XO - 1 || bx == XO + TX)
-                        sh.push_back(uint16_t(bz * PS + by * BX + bx));
+                        sh.push_back(uint16_t(2 * (bz * PS + by * BX + bx)));
         if (int(sh.size()) != kShell) {
             if (err) *err = "shell size";
             return EG_ERR_STATE;
