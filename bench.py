@@ -238,6 +238,8 @@ def run_ours(args):
     ctx = eg.init_distributed(stream=stream) if (world > 1 and parallelism != "replicas") else \
         eg.Context(torch.cuda.current_device(), stream)
     flags = eg.EG_CHECK_NAN
+    if os.environ.get("EG_BENCH_VPARTS"):          # experiments: k virtual slabs on one GPU
+        flags |= eg.EG_VIRTUAL_PARTS(int(os.environ["EG_BENCH_VPARTS"]))
 
     for _ in range(args.warmup):
         g = ctx.compute(f, flags=flags, **kw)
