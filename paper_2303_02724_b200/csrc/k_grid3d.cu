@@ -127,6 +127,7 @@ struct TileArgs {
     int32_t tiles_x, tiles_y;       // interior variant: sub-box extents
     int3 origin;                    // interior variant: first interior tile
     int32_t rounds;                 // pointer-doubling rounds before the chase
+    int32_t no_elist;               // one slab: no exit-target list (finalize chases with memoisation)
     int32_t tma;                    // field box by TMA (else plain row loads)
 };
 
@@ -452,7 +453,7 @@ __global__ void __launch_bounds__(kThreads, 2)
         const int32_t root = g_box0 + bz * nxy + (t & 0x7fffffff);
         if (kInterior || ok) {
             A.label[i_col + z * nxy] = exit ? int32_t(uint32_t(root) | kFlag) : root;
-            if (exit) used[r] = 1;
+            if (exit && !A.no_elist) used[r] = 1;
         }
     }
 
@@ -483,6 +484,7 @@ __global__ void __launch_bounds__(kThreads, 2)
                 if (js < (unsigned long long)A.list_cap) A.sad_list[js] = g0 + (__ffs(m) - 1) * nxy;
         }
     }
+    if (A.no_elist) return;
     __syncthreads();
 
     // ---- append the tile's exit targets (marked shell cells) to E: per-warp
@@ -742,6 +744,9 @@ eg_status tiled3d_local(Tiled3D *t, int ndim, const int64_t *dims, const Slab &s
         A.shell = t->d_shell;
         A.btiles = t->d_btiles;
         A.rounds = t->rounds;
+        // one slab: no exit list, the finalize pass chases (EG_ELIST=1 forces the list)
+        const char *el = std::getenv("EG_ELIST");
+        A.no_elist = (!F.lo && !F.hi && !(el && el[0] == '1')) ? 1 : 0;
         A.tma = tma ? 1 : 0;
         if (ev_main0) cudaEventRecord(ev_main0, st);
         if (t->n_btiles > 0) {
@@ -760,9 +765,11 @@ eg_status tiled3d_local(Tiled3D *t, int ndim, const int64_t *dims, const Slab &s
         }
         if (ev_main1) cudaEventRecord(ev_main1, st);
         // resolve the owned part of E
-        k_resolve_exits<<<148 * 64, 256, 0, st>>>(labels, t->d_elist, t->d_ecount, t->ecap, s.v0, s.v1);
-        stats->kernel_launches += 1;
-        if ((e = cudaGetLastError()) != cudaSuccess) return fail(err, e, "k_resolve_exits");
+        if (!A.no_elist) {
+            k_resolve_exits<<<148 * 64, 256, 0, st>>>(labels, t->d_elist, t->d_ecount, t->ecap, s.v0, s.v1);
+            stats->kernel_launches += 1;
+            if ((e = cudaGetLastError()) != cudaSuccess) return fail(err, e, "k_resolve_exits");
+        }
         unsigned long long cnt[3] = {0, 0, 0};
         if ((e = cudaMemcpyAsync(cnt, t->d_ecount, sizeof(cnt), cudaMemcpyDeviceToHost, st)) != cudaSuccess ||
             (e = cudaStreamSynchronize(st)) != cudaSuccess)

@@ -116,10 +116,28 @@ __global__ void __launch_bounds__(256) k_finalize(int32_t *label, const uint32_t
 #pragma unroll
     for (int k = 0; k < kW; ++k) need[k] = need[k] && e[k] < 0;
     if (!hlo && !hhi) {
-        // one slab: every exit target is owned and final
+        // one slab: every exit target is owned.  Its label is final when the
+        // exit list was resolved first (k_resolve_exits); otherwise the chain
+        // is chased here and its final label memoised in the first target
+        // (race-benign: every value ever stored is a later vertex of the same
+        // ascending path; compressing the whole chain measured 5x slower).
+        int32_t tg[kW];
 #pragma unroll
-        for (int k = 0; k < kW; ++k)
-            if (need[k]) e[k] = __ldg(label + ((e[k] & 0x7fffffff) - v0));
+        for (int k = 0; k < kW; ++k) {
+            tg[k] = e[k] & 0x7fffffff;
+            if (need[k]) e[k] = *(volatile const int32_t *)(label + (tg[k] - v0));
+        }
+#pragma unroll
+        for (int k = 0; k < kW; ++k) {
+            if (need[k] && e[k] < 0) {
+                int32_t w = e[k];
+                do {
+                    w = *(volatile const int32_t *)(label + ((w & 0x7fffffff) - v0));
+                } while (w < 0);
+                e[k] = w;
+                label[tg[k] - v0] = w;
+            }
+        }
 #pragma unroll
         for (int k = 0; k < kW; ++k)
             if (need[k]) label[(w0 + k) * 32 + lane] = e[k];
