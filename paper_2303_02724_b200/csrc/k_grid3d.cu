@@ -690,7 +690,15 @@ eg_status tiled3d_local(Tiled3D *t, int ndim, const int64_t *dims, const Slab &s
         t->ptab_nx = d3[0];
     }
     // exit-target list capacity: N / 8 (falls back to a per-vertex chase on overflow)
-    const int64_t want = std::max<int64_t>(nown / 8, 4096);
+    // (EG_LIST_DIV / EG_ELIST_DIV: test knobs that start the lists small, to
+    // exercise the grow-and-rerun path)
+    auto env_div = [](const char *name, int64_t dflt) {
+        const char *v = std::getenv(name);
+        const int64_t d = v ? std::atoll(v) : 0;
+        return d > 0 ? d : dflt;
+    };
+    const int64_t floor_cap = std::getenv("EG_LIST_DIV") ? 16 : (1 << 16);
+    const int64_t want = std::max<int64_t>(nown / env_div("EG_ELIST_DIV", 8), std::getenv("EG_ELIST_DIV") ? 16 : 4096);
     if (t->ecap < want) {
         if (t->d_elist) cudaFree(t->d_elist);
         t->d_elist = nullptr;
@@ -700,8 +708,8 @@ eg_status tiled3d_local(Tiled3D *t, int ndim, const int64_t *dims, const Slab &s
     }
     // maxima / saddle list capacity: N / 4 to start with (a noisy field has
     // ~15 % saddles); on overflow the lists grow and the pass runs again
-    if (t->list_cap < std::max<int64_t>(nown / 4, 1 << 16)) {
-        const int64_t cap = std::max<int64_t>(nown / 4, 1 << 16);
+    if (t->list_cap < std::max<int64_t>(nown / env_div("EG_LIST_DIV", 4), floor_cap)) {
+        const int64_t cap = std::max<int64_t>(nown / env_div("EG_LIST_DIV", 4), floor_cap);
         if ((e = grow_lists(t, cap)) != cudaSuccess) return fail(err, e, "cudaMalloc lists");
     }
     // TMA tensor map over the owned planes (needs 16-byte row and plane

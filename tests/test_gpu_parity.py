@@ -279,3 +279,19 @@ def test_virtual_slabs_invalid(eg, ctx):
     with pytest.raises(eg.EgError) as e:          # 5 planes cannot make 3 slabs of >= 2 planes
         ctx.compute(torch.from_numpy(f).cuda(), dims=dims, flags=eg.EG_VIRTUAL_PARTS(3))
     assert "INVALID_ARG" in str(e.value)
+
+
+@pytest.mark.parametrize("env", [{"EG_LIST_DIV": "100000"},                       # maxima/saddle lists regrow + rerun
+                                 {"EG_ELIST": "1"},                               # one slab with the exit list + resolve
+                                 {"EG_ELIST": "1", "EG_ELIST_DIV": "100000"}])    # exit list overflow -> per-vertex chase
+def test_tiled_capacity_paths(eg, env, monkeypatch):
+    """The tiled path's fallbacks (list growth, exit list, exit-list overflow) stay bit-exact."""
+    import torch
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    ctx = eg.Context()
+    for dims, kind in [([96, 64, 48], "int"), ([70, 41, 37], "normal")]:
+        f, _ = G.random_field(dims, 23 + len(dims), kind)
+        o = O.grid(f, dims)
+        g = ctx.compute(torch.from_numpy(f).cuda(), dims=dims)
+        assert_graph_equal(g, o, what=f"{env} {dims} {kind}")
