@@ -184,8 +184,15 @@ __device__ __forceinline__ VK vmax(VK a, VK b) {
         : "f"(b.v), "f"(a.v), "r"(b.d), "r"(a.d));
     return r;
 }
-// the same where NaN marks a cell outside the domain: a NaN never wins
-__device__ __forceinline__ VK vmaxn(VK a, VK b) { return (b.v >= a.v || a.v != a.v) ? b : a; }
+// b is the earlier (lower-index) operand: it wins only if strictly greater
+// (so ties keep the later a, and a NaN b never wins)
+__device__ __forceinline__ VK vearlier(VK a, VK b) {
+    VK r;
+    asm("{\n\t.reg .pred p;\n\tsetp.gt.f32 p, %2, %3;\n\tselp.b32 %0, %2, %3, p;\n\tselp.b32 %1, %4, %5, p;\n\t}"
+        : "=f"(r.v), "=r"(r.d)
+        : "f"(b.v), "f"(a.v), "r"(b.d), "r"(a.d));
+    return r;
+}
 
 // IEEE compares (no ftz: distinct denormals stay distinct, reading L2; a NaN
 // compares false): m |= kBit if a > b (a >= b), one FSETP + one predicated add
@@ -329,20 +336,25 @@ __global__ void __launch_bounds__(kThreads, 2)
         s[5] = p[-BX];
         s[6] = p[-BX - 1];
     };
-    // in-plane 2x2 maxima (ascending index order inside each, later wins
-    // ties), offsets in pointer-box bytes.  Edge tiles hold NaN in the cells
-    // outside the domain: a NaN never wins (vmaxn) and every compare with it
-    // is false, so the truncated link (reading L3) falls out of the same code.
-    auto vm = [](VK a, VK b) -> VK { return kInterior ? vmax(a, b) : vmaxn(a, b); };
+    // in-plane 2x2 maxima, offsets in pointer-box bytes, as scans that start
+    // at the column's own cell: B+ forward in index order (a later cell wins
+    // ties), B- backward (an earlier cell must be strictly greater).  Cells
+    // outside the domain hold NaN (TMA fill): a NaN never wins, and every
+    // compare with it is false, so the truncated link (reading L3) falls out
+    // of the same code for every tile.
     auto bplus = [&](const float *s, int dz) -> VK {    // (0,0) (1,0) (0,1) (1,1)
-        VK a = vm(VK{s[0], 2 * (dz * PS)}, VK{s[1], 2 * (1 + dz * PS)});
-        VK b = vm(VK{s[2], 2 * (BX + dz * PS)}, VK{s[3], 2 * (BX + 1 + dz * PS)});
-        return vm(a, b);
+        VK m{s[0], 2 * (dz * PS)};
+        m = vmax(m, VK{s[1], 2 * (1 + dz * PS)});
+        m = vmax(m, VK{s[2], 2 * (BX + dz * PS)});
+        m = vmax(m, VK{s[3], 2 * (BX + 1 + dz * PS)});
+        return m;
     };
-    auto bminus = [&](const float *s, int dz) -> VK {   // (-1,-1) (0,-1) (-1,0) (0,0)
-        VK a = vm(VK{s[6], 2 * (-BX - 1 + dz * PS)}, VK{s[5], 2 * (-BX + dz * PS)});
-        VK b = vm(VK{s[4], 2 * (-1 + dz * PS)}, VK{s[0], 2 * (dz * PS)});
-        return vm(a, b);
+    auto bminus = [&](const float *s, int dz) -> VK {   // (0,0) (-1,0) (0,-1) (-1,-1), backwards
+        VK m{s[0], 2 * (dz * PS)};
+        m = vearlier(m, VK{s[4], 2 * (-1 + dz * PS)});
+        m = vearlier(m, VK{s[5], 2 * (-BX + dz * PS)});
+        m = vearlier(m, VK{s[6], 2 * (-BX - 1 + dz * PS)});
+        return m;
     };
 
     float pm[7], p0[7], pp[7];
@@ -359,9 +371,9 @@ __global__ void __launch_bounds__(kThreads, 2)
         // S1: argmax over box(v) u box(v - 1); the upper box wins ties
         const VK bp_next = bplus(pp, 1);
         const VK bm_cur = bminus(p0, 0);
-        const VK U = vm(bp_cur, bp_next);
-        const VK L = vm(bm_prev, bm_cur);
-        int d = vm(L, U).d;
+        const VK U = vmax(bp_cur, bp_next);        // B+(z+1) is later (NaN beyond the domain)
+        const VK L = vearlier(bm_cur, bm_prev);     // B-(z-1) is earlier (NaN below the domain)
+        int d = vmax(L, U).d;
         bp_cur = VK{bp_next.v, bp_next.d - 2 * PS};
         bm_prev = VK{bm_cur.v, bm_cur.d - 2 * PS};
         // S3: upper mask, bit k = k-th link vertex in ascending index order:
@@ -651,11 +663,12 @@ eg_status tiled3d_local(Tiled3D *t, int ndim, const int64_t *dims, const Slab &s
         if (err) *err = "grid too large for the tiled path";
         return EG_ERR_UNSUPPORTED;
     }
-    // interior tiles: x/y halo box inside the domain and z box inside the
-    // owned planes: 1 <= b <= (extent - 1 - T) / T on every axis
-    int3 lo = make_int3(1, 1, 1);
-    int3 hi = make_int3(int((d3[0] - 1 - TX) / TX), int((d3[1] - 1 - TY) / TY), int((z_hi - z_lo - 1 - TZ) / TZ));
-    if (d3[0] - 1 - TX < 0 || d3[1] - 1 - TY < 0 || z_hi - z_lo - 1 - TZ < 0) hi = make_int3(0, 0, 0);
+    // "interior" tiles: every own cell inside the domain and the owned planes
+    // (full tiles; the halo may be outside the domain -- NaN by TMA), and no
+    // halo plane held by a neighbour slab (those tiles patch it in)
+    const int nfx = int(d3[0] / TX), nfy = int(d3[1] / TY), nfz = int((z_hi - z_lo) / TZ);
+    int3 lo = make_int3(0, 0, F.lo ? 1 : 0);
+    int3 hi = make_int3(nfx - 1, nfy - 1, nfz - 1 - ((F.hi && int64_t(nfz) * TZ == z_hi - z_lo) ? 1 : 0));
     const bool have_interior = hi.x >= lo.x && hi.y >= lo.y && hi.z >= lo.z;
     // boundary tile list, cached per (dims, slab)
     if (t->bdims[0] != d3[0] || t->bdims[1] != d3[1] || t->bdims[2] != d3[2] || t->bz[0] != z_lo || t->bz[1] != z_hi) {
