@@ -10,7 +10,7 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libeg_b200.so")
+LIB_PATH = os.environ.get("EG_LIB_PATH") or os.path.join(HERE, "libeg_b200.so")   # (override: timing experiments)
 
 EG_OK, EG_ERR_INVALID_ARG, EG_ERR_NAN, EG_ERR_OOM, EG_ERR_CUDA, EG_ERR_NCCL, EG_ERR_STATE, EG_ERR_UNSUPPORTED = range(8)
 STATUS_NAMES = ["EG_OK", "EG_ERR_INVALID_ARG", "EG_ERR_NAN", "EG_ERR_OOM", "EG_ERR_CUDA", "EG_ERR_NCCL",
