@@ -11,6 +11,10 @@ __global__ void __launch_bounds__(256) k(float *out, float b, int iters, long lo
     float x[CH];
     uint32_t m[CH];
     for (int i = 0; i < CH; ++i) { x[i] = threadIdx.x * 0.001f + i; m[i] = threadIdx.x + i; }
+    __shared__ uint32_t sh[256];
+    sh[threadIdx.x & 255] = threadIdx.x;
+    __syncthreads();
+    const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(sh);
     long long t0 = clock64();
     for (int it = 0; it < iters; ++it) {
 #pragma unroll
@@ -28,6 +32,9 @@ __global__ void __launch_bounds__(256) k(float *out, float b, int iters, long lo
             if (K == 10) asm volatile("{.reg .pred p; setp.ge.f32 p, %1, %2; selp.b32 %0, 5, %0, p;}" : "+r"(m[i]) : "f"(x[i]), "f"(b));
             if (K == 11) asm volatile("add.f32 %0, %0, %1;" : "+f"(x[i]) : "f"(x[(i + 1) % CH]));
             if (K == 12) asm volatile("shf.l.wrap.b32 %0, %1, %0, 1;" : "+r"(m[i]) : "r"(m[(i + 1) % CH]));
+            if (K == 13) { uint32_t v; asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(sbase + ((m[i] & 255u) << 2))); m[i] += v; }
+            if (K == 14) { m[i] = __shfl_down_sync(0xffffffffu, m[i], 1) + 1u; }
+            if (K == 15) { uint32_t v; asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(sbase + ((m[i] & 255u) << 2))); m[i] = __shfl_down_sync(0xffffffffu, m[i], 1) + v; }
         }
     }
     long long t1 = clock64();
@@ -72,5 +79,8 @@ int main() {
     run<10>("FSETP + SEL", 2);
     run<11>("FADD", 1);
     run<12>("SHF funnel", 1);
+    run<13>("LDS (+IADD)", 2);
+    run<14>("SHFL (+IADD)", 2);
+    run<15>("LDS + SHFL (+IADD)", 3);
     return 0;
 }
