@@ -396,25 +396,6 @@ static eg_status grid_graph(eg_ctx *c, const Problem &P, SlabState &S, bool raw)
     CK(S.n_unique.ensure(sizeof(int32_t) * std::max<int64_t>(ns, 1)));
     const size_t sb = scan_scratch_bytes(std::max<int64_t>(ns, 1));
     CK(c->scratch.ensure(sb));
-    if (P.grid)
-        CK(launch_saddle_beta_grid(c->host_tab, P.ndim, S.F, S.saddles32.as<int32_t>(), ns,
-                                   S.sbeta.as<int32_t>(), c->stream));
-    else
-        CK(launch_gather_beta(S.beta8.as<uint8_t>(), S.s.v0, S.saddles32.as<int32_t>(), ns, S.sbeta.as<int32_t>(),
-                              c->stream));
-    CK(launch_scan_i32(S.sbeta.as<int32_t>(), S.slot_off.as<int64_t>(), ns, c->scratch.p, sb, c->stream));
-    c->stats.kernel_launches += 2;
-    CK(cudaMemcpyAsync(hc, S.slot_off.as<int64_t>() + ns, sizeof(int64_t), cudaMemcpyDeviceToHost, c->stream));
-    CK(cudaStreamSynchronize(c->stream));
-    const int64_t nraw = hc[0];
-    S.n_raw = nraw;
-    CK(S.tmp_m.ensure(sizeof(int32_t) * std::max<int64_t>(nraw, 1)));
-    CK(S.tmp_mult.ensure(sizeof(int32_t) * std::max<int64_t>(nraw, 1)));
-    if (raw) {
-        CK(S.raw_s.ensure(sizeof(int64_t) * std::max<int64_t>(nraw, 1)));
-        CK(S.raw_rep.ensure(sizeof(int64_t) * std::max<int64_t>(nraw, 1)));
-        CK(S.raw_m.ensure(sizeof(int64_t) * std::max<int64_t>(nraw, 1)));
-    }
     LabelView lv{};
     if (P.grid) {
         lv.own = S.label;
@@ -423,18 +404,56 @@ static eg_status grid_graph(eg_ctx *c, const Problem &P, SlabState &S, bool raw)
         lv.lo = S.has_lo ? S.hval_lo.as<int32_t>() : nullptr;
         lv.hi = S.has_hi ? S.hval_hi.as<int32_t>() : nullptr;
         lv.plane = S.s.plane;
-        CK(launch_arcs_grid(c->host_tab, P.ndim, S.F, S.saddles32.as<int32_t>(), ns,
-                            S.slot_off.as<int64_t>(), lv, S.tmp_m.as<int32_t>(), S.tmp_mult.as<int32_t>(),
-                            S.n_unique.as<int32_t>(), raw ? S.raw_s.as<int64_t>() : nullptr,
-                            raw ? S.raw_rep.as<int64_t>() : nullptr, raw ? S.raw_m.as<int64_t>() : nullptr, c->stream));
     } else {
         lv.own = c->label_all.as<int32_t>();     // CSR: labels of every vertex
         lv.v0 = 0;
         lv.v1 = P.N;
-        CK(launch_arcs_csr(P.row_ptr, P.col_idx, S.F.own, S.saddles32.as<int32_t>(), ns, S.slot_off.as<int64_t>(),
-                           lv, S.tmp_m.as<int32_t>(), S.tmp_mult.as<int32_t>(), S.n_unique.as<int32_t>(),
-                           raw ? S.raw_s.as<int64_t>() : nullptr, raw ? S.raw_rep.as<int64_t>() : nullptr,
-                           raw ? S.raw_m.as<int64_t>() : nullptr, c->stream));
+    }
+    // grids without raw arcs: one pass computes beta0+ and the arcs into fixed
+    // slots of link size per saddle (no beta0+ pass, scan or sync before it)
+    const bool fused = P.grid && !raw;
+    const int stride = fused ? grid_link_size(P.ndim) : 0;
+    if (fused) {
+        S.n_raw = 0;
+        CK(S.tmp_m.ensure(sizeof(int32_t) * std::max<int64_t>(ns * stride, 1)));
+        CK(S.tmp_mult.ensure(sizeof(int32_t) * std::max<int64_t>(ns * stride, 1)));
+        CK(launch_arcs_grid(c->host_tab, P.ndim, S.F, S.saddles32.as<int32_t>(), ns, nullptr, lv,
+                            S.tmp_m.as<int32_t>(), S.tmp_mult.as<int32_t>(), S.n_unique.as<int32_t>(), nullptr,
+                            nullptr, nullptr, c->stream, S.sbeta.as<int32_t>()));
+        c->stats.kernel_launches += 1;
+    } else {
+        if (P.grid)
+            CK(launch_saddle_beta_grid(c->host_tab, P.ndim, S.F, S.saddles32.as<int32_t>(), ns,
+                                       S.sbeta.as<int32_t>(), c->stream));
+        else
+            CK(launch_gather_beta(S.beta8.as<uint8_t>(), S.s.v0, S.saddles32.as<int32_t>(), ns,
+                                  S.sbeta.as<int32_t>(), c->stream));
+        CK(launch_scan_i32(S.sbeta.as<int32_t>(), S.slot_off.as<int64_t>(), ns, c->scratch.p, sb, c->stream));
+        c->stats.kernel_launches += 2;
+        CK(cudaMemcpyAsync(hc, S.slot_off.as<int64_t>() + ns, sizeof(int64_t), cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        const int64_t nraw = hc[0];
+        S.n_raw = nraw;
+        CK(S.tmp_m.ensure(sizeof(int32_t) * std::max<int64_t>(nraw, 1)));
+        CK(S.tmp_mult.ensure(sizeof(int32_t) * std::max<int64_t>(nraw, 1)));
+        if (raw) {
+            CK(S.raw_s.ensure(sizeof(int64_t) * std::max<int64_t>(nraw, 1)));
+            CK(S.raw_rep.ensure(sizeof(int64_t) * std::max<int64_t>(nraw, 1)));
+            CK(S.raw_m.ensure(sizeof(int64_t) * std::max<int64_t>(nraw, 1)));
+        }
+        if (P.grid)
+            CK(launch_arcs_grid(c->host_tab, P.ndim, S.F, S.saddles32.as<int32_t>(), ns,
+                                S.slot_off.as<int64_t>(), lv, S.tmp_m.as<int32_t>(), S.tmp_mult.as<int32_t>(),
+                                S.n_unique.as<int32_t>(), raw ? S.raw_s.as<int64_t>() : nullptr,
+                                raw ? S.raw_rep.as<int64_t>() : nullptr, raw ? S.raw_m.as<int64_t>() : nullptr,
+                                c->stream));
+        else
+            CK(launch_arcs_csr(P.row_ptr, P.col_idx, S.F.own, S.saddles32.as<int32_t>(), ns,
+                               S.slot_off.as<int64_t>(), lv, S.tmp_m.as<int32_t>(), S.tmp_mult.as<int32_t>(),
+                               S.n_unique.as<int32_t>(), raw ? S.raw_s.as<int64_t>() : nullptr,
+                               raw ? S.raw_rep.as<int64_t>() : nullptr, raw ? S.raw_m.as<int64_t>() : nullptr,
+                               c->stream));
+        c->stats.kernel_launches += 1;
     }
     CK(launch_scan_i32(S.n_unique.as<int32_t>(), S.arc_off.as<int64_t>(), ns, c->scratch.p, sb, c->stream));
     c->stats.kernel_launches += 2;
@@ -444,9 +463,9 @@ static eg_status grid_graph(eg_ctx *c, const Problem &P, SlabState &S, bool raw)
     CK(S.arc_s.ensure(sizeof(int64_t) * std::max<int64_t>(S.n_arc, 1)));
     CK(S.arc_m.ensure(sizeof(int64_t) * std::max<int64_t>(S.n_arc, 1)));
     CK(S.arc_mult.ensure(sizeof(int32_t) * std::max<int64_t>(S.n_arc, 1)));
-    CK(launch_emit_arcs(S.saddles32.as<int32_t>(), ns, S.slot_off.as<int64_t>(), S.arc_off.as<int64_t>(),
+    CK(launch_emit_arcs(S.saddles32.as<int32_t>(), ns, fused ? nullptr : S.slot_off.as<int64_t>(), S.arc_off.as<int64_t>(),
                         S.tmp_m.as<int32_t>(), S.tmp_mult.as<int32_t>(), S.n_unique.as<int32_t>(),
-                        S.arc_s.as<int64_t>(), S.arc_m.as<int64_t>(), S.arc_mult.as<int32_t>(), c->stream));
+                        S.arc_s.as<int64_t>(), S.arc_m.as<int64_t>(), S.arc_mult.as<int32_t>(), c->stream, stride));
     c->stats.kernel_launches += 1;
     return EG_OK;
 }

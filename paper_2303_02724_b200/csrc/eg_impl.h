@@ -105,9 +105,14 @@ cudaError_t launch_emit_counted(const uint32_t *bits, int64_t n, int64_t v0, con
 // S4 for grids and CSR.
 cudaError_t launch_saddle_beta_grid(const LinkTable &tab, int ndim, FieldView F, const int32_t *saddles,
                                     int64_t n_sad, int32_t *beta, cudaStream_t st);
+// slot_off == null: fixed slots of link size K per saddle (no beta0+ pass
+// needed first) and beta0+ written to beta_out
 cudaError_t launch_arcs_grid(const LinkTable &tab, int ndim, FieldView F, const int32_t *saddles, int64_t n_sad,
                              const int64_t *slot_off, LabelView lv, int32_t *tmp_m, int32_t *tmp_mult,
-                             int32_t *n_unique, int64_t *raw_s, int64_t *raw_rep, int64_t *raw_m, cudaStream_t st);
+                             int32_t *n_unique, int64_t *raw_s, int64_t *raw_rep, int64_t *raw_m, cudaStream_t st,
+                             int32_t *beta_out = nullptr);
+// link size 2 (2^n - 1): the fixed slot stride of launch_arcs_grid without slot_off
+inline int grid_link_size(int ndim) { return 2 * ((1 << ndim) - 1); }
 // beta0+ of the saddles from a per-vertex beta0+ array written by classify
 cudaError_t launch_gather_beta(const uint8_t *beta8, int64_t v0, const int32_t *saddles, int64_t n, int32_t *out,
                                cudaStream_t st);
@@ -118,7 +123,8 @@ cudaError_t launch_arcs_csr(const int64_t *row_ptr, const int32_t *col_idx, cons
                             int32_t *n_unique, int64_t *raw_s, int64_t *raw_rep, int64_t *raw_m, cudaStream_t st);
 cudaError_t launch_emit_arcs(const int32_t *saddles, int64_t n_sad, const int64_t *slot_off, const int64_t *arc_off,
                              const int32_t *tmp_m, const int32_t *tmp_mult, const int32_t *n_unique,
-                             int64_t *arc_s, int64_t *arc_m, int32_t *arc_mult, cudaStream_t st);
+                             int64_t *arc_s, int64_t *arc_m, int32_t *arc_mult, cudaStream_t st,
+                             int slot_stride = 0);   // slot_off == null: saddle j's slots start at j * slot_stride
 
 // exclusive scan of int32 counts into int64 offsets (offsets[n] = total)
 size_t scan_scratch_bytes(int64_t n);

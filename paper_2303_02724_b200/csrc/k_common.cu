@@ -195,12 +195,12 @@ cudaError_t launch_count_bits(const uint32_t *bits, int64_t n, void *scratch, in
 
 // ------------------------------------------------------------ arc emission
 __global__ void k_emit_arcs(const int32_t *__restrict__ saddles, int64_t n_sad, const int64_t *__restrict__ slot_off,
-                            const int64_t *__restrict__ arc_off, const int32_t *__restrict__ tmp_m,
+                            int slot_stride, const int64_t *__restrict__ arc_off, const int32_t *__restrict__ tmp_m,
                             const int32_t *__restrict__ tmp_mult, const int32_t *__restrict__ n_unique,
                             int64_t *arc_s, int64_t *arc_m, int32_t *arc_mult) {
     const int64_t j = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (j >= n_sad) return;
-    const int64_t so = slot_off[j], ao = arc_off[j];
+    const int64_t so = slot_off ? slot_off[j] : j * slot_stride, ao = arc_off[j];
     const int u = n_unique[j];
     const int64_t s = saddles[j];
     for (int k = 0; k < u; ++k) {
@@ -212,10 +212,10 @@ __global__ void k_emit_arcs(const int32_t *__restrict__ saddles, int64_t n_sad, 
 
 cudaError_t launch_emit_arcs(const int32_t *saddles, int64_t n_sad, const int64_t *slot_off, const int64_t *arc_off,
                              const int32_t *tmp_m, const int32_t *tmp_mult, const int32_t *n_unique,
-                             int64_t *arc_s, int64_t *arc_m, int32_t *arc_mult, cudaStream_t st) {
+                             int64_t *arc_s, int64_t *arc_m, int32_t *arc_mult, cudaStream_t st, int slot_stride) {
     if (n_sad <= 0) return cudaSuccess;
-    k_emit_arcs<<<blocks_for(n_sad, 256), 256, 0, st>>>(saddles, n_sad, slot_off, arc_off, tmp_m, tmp_mult, n_unique,
-                                                        arc_s, arc_m, arc_mult);
+    k_emit_arcs<<<blocks_for(n_sad, 256), 256, 0, st>>>(saddles, n_sad, slot_off, slot_stride, arc_off, tmp_m,
+                                                        tmp_mult, n_unique, arc_s, arc_m, arc_mult);
     return cudaGetLastError();
 }
 

@@ -330,7 +330,8 @@ __global__ void __launch_bounds__(128) k_arcs_grid(const __grid_constant__ GridC
                                                    const int32_t *__restrict__ saddles, int64_t n_sad,
                                                    const int64_t *__restrict__ slot_off, LabelView lv,
                                                    int32_t *tmp_m, int32_t *tmp_mult, int32_t *n_unique,
-                                                   int64_t *raw_s, int64_t *raw_rep, int64_t *raw_m) {
+                                                   int64_t *raw_s, int64_t *raw_rep, int64_t *raw_m,
+                                                   int32_t *beta_out) {
     const int64_t j = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (j >= n_sad) return;
     constexpr int K = 2 * ((1 << NDIM) - 1);
@@ -342,7 +343,8 @@ __global__ void __launch_bounds__(128) k_arcs_grid(const __grid_constant__ GridC
     upper_link<NDIM, false>(S, F, v, fv, up, un, &best);
     const int b = components<NDIM>(S, up, un, F, v, reps);
     sort_reps(reps, b);
-    const int64_t off = slot_off[j];
+    if (beta_out) beta_out[j] = b;
+    const int64_t off = slot_off ? slot_off[j] : j * K;
     int32_t ms[K];
     for (int c = 0; c < b; ++c) {
         ms[c] = lv.at(reps[c]);
@@ -397,11 +399,12 @@ cudaError_t launch_saddle_beta_grid(const LinkTable &tab, int ndim, FieldView F,
 
 cudaError_t launch_arcs_grid(const LinkTable &tab, int ndim, FieldView F, const int32_t *saddles, int64_t n_sad,
                              const int64_t *slot_off, LabelView lv, int32_t *tmp_m, int32_t *tmp_mult,
-                             int32_t *n_unique, int64_t *raw_s, int64_t *raw_rep, int64_t *raw_m, cudaStream_t st) {
+                             int32_t *n_unique, int64_t *raw_s, int64_t *raw_rep, int64_t *raw_m, cudaStream_t st,
+                             int32_t *beta_out) {
     if (n_sad <= 0) return cudaSuccess;
 #define CALL(D)                                                                                              \
     k_arcs_grid<D><<<blocks_for(n_sad, 128), 128, 0, st>>>(make_grid_const<D>(tab), F, saddles, n_sad, slot_off, lv, tmp_m, \
-                                                           tmp_mult, n_unique, raw_s, raw_rep, raw_m)
+                                                           tmp_mult, n_unique, raw_s, raw_rep, raw_m, beta_out)
     EG_DISPATCH_NDIM(ndim, CALL)
 #undef CALL
     return cudaGetLastError();

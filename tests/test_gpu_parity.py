@@ -283,9 +283,10 @@ def test_virtual_slabs_invalid(eg, ctx):
 
 @pytest.mark.parametrize("env", [{"EG_LIST_DIV": "100000"},                       # maxima/saddle lists regrow + rerun
                                  {"EG_ELIST": "1"},                               # one slab with the exit list + resolve
+                                 {"EG_ELIST": "0"},                               # one slab, no list: finalize chases
                                  {"EG_ELIST": "1", "EG_ELIST_DIV": "100000"}])    # exit list overflow -> per-vertex chase
 def test_tiled_capacity_paths(eg, env, monkeypatch):
-    """The tiled path's fallbacks (list growth, exit list, exit-list overflow) stay bit-exact."""
+    """The tiled path's variants (list growth, exit list or finalize chase, exit-list overflow) stay bit-exact."""
     import torch
     for k, v in env.items():
         monkeypatch.setenv(k, v)
