@@ -122,6 +122,11 @@ struct eg_ctx {
     eg_stats stats{};
     cudaEvent_t ev[8] = {};
     cudaEvent_t ev_main[2] = {};       // around the main per-vertex kernel(s) of one slab
+    // one GPU, one slab: the node lists go to the host on a copy stream while
+    // the arcs are computed (ev_d2h[0]: lists ready, [1]: beta ready, [2]: copies done)
+    cudaStream_t d2h = nullptr;
+    cudaEvent_t ev_d2h[3] = {};
+    bool early_d2h = false;            // set per compute: the node-list copies are already queued
 };
 
 static eg_status set_err(eg_ctx *c, eg_status s, const char *fmt, ...) {
@@ -346,7 +351,7 @@ static eg_status generic_local(eg_ctx *c, const Problem &P, SlabState &S, bool m
     return EG_OK;
 }
 
-static eg_status grid_graph(eg_ctx *c, const Problem &P, SlabState &S, bool raw) {
+static eg_status grid_graph(eg_ctx *c, const Problem &P, SlabState &S, bool raw, bool early) {
     const int64_t n = S.s.v1 - S.s.v0;
     int64_t *cnt = c->counts.as<int64_t>();
     CK(c->h_counts.ensure(sizeof(int64_t) * 8));
@@ -388,6 +393,18 @@ static eg_status grid_graph(eg_ctx *c, const Problem &P, SlabState &S, bool raw)
     }
     const int64_t ns = S.n_sad;
     CK(cudaEventRecord(c->ev[3], c->stream));
+    if (early) {
+        // the node lists are final: copy them while the arcs are computed
+        CK(c->h_maxima.ensure(sizeof(int64_t) * std::max<int64_t>(S.n_max, 1)));
+        CK(c->h_saddles.ensure(sizeof(int64_t) * std::max<int64_t>(ns, 1)));
+        CK(c->h_sbeta.ensure(sizeof(int32_t) * std::max<int64_t>(ns, 1)));
+        CK(cudaEventRecord(c->ev_d2h[0], c->stream));
+        CK(cudaStreamWaitEvent(c->d2h, c->ev_d2h[0], 0));
+        if (S.n_max)
+            CK(cudaMemcpyAsync(c->h_maxima.p, S.maxima64.p, sizeof(int64_t) * S.n_max, cudaMemcpyDeviceToHost, c->d2h));
+        if (ns)
+            CK(cudaMemcpyAsync(c->h_saddles.p, S.saddles64.p, sizeof(int64_t) * ns, cudaMemcpyDeviceToHost, c->d2h));
+    }
 
     // beta0+ per saddle and slot offsets (sum beta0+ = raw arcs)
     CK(S.sbeta.ensure(sizeof(int32_t) * std::max<int64_t>(ns, 1)));
@@ -421,6 +438,12 @@ static eg_status grid_graph(eg_ctx *c, const Problem &P, SlabState &S, bool raw)
                             S.tmp_m.as<int32_t>(), S.tmp_mult.as<int32_t>(), S.n_unique.as<int32_t>(), nullptr,
                             nullptr, nullptr, c->stream, S.sbeta.as<int32_t>()));
         c->stats.kernel_launches += 1;
+        if (early) {
+            CK(cudaEventRecord(c->ev_d2h[1], c->stream));
+            CK(cudaStreamWaitEvent(c->d2h, c->ev_d2h[1], 0));
+            if (ns)
+                CK(cudaMemcpyAsync(c->h_sbeta.p, S.sbeta.p, sizeof(int32_t) * ns, cudaMemcpyDeviceToHost, c->d2h));
+        }
     } else {
         if (P.grid)
             CK(launch_saddle_beta_grid(c->host_tab, P.ndim, S.F, S.saddles32.as<int32_t>(), ns,
@@ -521,10 +544,10 @@ static eg_status gather_graph(eg_ctx *c, bool raw) {
     if (c->world == 1) {
         int64_t om = 0, os = 0, oa = 0;
         for (SlabState *S : c->slabs) {
-            if (S->n_max)
+            if (S->n_max && !c->early_d2h)
                 CK(cudaMemcpyAsync(c->h_maxima.as<int64_t>() + om, S->maxima64.p, sizeof(int64_t) * S->n_max,
                                    cudaMemcpyDeviceToHost, st));
-            if (S->n_sad) {
+            if (S->n_sad && !c->early_d2h) {
                 CK(cudaMemcpyAsync(c->h_saddles.as<int64_t>() + os, S->saddles64.p, sizeof(int64_t) * S->n_sad,
                                    cudaMemcpyDeviceToHost, st));
                 CK(cudaMemcpyAsync(c->h_sbeta.as<int32_t>() + os, S->sbeta.p, sizeof(int32_t) * S->n_sad,
@@ -542,6 +565,7 @@ static eg_status gather_graph(eg_ctx *c, bool raw) {
             os += S->n_sad;
             oa += S->n_arc;
         }
+        if (c->early_d2h) CK(cudaStreamWaitEvent(st, c->ev_d2h[2], 0));   // the node lists' copies
     } else {
         // padded all-gather of 6 arrays through one staging buffer, 8-byte slots
         SlabState &S = *c->slabs[0];
@@ -758,7 +782,10 @@ static eg_status compute_grid(eg_ctx *c, const Problem &P, const float *f, uint3
     c->n_own = nlab;
     c->have_labels = true;
     const bool raw = (flags & EG_RAW_ARCS) != 0;
-    for (SlabState *S : c->slabs) ST(grid_graph(c, P, *S, raw));
+    // one GPU, one slab, graph wanted: the node lists are copied early
+    c->early_d2h = c->world == 1 && c->slabs.size() == 1 && !raw && !(flags & EG_NO_GRAPH_D2H);
+    for (SlabState *S : c->slabs) ST(grid_graph(c, P, *S, raw, c->early_d2h));
+    if (c->early_d2h) CK(cudaEventRecord(c->ev_d2h[2], c->d2h));
     CK(cudaEventRecord(c->ev[4], c->stream));
     c->raw_valid = raw;
     return EG_OK;
@@ -861,7 +888,8 @@ static eg_status compute_csr(eg_ctx *c, const Problem &P, const float *f, uint32
     c->n_own = (c->world > 1) ? P.v1 - P.v0 : P.N;
     c->have_labels = true;
     const bool raw = (flags & EG_RAW_ARCS) != 0;
-    for (SlabState *S : c->slabs) ST(grid_graph(c, P, *S, raw));
+    c->early_d2h = false;
+    for (SlabState *S : c->slabs) ST(grid_graph(c, P, *S, raw, false));
     CK(cudaEventRecord(c->ev[4], c->stream));
     c->raw_valid = raw;
     return EG_OK;
@@ -872,6 +900,7 @@ static eg_status compute_impl(eg_ctx *c, const eg_domain *d, const float *f, uin
     if (c->poisoned)
         return set_err(c, EG_ERR_STATE, "context is poisoned by an earlier CUDA/NCCL error: %s", c->err.c_str());
     c->have_graph = c->have_labels = c->graph_on_host = false;
+    if (c->d2h) CK(cudaStreamSynchronize(c->d2h));   // no copy of an earlier call still in flight
     Problem P;
     ST(validate(c, d, f, device_field, &P));
     CK(cudaSetDevice(c->device));
@@ -933,6 +962,15 @@ eg_status eg_create(eg_ctx **out, int cuda_device, void *cuda_stream) {
             delete c;
             return EG_ERR_CUDA;
         }
+    for (auto &e : c->ev_d2h)
+        if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) {
+            delete c;
+            return EG_ERR_CUDA;
+        }
+    if (cudaStreamCreateWithFlags(&c->d2h, cudaStreamNonBlocking) != cudaSuccess) {
+        delete c;
+        return EG_ERR_CUDA;
+    }
     *out = c;
     return EG_OK;
 }
@@ -1096,6 +1134,12 @@ eg_status eg_destroy(eg_ctx *c) {
     for (auto &e : c->ev)
         if (e) cudaEventDestroy(e);
     for (auto &e : c->ev_main)
+        if (e) cudaEventDestroy(e);
+    if (c->d2h) {
+        cudaStreamSynchronize(c->d2h);
+        cudaStreamDestroy(c->d2h);
+    }
+    for (auto &e : c->ev_d2h)
         if (e) cudaEventDestroy(e);
     if (c->comm) ncclCommDestroy(c->comm);
     delete c;
