@@ -77,6 +77,7 @@ struct SlabState {
     DevBuf f_lo, f_hi;                 // halo planes of f received from the neighbours
     DevBuf sad_bits, max_bits;
     DevBuf beta8;                      // CSR: beta0+ per owned vertex (from classify)
+    DevBuf rep_buf;                    // CSR: the saddles' component representatives, by row_ptr
     DevBuf bval, hval_lo, hval_hi;     // boundary-plane label values (own / neighbours')
     bool has_lo = false, has_hi = false;
     Tiled3D *tiled = nullptr;
@@ -85,7 +86,7 @@ struct SlabState {
     DevBuf arc_s, arc_m, arc_mult, raw_s, raw_rep, raw_m;
     int64_t n_max = 0, n_sad = 0, n_arc = 0, n_raw = 0;
     ~SlabState() {
-        DevBuf *b[] = {&f_lo, &f_hi, &sad_bits, &max_bits, &beta8, &bval, &hval_lo, &hval_hi, &maxima64,
+        DevBuf *b[] = {&f_lo, &f_hi, &sad_bits, &max_bits, &beta8, &rep_buf, &bval, &hval_lo, &hval_hi, &maxima64,
                        &saddles32, &saddles64, &sbeta, &slot_off, &tmp_m, &tmp_mult, &n_unique, &arc_off, &arc_s,
                        &arc_m, &arc_mult, &raw_s, &raw_rep, &raw_m};
         for (DevBuf *x : b) x->release();
@@ -470,12 +471,12 @@ static eg_status grid_graph(eg_ctx *c, const Problem &P, SlabState &S, bool raw,
                                 S.n_unique.as<int32_t>(), raw ? S.raw_s.as<int64_t>() : nullptr,
                                 raw ? S.raw_rep.as<int64_t>() : nullptr, raw ? S.raw_m.as<int64_t>() : nullptr,
                                 c->stream));
-        else
-            CK(launch_arcs_csr(P.row_ptr, P.col_idx, S.F.own, S.saddles32.as<int32_t>(), ns,
-                               S.slot_off.as<int64_t>(), lv, S.tmp_m.as<int32_t>(), S.tmp_mult.as<int32_t>(),
-                               S.n_unique.as<int32_t>(), raw ? S.raw_s.as<int64_t>() : nullptr,
-                               raw ? S.raw_rep.as<int64_t>() : nullptr, raw ? S.raw_m.as<int64_t>() : nullptr,
-                               c->stream));
+        else   // the representatives were stored by classify: no second link computation
+            CK(launch_arcs_csr_reps(P.row_ptr, S.rep_buf.as<int32_t>(), S.saddles32.as<int32_t>(),
+                                    S.sbeta.as<int32_t>(), ns, S.slot_off.as<int64_t>(), lv, S.tmp_m.as<int32_t>(),
+                                    S.tmp_mult.as<int32_t>(), S.n_unique.as<int32_t>(),
+                                    raw ? S.raw_s.as<int64_t>() : nullptr, raw ? S.raw_rep.as<int64_t>() : nullptr,
+                                    raw ? S.raw_m.as<int64_t>() : nullptr, c->stream));
         c->stats.kernel_launches += 1;
     }
     CK(launch_scan_i32(S.n_unique.as<int32_t>(), S.arc_off.as<int64_t>(), ns, c->scratch.p, sb, c->stream));
@@ -824,6 +825,7 @@ static eg_status compute_csr(eg_ctx *c, const Problem &P, const float *f, uint32
         CK(S.max_bits.ensure(sizeof(uint32_t) * std::max<int64_t>(words, 1)));
         S.tiled_lists = false;
         CK(S.beta8.ensure(std::max<int64_t>(S.s.v1 - S.s.v0, 1)));
+        CK(S.rep_buf.ensure(sizeof(int32_t) * std::max<int64_t>(P.nnz, 1)));
         S.has_lo = S.has_hi = false;
     }
     CK(cudaEventRecord(c->ev[0], c->stream));
@@ -837,7 +839,8 @@ static eg_status compute_csr(eg_ctx *c, const Problem &P, const float *f, uint32
         const bool first = S == c->slabs[0];
         if (first) CK(cudaEventRecord(c->ev_main[0], c->stream));
         CK(launch_classify_csr(P.row_ptr, P.col_idx, f, S->s.v0, S->s.v1, S->label, S->sad_bits.as<uint32_t>(),
-                               S->max_bits.as<uint32_t>(), S->beta8.as<uint8_t>(), fl, fl + 1, c->stream));
+                               S->max_bits.as<uint32_t>(), S->beta8.as<uint8_t>(), fl, fl + 1, c->stream,
+                               S->rep_buf.as<int32_t>()));
         if (first) CK(cudaEventRecord(c->ev_main[1], c->stream));
         c->stats.kernel_launches += 1;
     }

@@ -86,7 +86,8 @@ cudaError_t launch_classify_grid(const LinkTable &tab, int ndim, FieldView F, co
                                  cudaStream_t st);
 cudaError_t launch_classify_csr(const int64_t *row_ptr, const int32_t *col_idx, const float *f, int64_t v0,
                                 int64_t v1, int32_t *ptr, uint32_t *sad_bits, uint32_t *max_bits,
-                                uint8_t *beta_out, int *nan_flag, int *deg_overflow, cudaStream_t st);
+                                uint8_t *beta_out, int *nan_flag, int *deg_overflow, cudaStream_t st,
+                                int32_t *rep_buf = nullptr);   // saddles' component reps at rep_buf[row_ptr[v] ..]
 
 // S2: in-place pointer jumping over ptr[0..n) whose entries are global ids;
 // entries outside [v0, v0 + n) are terminal (remote).  changed[r] is set when
@@ -116,11 +117,11 @@ inline int grid_link_size(int ndim) { return 2 * ((1 << ndim) - 1); }
 // beta0+ of the saddles from a per-vertex beta0+ array written by classify
 cudaError_t launch_gather_beta(const uint8_t *beta8, int64_t v0, const int32_t *saddles, int64_t n, int32_t *out,
                                cudaStream_t st);
-cudaError_t launch_saddle_beta_csr(const int64_t *row_ptr, const int32_t *col_idx, const float *f,
-                                   const int32_t *saddles, int64_t n_sad, int32_t *beta, cudaStream_t st);
-cudaError_t launch_arcs_csr(const int64_t *row_ptr, const int32_t *col_idx, const float *f, const int32_t *saddles,
-                            int64_t n_sad, const int64_t *slot_off, LabelView lv, int32_t *tmp_m, int32_t *tmp_mult,
-                            int32_t *n_unique, int64_t *raw_s, int64_t *raw_rep, int64_t *raw_m, cudaStream_t st);
+// S4 on CSR from the representatives classify stored in rep_buf
+cudaError_t launch_arcs_csr_reps(const int64_t *row_ptr, const int32_t *rep_buf, const int32_t *saddles,
+                                 const int32_t *sbeta, int64_t n_sad, const int64_t *slot_off, LabelView lv,
+                                 int32_t *tmp_m, int32_t *tmp_mult, int32_t *n_unique, int64_t *raw_s,
+                                 int64_t *raw_rep, int64_t *raw_m, cudaStream_t st);
 cudaError_t launch_emit_arcs(const int32_t *saddles, int64_t n_sad, const int64_t *slot_off, const int64_t *arc_off,
                              const int32_t *tmp_m, const int32_t *tmp_mult, const int32_t *n_unique,
                              int64_t *arc_s, int64_t *arc_m, int32_t *arc_mult, cudaStream_t st,
