@@ -456,6 +456,8 @@ static eg_status grid_graph(eg_ctx *c, const Problem &P, SlabState &S, bool raw,
         c->stats.kernel_launches += 2;
         CK(cudaMemcpyAsync(hc, S.slot_off.as<int64_t>() + ns, sizeof(int64_t), cudaMemcpyDeviceToHost, c->stream));
         CK(cudaStreamSynchronize(c->stream));
+        if (early && ns)   // beta0+ is final (the stream was just synchronised)
+            CK(cudaMemcpyAsync(c->h_sbeta.p, S.sbeta.p, sizeof(int32_t) * ns, cudaMemcpyDeviceToHost, c->d2h));
         const int64_t nraw = hc[0];
         S.n_raw = nraw;
         CK(S.tmp_m.ensure(sizeof(int32_t) * std::max<int64_t>(nraw, 1)));
@@ -891,8 +893,9 @@ static eg_status compute_csr(eg_ctx *c, const Problem &P, const float *f, uint32
     c->n_own = (c->world > 1) ? P.v1 - P.v0 : P.N;
     c->have_labels = true;
     const bool raw = (flags & EG_RAW_ARCS) != 0;
-    c->early_d2h = false;
-    for (SlabState *S : c->slabs) ST(grid_graph(c, P, *S, raw, false));
+    c->early_d2h = c->world == 1 && c->slabs.size() == 1 && !raw && !(flags & EG_NO_GRAPH_D2H);
+    for (SlabState *S : c->slabs) ST(grid_graph(c, P, *S, raw, c->early_d2h));
+    if (c->early_d2h) CK(cudaEventRecord(c->ev_d2h[2], c->d2h));
     CK(cudaEventRecord(c->ev[4], c->stream));
     c->raw_valid = raw;
     return EG_OK;
