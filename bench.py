@@ -36,6 +36,9 @@ CONFIGS = {
     "C4": dict(desc="C4 5D 32^5 Schwefel f32", kind="grid"),
     "C5": dict(desc="C5 1M x 10D GMM kNN(k=16) CSR f32", kind="csr"),
 }
+# the paper's resolution sweep, Schwefel 3-D resampled 128^3 .. 1024^3
+for _n in (128, 256, 512, 1024):
+    CONFIGS[f"F1-{_n}"] = dict(desc=f"F1 3D {_n}^3 Schwefel f32 (resolution sweep)", kind="grid")
 
 
 def make_input(cfg: str, device: str):
@@ -54,6 +57,10 @@ def make_input(cfg: str, device: str):
     if cfg == "C4":
         f, dims = G.schwefel()
         return torch.from_numpy(f).to(device), dims, None
+    if cfg.startswith("F1-"):
+        n = int(cfg[3:])
+        f, dims = G.schwefel((n, n, n), device=device)
+        return f, dims, None
     if cfg == "C5":
         X, f = G.gmm_points(1_000_000, seed=10)
         rp, ci = G.knn_csr(X, 16, device=device)

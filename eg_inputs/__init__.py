@@ -148,16 +148,30 @@ def turbulence(n: int = 1024, seed: int = 1024, device: str = "cpu", kc_div: int
 # ---------------------------------------------------------------------- C4
 
 
-def schwefel(dims=(32,) * 5, lo: float = -500.0, hi: float = 500.0):
+def schwefel_profile(D: int, lo: float = -500.0, hi: float = 500.0) -> np.ndarray:
+    """The 1-D Schwefel term t(x) = x sin(sqrt|x|) at x = lo + k (hi - lo) / (D - 1), float64."""
+    x = lo + np.arange(D, dtype=np.float64) * (hi - lo) / (D - 1)
+    return x * np.sin(np.sqrt(np.abs(x)))
+
+
+def schwefel(dims=(32,) * 5, lo: float = -500.0, hi: float = 500.0, device=None):
     """C4: g(x) = 418.9829 n - sum_i x_i sin(sqrt|x_i|) on [lo, hi]^n,
     x = lo + k (hi - lo) / (D - 1); evaluated in float64 starting from
-    418.9829 n and subtracting the slowest axis' term first, then cast to f32."""
+    418.9829 n and subtracting the slowest axis' term first, then cast to f32.
+    device: build the field there (the 1-D terms come from numpy, the float64
+    subtractions and the rounding to f32 are IEEE-exact on either side, so the
+    bytes are the same); returns a torch tensor then."""
     n = len(dims)
-    terms = []
-    for D in dims:
-        x = lo + np.arange(D, dtype=np.float64) * (hi - lo) / (D - 1)
-        terms.append(x * np.sin(np.sqrt(np.abs(x))))
+    terms = [schwefel_profile(D, lo, hi) for D in dims]
     shape = list(reversed(dims))
+    if device is not None:
+        import torch
+        acc = torch.full(shape, 418.9829 * n, dtype=torch.float64, device=device)
+        for ax in reversed(range(n)):
+            view = [1] * n
+            view[n - 1 - ax] = dims[ax]
+            acc -= torch.from_numpy(terms[ax]).to(device).reshape(view)
+        return acc.to(torch.float32).reshape(-1).contiguous(), list(dims)
     acc = np.full(shape, 418.9829 * n, dtype=np.float64)
     for ax in reversed(range(n)):         # axis n-1 (slowest) first
         view = [1] * n

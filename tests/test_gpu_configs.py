@@ -166,3 +166,23 @@ def test_c5_config_sampled(eg, ctx):
         p, b, _ = O.csr_vertex(f, rp, ci, int(v))
         assert ptr[v] == p and beta[v] == min(b, 255)
     assert int(g.arcs[:, 2].sum()) == int(g.saddle_beta.sum())
+
+
+def test_f1_resolution_sweep(eg, ctx):
+    """the Schwefel 3-D resolution sweep.  128^3 in full against
+    the oracle; 256^3 and 512^3 against the separable product rule (the same
+    512 maxima / 1344 2-saddles at every resolution >= 128) plus sampled parity."""
+    import torch
+    src = open(__file__.replace("test_gpu_configs.py", "../tools/sweep_f1.py")).read()
+    ns = {}
+    exec(src[src.index("def product_rule"):src.index("rows = []")], {"np": np, "G": G}, ns)
+    f, dims = G.schwefel((128,) * 3)
+    o = O.grid(f, dims)
+    assert_graph_equal(ctx.compute(torch.from_numpy(f).cuda(), dims=dims), o, what="F1 128^3")
+    assert (len(o.maxima), len(o.saddles)) == ns["product_rule"](128)
+    for n in (256, 512):
+        t, dims = G.schwefel((n,) * 3, device="cuda")
+        g = ctx.compute(t, dims=dims)
+        assert (len(g.maxima), len(g.saddles)) == ns["product_rule"](n)
+        assert np.all(g.saddle_beta == 2)
+        _sampled_grid_checks(g, t.cpu().numpy(), dims, g.labels.cpu().numpy().astype(np.int64), n_lab=200, n_sad=80)
