@@ -77,7 +77,22 @@ def _L():
         _lib.ego_grid_euler.argtypes = [C.c_int, i64p, f32p, i64p]
         _lib.ego_csr_euler.argtypes = [C.c_int64, i64p, i32p, f32p, i64p]
         _lib.ego_grid_link_stats.argtypes = [C.c_int, i64p, C.c_int64, i64p, i64p, i64p]
+        _lib.ego_set_order.argtypes = [C.c_int]
     return _lib
+
+
+class reversed_order:
+    """Context manager: every oracle call inside runs under the reversed total
+    order (O10), i.e. computes the MINIMUM graph: minima, 1-saddles (beta0 of the
+    lower link >= 2) and the descending arcs / labels (reading L11)."""
+
+    def __enter__(self):
+        _L().ego_set_order(1)
+        return self
+
+    def __exit__(self, *exc):
+        _L().ego_set_order(0)
+        return False
 
 
 def _p(a, ct):
@@ -132,9 +147,13 @@ def _dims_arr(dims):
     return np.ascontiguousarray(np.asarray(dims, dtype=np.int64))
 
 
-def grid(f: np.ndarray, dims) -> Graph:
+def grid(f: np.ndarray, dims, minimum: bool = False) -> Graph:
     """Extremum graph of a float32 field on a Freudenthal grid; ``dims`` is
-    fastest axis first and ``f`` is the flat row-major array (axis 0 fastest)."""
+    fastest axis first and ``f`` is the flat row-major array (axis 0 fastest).
+    minimum=True: the minimum graph (O10)."""
+    if minimum:
+        with reversed_order():
+            return grid(f, dims)
     f = np.ascontiguousarray(np.asarray(f, dtype=np.float32).reshape(-1))
     d = _dims_arr(dims)
     res = _Result()

@@ -34,6 +34,12 @@
  *                         of m is reduced to unique (s, m) with multiplicity
  *                         (L7).  Raw (s, rep, m) triples are kept as well.
  *
+ *   O10 minimum graph  P:62, "computes both maximum and minimum graph".
+ *                         Reading L11: the minimum graph (minima, 1-saddles,
+ *                         descending arcs) is the maximum graph under the
+ *                         REVERSED total order -- O1 with u and v swapped
+ *                         (ego_set_order(1)); every other step is unchanged.
+ *
  * Parity status: every function below is pinned by tests/test_oracle_pins.py
  * (closed forms, Euler invariant, literal brute force, golden examples); the
  * CSR path on kNN graphs is pinned only by brute force on small graphs and
@@ -70,8 +76,13 @@ typedef struct {
 
 /* ---------------------------------------------------------------- O1 order */
 
+static int g_reverse = 0;   /* O10: 1 = the reversed order (minimum graph) */
+
+void ego_set_order(int reverse) { g_reverse = reverse != 0; }
+
 static int less(const float *f, int64_t u, int64_t v) {
     /* P:184 simulated perturbation, lower index = lower (L1). */
+    if (g_reverse) { const int64_t t = u; u = v; v = t; }
     return f[u] < f[v] || (f[u] == f[v] && u < v);
 }
 

@@ -535,3 +535,67 @@ def test_knn_small_sanity():
     assert int(g.arc_mult.sum()) == int(g.saddle_beta.sum())
     for v in range(0, 2000, 131):
         assert O.csr_walk(f, row_ptr, col_idx, v)[0] == g.label[v]
+
+
+# ------------------------------------------- O10: the minimum graph (L11)
+# Pinned independently of the reflection the GPU path uses: hand-derived 1-D
+# valleys, the constant field under the reversed order, the Euler identity for
+# the lower links, the separable product rule applied to minima, and the
+# literal brute force run on -f with the tie order reversed (the max graph of
+# -f under descending-index SoS is the min graph of f).
+
+def test_minimum_graph_1d_golden():
+    # [0, 5, 1, 9, 2]: minima 0, 2, 4; 1-saddles (interior maxima) 1 and 3,
+    # each with one descending arc to either side; labels follow steepest descent
+    f = np.array([0, 5, 1, 9, 2], np.float32)
+    g = O.grid(f, [5], minimum=True)
+    assert g.maxima.tolist() == [0, 2, 4]
+    assert g.saddles.tolist() == [1, 3] and g.saddle_beta.tolist() == [2, 2]
+    assert g.arcs.tolist() == [[1, 0, 1], [1, 2, 1], [3, 2, 1], [3, 4, 1]]
+    assert g.label.tolist() == [0, 0, 2, 2, 4]
+
+
+@pytest.mark.parametrize("dims", [[7], [5, 4], [4, 3, 5], [3, 3, 3, 2]])
+def test_minimum_graph_constant_field(dims):
+    # reversed SoS on a constant field: the LOWEST index is the only minimum
+    N = int(np.prod(dims))
+    g = O.grid(np.zeros(N, np.float32), dims, minimum=True)
+    assert g.maxima.tolist() == [0] and len(g.saddles) == 0
+    assert (g.label == 0).all()
+
+
+@pytest.mark.parametrize("dims,seed", [([9, 7], 0), ([5, 6, 4], 2), ([4, 3, 4, 3], 4)])
+def test_minimum_graph_euler(dims, seed):
+    # sum_v (1 - chi(Lk-(v))) = chi(box) = 1 for the reversed order too (Banchoff)
+    f, _ = G.random_field(dims, seed, "int")
+    with O.reversed_order():
+        assert O.grid_euler(f, dims) == 1
+
+
+@pytest.mark.parametrize("dims,seed", [([40, 40], 0), ([24, 24, 24], 2), ([7, 7, 7, 7, 7], 5)])
+def test_minimum_graph_product_rule(dims, seed):
+    # tie-free separable f: #minima = prod m_i, #1-saddles = sum_i s_i prod_{j != i} m_j
+    # with m_i, s_i the 1-D minima / interior maxima = the maximum rule on -h_i
+    rng = np.random.default_rng(seed)
+    profiles = [rng.standard_normal(d) for d in dims]
+    f, _ = G.separable(profiles)
+    g = O.grid(f, dims, minimum=True)
+    n_min, n_sad = _product_rule([-p for p in profiles])
+    assert (len(g.maxima), len(g.saddles)) == (n_min, n_sad)
+    assert (g.saddle_beta == 2).all()
+
+
+@pytest.mark.parametrize("dims,kind,seed", [([6, 5], "int", 1), ([4, 4, 3], "int", 2), ([5, 4, 3], "normal", 3)])
+def test_minimum_graph_brute(dims, kind, seed):
+    # brute force on the reflected, negated field: g[i] = -f[N-1-i] (point
+    # reflection maps the Freudenthal grid to itself and reverses the index
+    # order), mapped back by i -> N-1-i
+    f, _ = G.random_field(dims, seed, kind)
+    N = len(f)
+    o = O.grid(f, dims, minimum=True)
+    b = brute.grid_graph((-f[::-1]).copy(), dims)
+    rev = lambda a: sorted(N - 1 - int(x) for x in a)
+    assert o.maxima.tolist() == rev(b["maxima"])
+    assert o.saddles.tolist() == rev(b["saddles"])
+    assert o.label.tolist() == [N - 1 - int(b["label"][N - 1 - v]) for v in range(N)]
+    assert sorted(map(tuple, o.arcs.tolist())) == sorted((N - 1 - s, N - 1 - m, c) for s, m, c in b["arcs"])
