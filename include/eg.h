@@ -111,7 +111,14 @@ enum {
     EG_RAW_ARCS = 2u,         /* also keep raw (s, rep, m) per component     */
     EG_CHECK_CSR = 4u,        /* validate CSR sortedness / symmetry           */
     EG_FORCE_GENERIC = 8u,    /* grid: use the generic n-D kernels even for n <= 3 */
-    EG_NO_GRAPH_D2H = 16u     /* leave the graph on the device (eg_get_graph then fails) */
+    EG_NO_GRAPH_D2H = 16u,    /* leave the graph on the device (eg_get_graph then fails) */
+    /* The MINIMUM graph instead ("computes both maximum and
+     * minimum graph"; reading L11): minima, 1-saddles (beta0 of the lower link
+     * >= 2) and the descending arcs / labels -- the maximum graph under the
+     * reversed total order.  eg_graph's "maxima" then hold the minima, labels
+     * the minimum each descending path reaches.  Grids, one GPU, one slab
+     * (EG_ERR_UNSUPPORTED otherwise). */
+    EG_MINIMUM = 32u
 };
 /* virtual partitions: process a grid as k slabs on one GPU, exchanging
  * boundaries by device copies exactly as k ranks would (partition test). */

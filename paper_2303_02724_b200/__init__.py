@@ -19,11 +19,11 @@ import numpy as np
 import torch
 
 from . import _abi
-from ._abi import (EG_CHECK_CSR, EG_CHECK_NAN, EG_FORCE_GENERIC, EG_NO_GRAPH_D2H, EG_RAW_ARCS,  # noqa: F401
+from ._abi import (EG_CHECK_CSR, EG_CHECK_NAN, EG_FORCE_GENERIC, EG_MINIMUM, EG_NO_GRAPH_D2H, EG_RAW_ARCS,  # noqa: F401
                    EG_VIRTUAL_PARTS)
 
 __all__ = ["Context", "Graph", "EgError", "grid_domain", "csr_domain", "EG_CHECK_NAN", "EG_RAW_ARCS",
-           "EG_CHECK_CSR", "EG_FORCE_GENERIC", "EG_NO_GRAPH_D2H", "EG_VIRTUAL_PARTS"]
+           "EG_CHECK_CSR", "EG_FORCE_GENERIC", "EG_NO_GRAPH_D2H", "EG_MINIMUM", "EG_VIRTUAL_PARTS"]
 
 
 class EgError(RuntimeError):

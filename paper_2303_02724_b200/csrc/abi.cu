@@ -107,6 +107,8 @@ struct eg_ctx {
     std::vector<SlabState *> slabs;
     DevBuf label_all;                  // labels of every slab of this process
     DevBuf field;                      // eg_compute_host staging target
+    DevBuf mirror;                     // EG_MINIMUM: g[i] = -f[N-1-i]
+    bool minimum = false;              // the current compute is a minimum graph
     DevBuf flags;                      // [0] nan, [1] deg overflow, [2..] jump-changed per round
     DevBuf counts;                     // int64 / u64 counters
     DevBuf scratch;                    // compaction / scan scratch
@@ -786,7 +788,7 @@ static eg_status compute_grid(eg_ctx *c, const Problem &P, const float *f, uint3
     c->have_labels = true;
     const bool raw = (flags & EG_RAW_ARCS) != 0;
     // one GPU, one slab, graph wanted: the node lists are copied early
-    c->early_d2h = c->world == 1 && c->slabs.size() == 1 && !raw && !(flags & EG_NO_GRAPH_D2H);
+    c->early_d2h = c->world == 1 && c->slabs.size() == 1 && !raw && !(flags & EG_NO_GRAPH_D2H) && !c->minimum;
     for (SlabState *S : c->slabs) ST(grid_graph(c, P, *S, raw, c->early_d2h));
     if (c->early_d2h) CK(cudaEventRecord(c->ev_d2h[2], c->d2h));
     CK(cudaEventRecord(c->ev[4], c->stream));
@@ -915,8 +917,32 @@ static eg_status compute_impl(eg_ctx *c, const eg_domain *d, const float *f, uin
     CK(c->flags.ensure(sizeof(int) * 128));
     CK(c->counts.ensure(sizeof(int64_t) * 16 * (c->world + 1)));
     CK(cudaMemsetAsync(c->flags.p, 0, sizeof(int) * 128, c->stream));
+    // EG_MINIMUM (reading L11): the maximum graph of g[i] = -f[N-1-i], mapped
+    // back by i -> N-1-i (k_common.cu)
+    c->minimum = (flags & EG_MINIMUM) != 0;
+    if (c->minimum) {
+        if (!P.grid || c->world > 1 || ((flags >> 8) & 0xffffff) > 1 || (flags & EG_RAW_ARCS))
+            return set_err(c, EG_ERR_UNSUPPORTED, "EG_MINIMUM: grids on one GPU and one slab, without raw arcs");
+        CK(c->mirror.ensure(sizeof(float) * std::max<int64_t>(P.N, 1)));
+        CK(launch_reflect_negate(f, c->mirror.as<float>(), P.N, c->stream));
+        c->stats.kernel_launches += 1;
+        f = c->mirror.as<float>();
+    }
     if (P.grid) ST(compute_grid(c, P, f, flags));
     else ST(compute_csr(c, P, f, flags));
+    if (c->minimum) {
+        SlabState &S = *c->slabs[0];
+        const int64_t N = P.N;
+        CK(launch_reverse_i32(c->label_all.as<int32_t>(), N, N, true, c->stream));
+        CK(launch_reverse_i64(S.maxima64.as<int64_t>(), S.n_max, N, true, c->stream));
+        CK(launch_reverse_i64(S.saddles64.as<int64_t>(), S.n_sad, N, true, c->stream));
+        CK(launch_reverse_i32(S.saddles32.as<int32_t>(), S.n_sad, N, true, c->stream));
+        CK(launch_reverse_i32(S.sbeta.as<int32_t>(), S.n_sad, N, false, c->stream));
+        CK(launch_reverse_i64(S.arc_s.as<int64_t>(), S.n_arc, N, true, c->stream));
+        CK(launch_reverse_i64(S.arc_m.as<int64_t>(), S.n_arc, N, true, c->stream));
+        CK(launch_reverse_i32(S.arc_mult.as<int32_t>(), S.n_arc, N, false, c->stream));
+        c->stats.kernel_launches += 8;
+    }
     if (!(flags & EG_NO_GRAPH_D2H)) {
         ST(gather_graph(c, (flags & EG_RAW_ARCS) != 0));
         c->graph_on_host = true;
@@ -1132,7 +1158,7 @@ eg_status eg_destroy(eg_ctx *c) {
     cudaSetDevice(c->device);
     cudaStreamSynchronize(c->stream);
     set_slab_count(c, 0);
-    DevBuf *bufs[] = {&c->label_all, &c->field, &c->flags, &c->counts, &c->scratch, &c->tab, &c->gsend, &c->grecv};
+    DevBuf *bufs[] = {&c->label_all, &c->field, &c->mirror, &c->flags, &c->counts, &c->scratch, &c->tab, &c->gsend, &c->grecv};
     for (DevBuf *b : bufs) b->release();
     HostBuf *hb[] = {&c->h_maxima, &c->h_saddles, &c->h_sbeta, &c->h_arc_s, &c->h_arc_m, &c->h_arc_mult,
                      &c->h_raw_s, &c->h_raw_rep, &c->h_raw_m, &c->h_counts, &c->h_stage};

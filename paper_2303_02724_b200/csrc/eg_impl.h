@@ -127,6 +127,12 @@ cudaError_t launch_emit_arcs(const int32_t *saddles, int64_t n_sad, const int64_
                              int64_t *arc_s, int64_t *arc_m, int32_t *arc_mult, cudaStream_t st,
                              int slot_stride = 0);   // slot_off == null: saddle j's slots start at j * slot_stride
 
+// minimum graph (reading L11): g[i] = -f[n-1-i]; in-place reversal of an id
+// list (entries x -> N-1-x when map_ids) or of a plain array
+cudaError_t launch_reflect_negate(const float *f, float *g, int64_t n, cudaStream_t st);
+cudaError_t launch_reverse_i64(int64_t *a, int64_t n, int64_t N, bool map_ids, cudaStream_t st);
+cudaError_t launch_reverse_i32(int32_t *a, int64_t n, int64_t N, bool map_ids, cudaStream_t st);
+
 // exclusive scan of int32 counts into int64 offsets (offsets[n] = total)
 size_t scan_scratch_bytes(int64_t n);
 cudaError_t launch_scan_i32(const int32_t *in, int64_t *out, int64_t n, void *scratch, size_t scratch_bytes,

@@ -243,6 +243,51 @@ cudaError_t launch_i32_to_i64(const int32_t *in, int64_t *out, int64_t n, cudaSt
     return cudaGetLastError();
 }
 
+// ------------------------------------------------- minimum graph (reading L11)
+// The minimum graph of f is the maximum graph of g[i] = -f[N-1-i]: the point
+// reflection x -> dims-1-x maps the Freudenthal grid onto itself and reverses
+// the linear index, so "lower under the reversed SoS order of f" becomes
+// "lower under the SoS order of g".  Outputs map back by i -> N-1-i, which
+// reverses every sorted list.
+__global__ void k_reflect_negate(const float *__restrict__ f, float *__restrict__ g, int64_t n) {
+    for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
+        g[i] = -__ldg(f + (n - 1 - i));
+}
+
+// a[0..n) := reverse(a), each entry x mapped to N - 1 - x when map_ids
+template <class T>
+__global__ void k_reverse(T *a, int64_t n, int64_t N, bool map_ids) {
+    for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < (n + 1) / 2;
+         i += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t j = n - 1 - i;
+        T x = a[i], y = a[j];
+        if (map_ids) {
+            x = T(N - 1 - int64_t(x));
+            y = T(N - 1 - int64_t(y));
+        }
+        a[i] = y;
+        a[j] = x;
+    }
+}
+
+cudaError_t launch_reflect_negate(const float *f, float *g, int64_t n, cudaStream_t st) {
+    if (n <= 0) return cudaSuccess;
+    k_reflect_negate<<<148 * 8, 256, 0, st>>>(f, g, n);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_reverse_i64(int64_t *a, int64_t n, int64_t N, bool map_ids, cudaStream_t st) {
+    if (n <= 0) return cudaSuccess;
+    k_reverse<int64_t><<<unsigned(std::min<int64_t>((n + 511) / 512, 148 * 8)), 256, 0, st>>>(a, n, N, map_ids);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_reverse_i32(int32_t *a, int64_t n, int64_t N, bool map_ids, cudaStream_t st) {
+    if (n <= 0) return cudaSuccess;
+    k_reverse<int32_t><<<unsigned(std::min<int64_t>((n + 511) / 512, 148 * 8)), 256, 0, st>>>(a, n, N, map_ids);
+    return cudaGetLastError();
+}
+
 __global__ void k_nan_scan(const float *__restrict__ f, int64_t n, int *flag) {
     bool bad = false;
     for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)

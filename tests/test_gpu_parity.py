@@ -296,3 +296,27 @@ def test_tiled_capacity_paths(eg, env, monkeypatch):
         o = O.grid(f, dims)
         g = ctx.compute(torch.from_numpy(f).cuda(), dims=dims)
         assert_graph_equal(g, o, what=f"{env} {dims} {kind}")
+
+
+@pytest.mark.parametrize("dims,kind", [([97], "int"), ([64, 64], "normal"), ([70, 41, 37], "int"),
+                                       ([96, 64, 48], "signed_zero"), ([9, 8, 7, 6], "normal")])
+@pytest.mark.parametrize("path", PATHS)
+def test_minimum_graph(eg, ctx, dims, kind, path):
+    """EG_MINIMUM (reading L11): minima, 1-saddles, descending arcs and labels,
+    bit-exact against the oracle's reversed-order transcription (O10)."""
+    import torch
+    f, _ = G.random_field(dims, 31 + len(dims), kind)
+    o = O.grid(f, dims, minimum=True)
+    g = ctx.compute(torch.from_numpy(f).cuda(), dims=dims, flags=_flags(eg, path, eg.EG_MINIMUM | eg.EG_CHECK_NAN))
+    assert_graph_equal(g, o, what=f"minimum {dims} {kind} {path}")
+    # and the maximum graph of the same field on the same context is unaffected
+    assert_graph_equal(ctx.compute(torch.from_numpy(f).cuda(), dims=dims, flags=_flags(eg, path)), O.grid(f, dims))
+
+
+def test_minimum_graph_unsupported(eg, ctx):
+    import torch
+    f, dims = G.random_field([20, 20, 20], 3, "normal")
+    with pytest.raises(Exception):
+        ctx.compute(torch.from_numpy(f).cuda(), dims=dims, flags=eg.EG_MINIMUM | eg.EG_VIRTUAL_PARTS(2))
+    with pytest.raises(Exception):
+        ctx.compute(torch.from_numpy(f).cuda(), dims=dims, flags=eg.EG_MINIMUM | eg.EG_RAW_ARCS)
