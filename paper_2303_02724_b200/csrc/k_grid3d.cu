@@ -50,6 +50,13 @@ constexpr int kThreads = TX * TY;                    // one z-column per thread
 constexpr int kWarps = kThreads / 32;
 constexpr int kLutWords = (1 << 14) / 32;            // 1 bit per 14-bit upper mask: beta0+ >= 2
 constexpr uint32_t kFlag = 0x80000000u;              // label bit 31: exit (not yet final)
+#ifndef EG_S1_UNROLL
+#define EG_S1_UNROLL 4
+#endif
+#ifndef EG_OUT_UNROLL
+#define EG_OUT_UNROLL 4
+#endif
+constexpr int kS1Unroll = EG_S1_UNROLL, kOutUnroll = EG_OUT_UNROLL;   // z-loop unrolling (tuned on C3)
 // the halo shell of a box (the cells a path can exit to): both z faces, and
 // the y rows / x columns of the inner planes, over box x in [XO - 1, XO + TX]
 constexpr int kShellW = TX + 2;
@@ -363,7 +370,7 @@ __global__ void __launch_bounds__(kThreads, 2)
     VK bm_prev = bminus(pm, -1);       // B-(z-1) for z = 0
     VK bp_cur = bplus(p0, 0);          // B+(z)   for z = 0
     uint32_t sad_mask = 0, max_mask = 0;
-#pragma unroll 4
+#pragma unroll kS1Unroll
     for (int z = 0; z < TZ; ++z) {
         star(z + 2, pp);
         const bool ok = col_ok && (kInterior || z0 + z < A.z_hi);
@@ -442,8 +449,9 @@ __global__ void __launch_bounds__(kThreads, 2)
     // and this column's owned index at z = 0
     const int32_t g_box0 = ((z0 - 1) * D.ny + (y0 - 1)) * D.nx + (x0 - XO);
     const int32_t i_col = (z0 * D.ny + gy) * D.nx + gx - int32_t(A.v0);
-#pragma unroll 2
-    for (int z = 0; z < TZ; ++z) {
+#pragma unroll kOutUnroll
+    for (int zz = 0; zz < TZ; ++zz) {
+        const int z = TZ - 1 - zz;   // top down: measured 1.5 % faster than bottom up on C3
         const bool ok = col_ok && (kInterior || z0 + z < A.z_hi);
         const int c = cfb + 2 * (z + 1) * PS;
         // chase to the root (a cell that points to itself), two hops per
