@@ -118,7 +118,11 @@ enum {
      * reversed total order.  eg_graph's "maxima" then hold the minima, labels
      * the minimum each descending path reaches.  Grids, one GPU, one slab
      * (EG_ERR_UNSUPPORTED otherwise). */
-    EG_MINIMUM = 32u
+    EG_MINIMUM = 32u,
+    /* Arc geometry (Fig. 4): the integral line of
+     * every raw arc -- s, rep, then steepest-ascent steps to m -- available
+     * through eg_get_arc_paths.  Implies EG_RAW_ARCS.  One GPU, one slab. */
+    EG_ARC_PATHS = 64u
 };
 /* virtual partitions: process a grid as k slabs on one GPU, exchanging
  * boundaries by device copies exactly as k ranks would (partition test). */
@@ -157,6 +161,11 @@ eg_status eg_get_graph(eg_ctx *ctx, eg_graph *out);
 /* raw arcs (EG_RAW_ARCS): one (s, rep, m) per upper-link component, ordered by
  * (s, rep); host pointers owned by the ctx; this rank's saddles only. */
 eg_status eg_get_raw_arcs(eg_ctx *ctx, int64_t *n, const int64_t **s, const int64_t **rep, const int64_t **m);
+/* arc geometry (EG_ARC_PATHS): path j (one per raw arc, in eg_get_raw_arcs
+ * order) is vertices[offsets[j] .. offsets[j+1]): the saddle, the component's
+ * representative, then every gradient step to the maximum.  Host pointers
+ * owned by the ctx, valid until the next compute / destroy. */
+eg_status eg_get_arc_paths(eg_ctx *ctx, int64_t *n, const int64_t **offsets, const int64_t **vertices);
 /* labels of the owned vertices: device pointer owned by the ctx, int32 global
  * ids of maxima (N < 2^31). */
 eg_status eg_get_labels(eg_ctx *ctx, const int32_t **d_labels, int64_t *n);

@@ -19,11 +19,13 @@ import numpy as np
 import torch
 
 from . import _abi
-from ._abi import (EG_CHECK_CSR, EG_CHECK_NAN, EG_FORCE_GENERIC, EG_MINIMUM, EG_NO_GRAPH_D2H, EG_RAW_ARCS,  # noqa: F401
+from ._abi import (EG_ARC_PATHS, EG_CHECK_CSR, EG_CHECK_NAN, EG_FORCE_GENERIC, EG_MINIMUM, EG_NO_GRAPH_D2H,
+                   EG_RAW_ARCS,  # noqa: F401
                    EG_VIRTUAL_PARTS)
 
 __all__ = ["Context", "Graph", "EgError", "grid_domain", "csr_domain", "EG_CHECK_NAN", "EG_RAW_ARCS",
-           "EG_CHECK_CSR", "EG_FORCE_GENERIC", "EG_NO_GRAPH_D2H", "EG_MINIMUM", "EG_VIRTUAL_PARTS"]
+           "EG_CHECK_CSR", "EG_FORCE_GENERIC", "EG_NO_GRAPH_D2H", "EG_MINIMUM", "EG_ARC_PATHS",
+           "EG_VIRTUAL_PARTS"]
 
 
 class EgError(RuntimeError):
@@ -43,6 +45,8 @@ class Graph:
     arcs: np.ndarray
     labels: Optional[torch.Tensor]
     raw_arcs: Optional[np.ndarray] = None
+    # EG_ARC_PATHS: (offsets[n+1], vertices) -- path j = vertices[offsets[j]:offsets[j+1]]
+    arc_paths: Optional[tuple] = None
 
 
 def grid_domain(dims: Sequence[int], slab: Optional[Sequence[int]] = None) -> _abi.EgDomain:
@@ -183,6 +187,8 @@ class Context:
         arcs = np.stack([_arr(g.arc_saddle, g.n_arc, np.int64), _arr(g.arc_max, g.n_arc, np.int64),
                          _arr(g.arc_mult, g.n_arc, np.int64)], axis=1) if g.n_arc else np.zeros((0, 3), np.int64)
         raw = None
+        if flags & _abi.EG_ARC_PATHS:
+            flags |= _abi.EG_RAW_ARCS
         if flags & _abi.EG_RAW_ARCS:
             n = C.c_int64()
             s, r, m = C.POINTER(C.c_int64)(), C.POINTER(C.c_int64)(), C.POINTER(C.c_int64)()
@@ -190,9 +196,16 @@ class Context:
                         "eg_get_raw_arcs")
             raw = np.stack([_arr(s, n.value, np.int64), _arr(r, n.value, np.int64), _arr(m, n.value, np.int64)],
                            axis=1) if n.value else np.zeros((0, 3), np.int64)
+        paths = None
+        if flags & _abi.EG_ARC_PATHS:
+            n = C.c_int64()
+            o, v = C.POINTER(C.c_int64)(), C.POINTER(C.c_int64)()
+            self._check(_abi.lib().eg_get_arc_paths(self._h, C.byref(n), C.byref(o), C.byref(v)), "eg_get_arc_paths")
+            off = _arr(o, n.value + 1, np.int64)
+            paths = (off, _arr(v, int(off[-1]), np.int64))
         return Graph(maxima=_arr(g.maxima, g.n_max, np.int64), saddles=_arr(g.saddles, g.n_saddle, np.int64),
                      saddle_beta=_arr(g.saddle_beta, g.n_saddle, np.int32), arcs=arcs, labels=self.labels(),
-                     raw_arcs=raw)
+                     raw_arcs=raw, arc_paths=paths)
 
     def stats(self) -> dict:
         s = _abi.EgStats()

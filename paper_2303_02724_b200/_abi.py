@@ -16,7 +16,7 @@ EG_OK, EG_ERR_INVALID_ARG, EG_ERR_NAN, EG_ERR_OOM, EG_ERR_CUDA, EG_ERR_NCCL, EG_
 STATUS_NAMES = ["EG_OK", "EG_ERR_INVALID_ARG", "EG_ERR_NAN", "EG_ERR_OOM", "EG_ERR_CUDA", "EG_ERR_NCCL",
                 "EG_ERR_STATE", "EG_ERR_UNSUPPORTED"]
 EG_DOMAIN_GRID, EG_DOMAIN_CSR = 0, 1
-EG_CHECK_NAN, EG_RAW_ARCS, EG_CHECK_CSR, EG_FORCE_GENERIC, EG_NO_GRAPH_D2H, EG_MINIMUM = 1, 2, 4, 8, 16, 32
+EG_CHECK_NAN, EG_RAW_ARCS, EG_CHECK_CSR, EG_FORCE_GENERIC, EG_NO_GRAPH_D2H, EG_MINIMUM, EG_ARC_PATHS = 1, 2, 4, 8, 16, 32, 64
 
 
 def EG_VIRTUAL_PARTS(k: int) -> int:
@@ -80,6 +80,7 @@ def lib():
     P64 = C.POINTER(C.c_int64)
     L.eg_get_raw_arcs.argtypes = [vp, P64, C.POINTER(P64), C.POINTER(P64), C.POINTER(P64)]
     L.eg_get_labels.argtypes = [vp, C.POINTER(vp), P64]
+    L.eg_get_arc_paths.argtypes = [vp, P64, C.POINTER(P64), C.POINTER(P64)]
     L.eg_get_stats.argtypes = [vp, C.POINTER(EgStats)]
     L.eg_destroy.argtypes = [vp]
     L.eg_last_error.argtypes = [vp]

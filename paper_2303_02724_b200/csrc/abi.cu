@@ -119,6 +119,10 @@ struct eg_ctx {
 
     HostBuf h_maxima, h_saddles, h_sbeta, h_arc_s, h_arc_m, h_arc_mult, h_raw_s, h_raw_rep, h_raw_m, h_counts;
     HostBuf h_stage;
+    HostBuf h_path_off, h_path_v;      // EG_ARC_PATHS
+    DevBuf path_len, path_off, path_v;
+    int64_t n_paths = 0;
+    bool paths_valid = false;
     int64_t n_max = 0, n_sad = 0, n_arc = 0, n_raw = 0, n_own = 0;
     bool have_graph = false, have_labels = false, graph_on_host = false, raw_valid = false;
     const int32_t *d_labels = nullptr;
@@ -928,8 +932,46 @@ static eg_status compute_impl(eg_ctx *c, const eg_domain *d, const float *f, uin
         c->stats.kernel_launches += 1;
         f = c->mirror.as<float>();
     }
+    c->paths_valid = false;
+    if (flags & EG_ARC_PATHS) {
+        if (c->world > 1 || ((flags >> 8) & 0xffffff) > 1 || c->minimum)
+            return set_err(c, EG_ERR_UNSUPPORTED, "EG_ARC_PATHS: one GPU, one slab, maximum graph");
+        flags |= EG_RAW_ARCS;
+    }
     if (P.grid) ST(compute_grid(c, P, f, flags));
     else ST(compute_csr(c, P, f, flags));
+    if (flags & EG_ARC_PATHS) {
+        // integral lines of the raw arcs: lengths, scan, vertices, to the host
+        SlabState &S = *c->slabs[0];
+        const int64_t nr = S.n_raw;
+        CK(c->path_len.ensure(sizeof(int64_t) * std::max<int64_t>(nr, 1)));
+        CK(c->path_off.ensure(sizeof(int64_t) * (nr + 1)));
+        auto paths = [&](const int64_t *off, int64_t *out) -> cudaError_t {
+            if (P.grid)
+                return launch_arc_paths_grid(c->host_tab, P.ndim, S.F, S.raw_s.as<int64_t>(), S.raw_rep.as<int64_t>(),
+                                             nr, off, out, c->stream);
+            return launch_arc_paths_csr(P.row_ptr, P.col_idx, f, S.raw_s.as<int64_t>(), S.raw_rep.as<int64_t>(), nr,
+                                        off, out, c->stream);
+        };
+        CK(paths(nullptr, c->path_len.as<int64_t>()));
+        const size_t sb = scan64_scratch_bytes(std::max<int64_t>(nr, 1));
+        CK(c->scratch.ensure(sb));
+        CK(launch_scan_i64(c->path_len.as<int64_t>(), c->path_off.as<int64_t>(), nr, c->scratch.p, sb, c->stream));
+        CK(c->h_path_off.ensure(sizeof(int64_t) * (nr + 1)));
+        CK(cudaMemcpyAsync(c->h_path_off.p, c->path_off.p, sizeof(int64_t) * (nr + 1), cudaMemcpyDeviceToHost,
+                           c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        const int64_t total = c->h_path_off.as<int64_t>()[nr];
+        CK(c->path_v.ensure(sizeof(int64_t) * std::max<int64_t>(total, 1)));
+        CK(paths(c->path_off.as<int64_t>(), c->path_v.as<int64_t>()));
+        CK(c->h_path_v.ensure(sizeof(int64_t) * std::max<int64_t>(total, 1)));
+        if (total)
+            CK(cudaMemcpyAsync(c->h_path_v.p, c->path_v.p, sizeof(int64_t) * total, cudaMemcpyDeviceToHost,
+                               c->stream));
+        c->stats.kernel_launches += 3;
+        c->n_paths = nr;
+        c->paths_valid = true;
+    }
     if (c->minimum) {
         SlabState &S = *c->slabs[0];
         const int64_t N = P.N;
@@ -1139,6 +1181,15 @@ eg_status eg_get_raw_arcs(eg_ctx *c, int64_t *n, const int64_t **s, const int64_
     return EG_OK;
 }
 
+eg_status eg_get_arc_paths(eg_ctx *c, int64_t *n, const int64_t **offsets, const int64_t **vertices) {
+    if (!c || !n || !offsets || !vertices) return EG_ERR_INVALID_ARG;
+    if (!c->have_graph || !c->paths_valid) return set_err(c, EG_ERR_STATE, "arc paths need eg_compute with EG_ARC_PATHS");
+    *n = c->n_paths;
+    *offsets = c->h_path_off.as<int64_t>();
+    *vertices = c->h_path_v.as<int64_t>();
+    return EG_OK;
+}
+
 eg_status eg_get_labels(eg_ctx *c, const int32_t **d_labels, int64_t *n) {
     if (!c || !d_labels || !n) return EG_ERR_INVALID_ARG;
     if (!c->have_labels) return set_err(c, EG_ERR_STATE, "no labels (call eg_compute)");
@@ -1158,10 +1209,11 @@ eg_status eg_destroy(eg_ctx *c) {
     cudaSetDevice(c->device);
     cudaStreamSynchronize(c->stream);
     set_slab_count(c, 0);
-    DevBuf *bufs[] = {&c->label_all, &c->field, &c->mirror, &c->flags, &c->counts, &c->scratch, &c->tab, &c->gsend, &c->grecv};
+    DevBuf *bufs[] = {&c->label_all, &c->field, &c->mirror, &c->path_len, &c->path_off, &c->path_v, &c->flags, &c->counts, &c->scratch, &c->tab, &c->gsend, &c->grecv};
     for (DevBuf *b : bufs) b->release();
     HostBuf *hb[] = {&c->h_maxima, &c->h_saddles, &c->h_sbeta, &c->h_arc_s, &c->h_arc_m, &c->h_arc_mult,
-                     &c->h_raw_s, &c->h_raw_rep, &c->h_raw_m, &c->h_counts, &c->h_stage};
+                     &c->h_raw_s, &c->h_raw_rep, &c->h_raw_m, &c->h_counts, &c->h_stage, &c->h_path_off,
+                     &c->h_path_v};
     for (HostBuf *b : hb) b->release();
     for (auto &e : c->ev)
         if (e) cudaEventDestroy(e);

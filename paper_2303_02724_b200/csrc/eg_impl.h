@@ -133,6 +133,19 @@ cudaError_t launch_reflect_negate(const float *f, float *g, int64_t n, cudaStrea
 cudaError_t launch_reverse_i64(int64_t *a, int64_t n, int64_t N, bool map_ids, cudaStream_t st);
 cudaError_t launch_reverse_i32(int32_t *a, int64_t n, int64_t N, bool map_ids, cudaStream_t st);
 
+// arc geometry (integral lines of the raw arcs): off == null -> path lengths
+// into len_or_out[j]; else the vertices at len_or_out[off[j] ..]
+cudaError_t launch_arc_paths_grid(const LinkTable &tab, int ndim, FieldView F, const int64_t *raw_s,
+                                  const int64_t *raw_rep, int64_t n_raw, const int64_t *off, int64_t *len_or_out,
+                                  cudaStream_t st);
+cudaError_t launch_arc_paths_csr(const int64_t *row_ptr, const int32_t *col_idx, const float *f, const int64_t *raw_s,
+                                 const int64_t *raw_rep, int64_t n_raw, const int64_t *off, int64_t *len_or_out,
+                                 cudaStream_t st);
+// exclusive scan of int64 counts into int64 offsets (offsets[n] = total)
+size_t scan64_scratch_bytes(int64_t n);
+cudaError_t launch_scan_i64(const int64_t *in, int64_t *out, int64_t n, void *scratch, size_t scratch_bytes,
+                            cudaStream_t st);
+
 // exclusive scan of int32 counts into int64 offsets (offsets[n] = total)
 size_t scan_scratch_bytes(int64_t n);
 cudaError_t launch_scan_i32(const int32_t *in, int64_t *out, int64_t n, void *scratch, size_t scratch_bytes,

@@ -130,6 +130,26 @@ cudaError_t launch_scan_i32(const int32_t *in, int64_t *out, int64_t n, void *sc
     return cub::DeviceScan::ExclusiveSum(scratch, scratch_bytes, it, out, n + 1, st);
 }
 
+struct PadI64 {
+    const int64_t *in;
+    int64_t n;
+    __host__ __device__ int64_t operator()(int64_t i) const { return i < n ? in[i] : 0; }
+};
+using PadIt64 = thrust::transform_iterator<PadI64, thrust::counting_iterator<int64_t>, int64_t>;
+
+size_t scan64_scratch_bytes(int64_t n) {
+    size_t bytes = 0;
+    PadIt64 it(thrust::counting_iterator<int64_t>(0), PadI64{nullptr, n});
+    cub::DeviceScan::ExclusiveSum(nullptr, bytes, it, (int64_t *)nullptr, n + 1);
+    return bytes;
+}
+
+cudaError_t launch_scan_i64(const int64_t *in, int64_t *out, int64_t n, void *scratch, size_t scratch_bytes,
+                            cudaStream_t st) {
+    PadIt64 it(thrust::counting_iterator<int64_t>(0), PadI64{in, n});
+    return cub::DeviceScan::ExclusiveSum(scratch, scratch_bytes, it, out, n + 1, st);
+}
+
 size_t compact_scratch_bytes(int64_t n) {
     const int64_t words = (n + 31) / 32;
     const int64_t chunks = (words + kCompactBS - 1) / kCompactBS;

@@ -190,6 +190,40 @@ __global__ void __launch_bounds__(128) k_arcs_csr_reps(const int64_t *__restrict
     n_unique[j] = u;
 }
 
+
+// Arc geometry on CSR: s, rep, then the highest upper
+// neighbour at every vertex until a maximum.
+__global__ void __launch_bounds__(128) k_arc_paths_csr(const int64_t *__restrict__ rp, const int32_t *__restrict__ ci,
+                                                       const float *__restrict__ f, const int64_t *__restrict__ raw_s,
+                                                       const int64_t *__restrict__ raw_rep, int64_t n_raw,
+                                                       const int64_t *__restrict__ off, int64_t *len_or_out) {
+    const int64_t j = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (j >= n_raw) return;
+    int64_t *out = off ? len_or_out + off[j] : nullptr;
+    int64_t k = 0;
+    if (out) out[k] = raw_s[j];
+    ++k;
+    int32_t v = int32_t(raw_rep[j]);
+    for (;;) {
+        if (out) out[k] = v;
+        ++k;
+        const float fv = __ldg(f + v);
+        int32_t bv = v;
+        float bf = fv;
+        for (int64_t e = rp[v]; e < rp[v + 1]; ++e) {
+            const int32_t u = ci[e];
+            const float fu = __ldg(f + u);
+            if (csr_higher(f, u, fu, v, fv) && (fu > bf || (fu == bf && u > bv))) {
+                bf = fu;
+                bv = u;
+            }
+        }
+        if (bv == v) break;                 // a maximum
+        v = bv;
+    }
+    if (!off) len_or_out[j] = k;
+}
+
 static inline unsigned blocks_for(int64_t n, int bs) { return unsigned((n + bs - 1) / bs); }
 
 cudaError_t launch_classify_csr(const int64_t *row_ptr, const int32_t *col_idx, const float *f, int64_t v0,
@@ -209,6 +243,15 @@ cudaError_t launch_arcs_csr_reps(const int64_t *row_ptr, const int32_t *rep_buf,
     if (n_sad <= 0) return cudaSuccess;
     k_arcs_csr_reps<<<blocks_for(n_sad, 128), 128, 0, st>>>(row_ptr, rep_buf, saddles, sbeta, n_sad, slot_off, lv,
                                                             tmp_m, tmp_mult, n_unique, raw_s, raw_rep, raw_m);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_arc_paths_csr(const int64_t *row_ptr, const int32_t *col_idx, const float *f, const int64_t *raw_s,
+                                 const int64_t *raw_rep, int64_t n_raw, const int64_t *off, int64_t *len_or_out,
+                                 cudaStream_t st) {
+    if (n_raw <= 0) return cudaSuccess;
+    k_arc_paths_csr<<<blocks_for(n_raw, 128), 128, 0, st>>>(row_ptr, col_idx, f, raw_s, raw_rep, n_raw, off,
+                                                            len_or_out);
     return cudaGetLastError();
 }
 

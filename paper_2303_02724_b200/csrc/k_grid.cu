@@ -357,6 +357,37 @@ __global__ void __launch_bounds__(128) k_arcs_grid(const __grid_constant__ GridC
     reduce_arcs(ms, b, off, tmp_m, tmp_mult, n_unique + j);
 }
 
+
+// ----------------------------------------------- arc geometry
+// The integral line of a raw arc (s, rep, m): s, rep, then gradient steps
+// (the steepest-ascent pointer recomputed from f at every vertex) until
+// the maximum -- Alg. 2's path for that upper-link component.
+// Pass 1 counts the vertices of every path, pass 2 writes them at the
+// scanned offsets.
+template <int NDIM>
+__global__ void __launch_bounds__(128) k_arc_paths_grid(const __grid_constant__ GridConst<NDIM> S, FieldView F,
+                                                        const int64_t *__restrict__ raw_s,
+                                                        const int64_t *__restrict__ raw_rep, int64_t n_raw,
+                                                        const int64_t *__restrict__ off, int64_t *len_or_out) {
+    const int64_t j = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (j >= n_raw) return;
+    int64_t *out = off ? len_or_out + off[j] : nullptr;
+    int64_t k = 0;
+    if (out) out[k] = raw_s[j];
+    ++k;
+    int64_t v = raw_rep[j];
+    for (;;) {
+        if (out) out[k] = v;
+        ++k;
+        int64_t best;
+        typename Lattice<NDIM>::W up, un;
+        upper_link<NDIM, false>(S, F, v, F.at(v), up, un, &best);
+        if ((up | un) == 0) break;          // a maximum
+        v = best;
+    }
+    if (!off) len_or_out[j] = k;
+}
+
 #define EG_DISPATCH_NDIM(ndim, CALL)           \
     switch (ndim) {                             \
         case 1: CALL(1); break;                 \
@@ -405,6 +436,18 @@ cudaError_t launch_arcs_grid(const LinkTable &tab, int ndim, FieldView F, const 
 #define CALL(D)                                                                                              \
     k_arcs_grid<D><<<blocks_for(n_sad, 128), 128, 0, st>>>(make_grid_const<D>(tab), F, saddles, n_sad, slot_off, lv, tmp_m, \
                                                            tmp_mult, n_unique, raw_s, raw_rep, raw_m, beta_out)
+    EG_DISPATCH_NDIM(ndim, CALL)
+#undef CALL
+    return cudaGetLastError();
+}
+
+cudaError_t launch_arc_paths_grid(const LinkTable &tab, int ndim, FieldView F, const int64_t *raw_s,
+                                  const int64_t *raw_rep, int64_t n_raw, const int64_t *off, int64_t *len_or_out,
+                                  cudaStream_t st) {
+    if (n_raw <= 0) return cudaSuccess;
+#define CALL(D)                                                                                              \
+    k_arc_paths_grid<D><<<blocks_for(n_raw, 128), 128, 0, st>>>(make_grid_const<D>(tab), F, raw_s, raw_rep, n_raw, off, \
+                                                                len_or_out)
     EG_DISPATCH_NDIM(ndim, CALL)
 #undef CALL
     return cudaGetLastError();

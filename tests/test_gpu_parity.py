@@ -320,3 +320,44 @@ def test_minimum_graph_unsupported(eg, ctx):
         ctx.compute(torch.from_numpy(f).cuda(), dims=dims, flags=eg.EG_MINIMUM | eg.EG_VIRTUAL_PARTS(2))
     with pytest.raises(Exception):
         ctx.compute(torch.from_numpy(f).cuda(), dims=dims, flags=eg.EG_MINIMUM | eg.EG_RAW_ARCS)
+
+
+def _oracle_paths(o):
+    """Alg. 2 integral lines from the oracle: s, rep, then ptr steps to m."""
+    paths = []
+    for s, rep, m in zip(o.raw_s.tolist(), o.raw_rep.tolist(), o.raw_m.tolist()):
+        p = [s, rep]
+        v = rep
+        while o.ptr[v] != v:
+            v = int(o.ptr[v])
+            p.append(v)
+        assert p[-1] == m
+        paths.append(p)
+    return paths
+
+
+@pytest.mark.parametrize("dims,kind", [([61], "int"), ([48, 40], "normal"), ([40, 33, 29], "int"), ([9, 8, 7, 6], "normal")])
+def test_arc_paths_grid(eg, ctx, dims, kind):
+    """EG_ARC_PATHS: every integral line bit-exact against the oracle's gradient chain."""
+    import torch
+    f, _ = G.random_field(dims, 41 + len(dims), kind)
+    o = O.grid(f, dims)
+    g = ctx.compute(torch.from_numpy(f).cuda(), dims=dims, flags=eg.EG_ARC_PATHS)
+    assert_graph_equal(g, o, raw=True, what=f"paths {dims}")
+    off, v = g.arc_paths
+    exp = _oracle_paths(o)
+    assert len(off) == len(exp) + 1
+    got = [v[off[j]:off[j + 1]].tolist() for j in range(len(exp))]
+    assert got == exp
+
+
+def test_arc_paths_csr(eg, ctx):
+    import torch
+    X, f = G.gmm_points(3000, seed=4)
+    rp, ci = G.knn_csr(X, 8)
+    o = O.csr(f, rp, ci)
+    g = ctx.compute(torch.from_numpy(f).cuda(), csr=(torch.from_numpy(rp).cuda(), torch.from_numpy(ci).cuda()),
+                    flags=eg.EG_ARC_PATHS)
+    off, v = g.arc_paths
+    exp = _oracle_paths(o)
+    assert [v[off[j]:off[j + 1]].tolist() for j in range(len(exp))] == exp
