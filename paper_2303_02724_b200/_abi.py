@@ -25,7 +25,8 @@ def EG_VIRTUAL_PARTS(k: int) -> int:
 
 # every symbol include/eg.h declares (checked by tests/test_abi_exports.py)
 EXPORTS = ["eg_create", "eg_nccl_unique_id", "eg_create_dist", "eg_compute", "eg_compute_host", "eg_gradient",
-           "eg_get_graph", "eg_get_raw_arcs", "eg_get_labels", "eg_get_stats", "eg_destroy", "eg_last_error"]
+           "eg_get_graph", "eg_get_raw_arcs", "eg_get_arc_paths", "eg_get_labels", "eg_get_stats", "eg_destroy",
+           "eg_last_error"]
 
 
 class EgGrid(C.Structure):
