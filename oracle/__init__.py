@@ -266,3 +266,32 @@ def csr_euler(f, row_ptr, col_idx) -> int:
     if rc != OK:
         raise OracleError("euler failed")
     return s.value
+
+
+def bundle(g: Graph, f: np.ndarray, minimum: bool = False) -> Graph:
+    """Arc bundling, literally: "a pair of maxima [may] contain more
+    than one common (n-1)-saddle ... We select a single representative saddle
+    ... the saddle with the highest scalar value" -- reading L19: among the
+    saddles whose arcs reach exactly two distinct maxima {m1, m2}, keep for each
+    pair the highest one (SoS order: value, then index); saddles with one or
+    with three or more distinct maxima are kept; arcs follow their saddles.
+    minimum=True: a minimum graph (O10), "highest" in the reversed order, i.e.
+    the lowest value, ties to the lower index."""
+    f = np.asarray(f, dtype=np.float32).reshape(-1)
+    by_saddle = {}
+    for s, m, c in g.arcs.tolist():
+        by_saddle.setdefault(s, []).append(m)
+    best = {}
+    for s, ms in by_saddle.items():
+        if len(ms) != 2:
+            continue
+        key = (min(ms), max(ms))
+        rank = (lambda t: (-f[t], -t)) if minimum else (lambda t: (f[t], t))
+        if key not in best or rank(s) > rank(best[key]):
+            best[key] = s
+    drop = {s for s, ms in by_saddle.items() if len(ms) == 2 and best[(min(ms), max(ms))] != s}
+    keep_s = np.array([s not in drop for s in g.saddles.tolist()], bool)
+    keep_a = np.array([s not in drop for s in g.arc_s.tolist()], bool)
+    return Graph(ptr=g.ptr, label=g.label, beta=g.beta, maxima=g.maxima, saddles=g.saddles[keep_s],
+                 saddle_beta=g.saddle_beta[keep_s], arc_s=g.arc_s[keep_a], arc_m=g.arc_m[keep_a],
+                 arc_mult=g.arc_mult[keep_a], raw_s=g.raw_s, raw_rep=g.raw_rep, raw_m=g.raw_m)

@@ -599,3 +599,45 @@ def test_minimum_graph_brute(dims, kind, seed):
     assert o.saddles.tolist() == rev(b["saddles"])
     assert o.label.tolist() == [N - 1 - int(b["label"][N - 1 - v]) for v in range(N)]
     assert sorted(map(tuple, o.arcs.tolist())) == sorted((N - 1 - s, N - 1 - m, c) for s, m, c in b["arcs"])
+
+
+# ------------------------------------------- arc bundling
+
+def test_bundle_two_bumps_two_saddles():
+    # 2-D, two bumps (ids 7 and 9 on row 1 of a 5x3 grid) joined through
+    # separate saddles on rows 0 and 2: only the highest saddle of each pair of
+    # maxima survives bundling
+    f = np.array([0.0, 0.1, 0.2, 2.0, 0.3,
+                  0.4, 0.5, 9.0, -5.0, 8.0,
+                  0.6, 0.7, 0.8, 3.0, 0.9], np.float32)
+    g = O.grid(f, [5, 3])
+    b = O.bundle(g, f)
+    pairs = lambda gr: {s: sorted(m for s2, m, _ in gr.arcs.tolist() if s2 == s) for s in gr.saddles.tolist()}
+    two = {s: ms for s, ms in pairs(g).items() if len(ms) == 2}
+    assert len(two) >= 2                                   # the field really has parallel saddles
+    for s, ms in pairs(b).items():
+        assert s in pairs(g)
+    kept2 = [s for s, ms in pairs(b).items() if len(ms) == 2]
+    assert len({tuple(pairs(b)[s]) for s in kept2}) == len(kept2)   # one saddle per pair
+    for s in kept2:                                        # the kept one is the highest of its pair
+        rivals = [t for t, ms in two.items() if ms == pairs(b)[s]]
+        assert max(rivals, key=lambda t: (f[t], t)) == s
+
+
+@pytest.mark.parametrize("dims,seed", [([40, 30], 0), ([20, 20, 16], 1), ([9, 9, 8, 7], 2)])
+def test_bundle_invariants(dims, seed):
+    f, _ = G.random_field(dims, seed, "normal")
+    g = O.grid(f, dims)
+    b = O.bundle(g, f)
+    # connectivity between maxima is unchanged (the Morse decomposition stays represented)
+    conn = lambda gr: {tuple(sorted(set(m for s2, m, _ in gr.arcs.tolist() if s2 == s))) for s in gr.saddles.tolist()}
+    assert conn(b) == conn(g)
+    # one saddle per 2-maxima pair, idempotent, arcs belong to kept saddles
+    ms = {}
+    for s, m, _ in b.arcs.tolist():
+        ms.setdefault(s, set()).add(m)
+    twos = [tuple(sorted(v)) for v in ms.values() if len(v) == 2]
+    assert len(twos) == len(set(twos))
+    bb = O.bundle(b, f)
+    assert np.array_equal(bb.saddles, b.saddles) and np.array_equal(bb.arcs, b.arcs)
+    assert set(b.arc_s.tolist()) <= set(b.saddles.tolist())
