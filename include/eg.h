@@ -122,7 +122,12 @@ enum {
     /* Arc geometry (Fig. 4): the integral line of
      * every raw arc -- s, rep, then steepest-ascent steps to m -- available
      * through eg_get_arc_paths.  Implies EG_RAW_ARCS.  One GPU, one slab. */
-    EG_ARC_PATHS = 64u
+    EG_ARC_PATHS = 64u,
+    /* Arc bundling (reading L19 in DESIGN.md): of the saddles whose
+     * arcs reach exactly the same two maxima, only the highest (value, then
+     * index) is kept in eg_graph -- for a minimum graph the lowest.  Raw arcs
+     * and paths are not filtered.  One GPU, one slab. */
+    EG_BUNDLE = 128u
 };
 /* virtual partitions: process a grid as k slabs on one GPU, exchanging
  * boundaries by device copies exactly as k ranks would (partition test). */

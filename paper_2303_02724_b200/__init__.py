@@ -19,12 +19,12 @@ import numpy as np
 import torch
 
 from . import _abi
-from ._abi import (EG_ARC_PATHS, EG_CHECK_CSR, EG_CHECK_NAN, EG_FORCE_GENERIC, EG_MINIMUM, EG_NO_GRAPH_D2H,
+from ._abi import (EG_ARC_PATHS, EG_BUNDLE, EG_CHECK_CSR, EG_CHECK_NAN, EG_FORCE_GENERIC, EG_MINIMUM, EG_NO_GRAPH_D2H,
                    EG_RAW_ARCS,  # noqa: F401
                    EG_VIRTUAL_PARTS)
 
 __all__ = ["Context", "Graph", "EgError", "grid_domain", "csr_domain", "EG_CHECK_NAN", "EG_RAW_ARCS",
-           "EG_CHECK_CSR", "EG_FORCE_GENERIC", "EG_NO_GRAPH_D2H", "EG_MINIMUM", "EG_ARC_PATHS",
+           "EG_CHECK_CSR", "EG_FORCE_GENERIC", "EG_NO_GRAPH_D2H", "EG_MINIMUM", "EG_ARC_PATHS", "EG_BUNDLE",
            "EG_VIRTUAL_PARTS"]
 
 

@@ -109,6 +109,9 @@ struct eg_ctx {
     DevBuf field;                      // eg_compute_host staging target
     DevBuf mirror;                     // EG_MINIMUM: g[i] = -f[N-1-i]
     bool minimum = false;              // the current compute is a minimum graph
+    bool bundle = false;               // the current compute bundles arcs (EG_BUNDLE)
+    DevBuf bund_scratch;               // arc bundling scratch (keys, indices, scans)
+    DevBuf b_sad64, b_sad32, b_sbeta, b_nu, b_arc_s, b_arc_m, b_arc_mult;   // bundled outputs (swapped in)
     DevBuf flags;                      // [0] nan, [1] deg overflow, [2..] jump-changed per round
     DevBuf counts;                     // int64 / u64 counters
     DevBuf scratch;                    // compaction / scan scratch
@@ -792,7 +795,8 @@ static eg_status compute_grid(eg_ctx *c, const Problem &P, const float *f, uint3
     c->have_labels = true;
     const bool raw = (flags & EG_RAW_ARCS) != 0;
     // one GPU, one slab, graph wanted: the node lists are copied early
-    c->early_d2h = c->world == 1 && c->slabs.size() == 1 && !raw && !(flags & EG_NO_GRAPH_D2H) && !c->minimum;
+    c->early_d2h =
+        c->world == 1 && c->slabs.size() == 1 && !raw && !(flags & EG_NO_GRAPH_D2H) && !c->minimum && !c->bundle;
     for (SlabState *S : c->slabs) ST(grid_graph(c, P, *S, raw, c->early_d2h));
     if (c->early_d2h) CK(cudaEventRecord(c->ev_d2h[2], c->d2h));
     CK(cudaEventRecord(c->ev[4], c->stream));
@@ -899,11 +903,91 @@ static eg_status compute_csr(eg_ctx *c, const Problem &P, const float *f, uint32
     c->n_own = (c->world > 1) ? P.v1 - P.v0 : P.N;
     c->have_labels = true;
     const bool raw = (flags & EG_RAW_ARCS) != 0;
-    c->early_d2h = c->world == 1 && c->slabs.size() == 1 && !raw && !(flags & EG_NO_GRAPH_D2H);
+    c->early_d2h = c->world == 1 && c->slabs.size() == 1 && !raw && !(flags & EG_NO_GRAPH_D2H) && !c->bundle;
     for (SlabState *S : c->slabs) ST(grid_graph(c, P, *S, raw, c->early_d2h));
     if (c->early_d2h) CK(cudaEventRecord(c->ev_d2h[2], c->d2h));
     CK(cudaEventRecord(c->ev[4], c->stream));
     c->raw_valid = raw;
+    return EG_OK;
+}
+
+// Arc bundling (reading L19) of the one slab's graph, on the
+// device: keep the highest saddle of every pair of maxima that several
+// two-maxima saddles share; the kept saddles and arcs replace the slab's.
+static eg_status bundle_arcs(eg_ctx *c) {
+    SlabState &S = *c->slabs[0];
+    const int64_t ns = S.n_sad;
+    if (ns == 0) return EG_OK;
+    const size_t sort_b = (bundle_sort_bytes(ns) + 255) / 256 * 256;
+    const size_t scan_b = (scan_scratch_bytes(ns) + 255) / 256 * 256;
+    const size_t n8 = (8 * size_t(ns) + 255) / 256 * 256, n4 = (4 * size_t(ns) + 255) / 256 * 256,
+                 p8 = (8 * size_t(ns + 1) + 255) / 256 * 256;
+    CK(c->bund_scratch.ensure(2 * n8 + 4 * n4 + 2 * p8 + sort_b + scan_b));
+    char *p = c->bund_scratch.as<char>();
+    BundleArgs B{};
+    B.ns = ns;
+    B.n_unique = S.n_unique.as<int32_t>();
+    B.arc_off = S.arc_off.as<int64_t>();
+    B.arc_s = S.arc_s.as<int64_t>();
+    B.arc_m = S.arc_m.as<int64_t>();
+    B.arc_mult = S.arc_mult.as<int32_t>();
+    B.sad64 = S.saddles64.as<int64_t>();
+    B.sad32 = S.saddles32.as<int32_t>();
+    B.sbeta = S.sbeta.as<int32_t>();
+    B.f = S.F.own;
+    B.f_base = S.F.v0;
+    B.keys = reinterpret_cast<uint64_t *>(p);
+    p += n8;
+    B.keys2 = reinterpret_cast<uint64_t *>(p);
+    p += n8;
+    B.idx = reinterpret_cast<int32_t *>(p);
+    p += n4;
+    B.idx2 = reinterpret_cast<int32_t *>(p);
+    p += n4;
+    B.keep = reinterpret_cast<int32_t *>(p);
+    p += n4;
+    B.arc_cnt = reinterpret_cast<int32_t *>(p);
+    p += n4;
+    B.s_pos = reinterpret_cast<int64_t *>(p);
+    p += p8;
+    B.a_pos = reinterpret_cast<int64_t *>(p);
+    p += p8;
+    B.sort_tmp = p;
+    B.sort_bytes = sort_b;
+    p += sort_b;
+    B.scan_tmp = p;
+    B.scan_bytes = scan_b;
+    CK(c->b_sad64.ensure(8 * std::max<int64_t>(ns, 1)));
+    CK(c->b_sad32.ensure(4 * std::max<int64_t>(ns, 1)));
+    CK(c->b_sbeta.ensure(4 * std::max<int64_t>(ns, 1)));
+    CK(c->b_nu.ensure(4 * std::max<int64_t>(ns, 1)));
+    CK(c->b_arc_s.ensure(8 * std::max<int64_t>(S.n_arc, 1)));
+    CK(c->b_arc_m.ensure(8 * std::max<int64_t>(S.n_arc, 1)));
+    CK(c->b_arc_mult.ensure(4 * std::max<int64_t>(S.n_arc, 1)));
+    B.o_sad64 = c->b_sad64.as<int64_t>();
+    B.o_sad32 = c->b_sad32.as<int32_t>();
+    B.o_sbeta = c->b_sbeta.as<int32_t>();
+    B.o_nu = c->b_nu.as<int32_t>();
+    B.o_arc_s = c->b_arc_s.as<int64_t>();
+    B.o_arc_m = c->b_arc_m.as<int64_t>();
+    B.o_arc_mult = c->b_arc_mult.as<int32_t>();
+    CK(launch_bundle(B, c->stream));
+    c->stats.kernel_launches += 9;
+    int64_t cnt[2];
+    CK(cudaMemcpyAsync(&cnt[0], B.s_pos + ns, sizeof(int64_t), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaMemcpyAsync(&cnt[1], B.a_pos + ns, sizeof(int64_t), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    std::swap(S.saddles64, c->b_sad64);
+    std::swap(S.saddles32, c->b_sad32);
+    std::swap(S.sbeta, c->b_sbeta);
+    std::swap(S.n_unique, c->b_nu);
+    std::swap(S.arc_s, c->b_arc_s);
+    std::swap(S.arc_m, c->b_arc_m);
+    std::swap(S.arc_mult, c->b_arc_mult);
+    S.n_sad = cnt[0];
+    S.n_arc = cnt[1];
+    c->n_sad = cnt[0];
+    c->n_arc = cnt[1];
     return EG_OK;
 }
 
@@ -933,6 +1017,9 @@ static eg_status compute_impl(eg_ctx *c, const eg_domain *d, const float *f, uin
         f = c->mirror.as<float>();
     }
     c->paths_valid = false;
+    c->bundle = (flags & EG_BUNDLE) != 0;
+    if (c->bundle && (c->world > 1 || ((flags >> 8) & 0xffffff) > 1))
+        return set_err(c, EG_ERR_UNSUPPORTED, "EG_BUNDLE: one GPU, one slab");
     if (flags & EG_ARC_PATHS) {
         if (c->world > 1 || ((flags >> 8) & 0xffffff) > 1 || c->minimum)
             return set_err(c, EG_ERR_UNSUPPORTED, "EG_ARC_PATHS: one GPU, one slab, maximum graph");
@@ -972,6 +1059,7 @@ static eg_status compute_impl(eg_ctx *c, const eg_domain *d, const float *f, uin
         c->n_paths = nr;
         c->paths_valid = true;
     }
+    if (c->bundle) ST(bundle_arcs(c));
     if (c->minimum) {
         SlabState &S = *c->slabs[0];
         const int64_t N = P.N;
@@ -1209,7 +1297,8 @@ eg_status eg_destroy(eg_ctx *c) {
     cudaSetDevice(c->device);
     cudaStreamSynchronize(c->stream);
     set_slab_count(c, 0);
-    DevBuf *bufs[] = {&c->label_all, &c->field, &c->mirror, &c->path_len, &c->path_off, &c->path_v, &c->flags, &c->counts, &c->scratch, &c->tab, &c->gsend, &c->grecv};
+    DevBuf *bufs[] = {&c->bund_scratch, &c->b_sad64, &c->b_sad32, &c->b_sbeta, &c->b_nu, &c->b_arc_s, &c->b_arc_m,
+                      &c->b_arc_mult, &c->label_all, &c->field, &c->mirror, &c->path_len, &c->path_off, &c->path_v, &c->flags, &c->counts, &c->scratch, &c->tab, &c->gsend, &c->grecv};
     for (DevBuf *b : bufs) b->release();
     HostBuf *hb[] = {&c->h_maxima, &c->h_saddles, &c->h_sbeta, &c->h_arc_s, &c->h_arc_m, &c->h_arc_mult,
                      &c->h_raw_s, &c->h_raw_rep, &c->h_raw_m, &c->h_counts, &c->h_stage, &c->h_path_off,

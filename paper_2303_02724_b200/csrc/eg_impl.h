@@ -133,6 +133,34 @@ cudaError_t launch_reflect_negate(const float *f, float *g, int64_t n, cudaStrea
 cudaError_t launch_reverse_i64(int64_t *a, int64_t n, int64_t N, bool map_ids, cudaStream_t st);
 cudaError_t launch_reverse_i32(int32_t *a, int64_t n, int64_t N, bool map_ids, cudaStream_t st);
 
+// arc bundling (reading L19) of one slab's graph: inputs, scratch
+// (keys / keys2 / idx / idx2 / keep / arc_cnt of ns entries, s_pos / a_pos of
+// ns + 1, sort and scan scratch) and outputs (the kept saddles and arcs; the
+// counts are s_pos[ns] and a_pos[ns])
+struct BundleArgs {
+    int64_t ns;
+    const int32_t *n_unique;
+    const int64_t *arc_off, *arc_s, *arc_m;
+    const int32_t *arc_mult;
+    const int64_t *sad64;
+    const int32_t *sad32, *sbeta;
+    const float *f;
+    int64_t f_base;                        // global id of f[0]
+    uint64_t *keys, *keys2;
+    int32_t *idx, *idx2, *keep, *arc_cnt;
+    int64_t *s_pos, *a_pos;
+    void *sort_tmp;
+    size_t sort_bytes;
+    void *scan_tmp;
+    size_t scan_bytes;
+    int64_t *o_sad64;
+    int32_t *o_sad32, *o_sbeta, *o_nu;
+    int64_t *o_arc_s, *o_arc_m;
+    int32_t *o_arc_mult;
+};
+size_t bundle_sort_bytes(int64_t ns);
+cudaError_t launch_bundle(const BundleArgs &B, cudaStream_t st);
+
 // arc geometry (integral lines of the raw arcs): off == null -> path lengths
 // into len_or_out[j]; else the vertices at len_or_out[off[j] ..]
 cudaError_t launch_arc_paths_grid(const LinkTable &tab, int ndim, FieldView F, const int64_t *raw_s,

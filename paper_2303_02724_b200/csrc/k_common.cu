@@ -263,6 +263,106 @@ cudaError_t launch_i32_to_i64(const int32_t *in, int64_t *out, int64_t n, cudaSt
     return cudaGetLastError();
 }
 
+
+// ------------------------------------------------ arc bundling
+// Saddles whose arcs reach exactly two distinct maxima {m1 < m2} are keyed by
+// the pair (others by an "absent" key); after a radix sort by key the first
+// thread of every pair's run keeps the highest saddle (value, then index) and
+// drops the rest; kept saddles and their arcs are compacted by scans.
+__global__ void k_bundle_keys(const int32_t *__restrict__ n_unique, const int64_t *__restrict__ arc_off,
+                              const int64_t *__restrict__ arc_m, int64_t ns, uint64_t *keys, int32_t *idx,
+                              int32_t *keep) {
+    const int64_t j = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (j >= ns) return;
+    uint64_t k = ~0ull;
+    if (n_unique[j] == 2) {
+        const int64_t o = arc_off[j];
+        k = (uint64_t(arc_m[o]) << 32) | uint64_t(arc_m[o + 1]);
+    }
+    keys[j] = k;
+    idx[j] = int32_t(j);
+    keep[j] = 1;
+}
+
+__global__ void k_bundle_pick(const uint64_t *__restrict__ keys, const int32_t *__restrict__ idx, int64_t ns,
+                              const int32_t *__restrict__ saddles, const float *__restrict__ f, int64_t f_base,
+                              int32_t *keep) {
+    const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= ns) return;
+    const uint64_t k = keys[i];
+    if (k == ~0ull || (i > 0 && keys[i - 1] == k)) return;     // not the first of a pair's run
+    int64_t e = i + 1;
+    while (e < ns && keys[e] == k) ++e;
+    if (e == i + 1) return;                                     // a single saddle for this pair
+    int32_t best = idx[i];
+    float bf = __ldg(f + (saddles[best] - f_base));
+    for (int64_t q = i + 1; q < e; ++q) {
+        const int32_t j = idx[q];
+        const float fj = __ldg(f + (saddles[j] - f_base));
+        if (fj > bf || (fj == bf && saddles[j] > saddles[best])) {
+            best = j;
+            bf = fj;
+        }
+    }
+    for (int64_t q = i; q < e; ++q)
+        if (idx[q] != best) keep[idx[q]] = 0;
+}
+
+// kept counts: saddles (keep) and arcs (keep * n_unique), for the scans
+__global__ void k_bundle_counts(const int32_t *__restrict__ keep, const int32_t *__restrict__ n_unique, int64_t ns,
+                                int32_t *arc_cnt) {
+    const int64_t j = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (j < ns) arc_cnt[j] = keep[j] ? n_unique[j] : 0;
+}
+
+__global__ void k_bundle_emit(const int32_t *__restrict__ keep, const int64_t *__restrict__ s_pos,
+                              const int64_t *__restrict__ a_pos, const int64_t *__restrict__ arc_off, int64_t ns,
+                              const int64_t *__restrict__ sad64, const int32_t *__restrict__ sad32,
+                              const int32_t *__restrict__ sbeta, const int32_t *__restrict__ n_unique,
+                              const int64_t *__restrict__ arc_s, const int64_t *__restrict__ arc_m,
+                              const int32_t *__restrict__ arc_mult, int64_t *o_sad64, int32_t *o_sad32,
+                              int32_t *o_sbeta, int32_t *o_nu, int64_t *o_arc_s, int64_t *o_arc_m, int32_t *o_arc_mult) {
+    const int64_t j = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (j >= ns || !keep[j]) return;
+    const int64_t p = s_pos[j];
+    o_sad64[p] = sad64[j];
+    o_sad32[p] = sad32[j];
+    o_sbeta[p] = sbeta[j];
+    o_nu[p] = n_unique[j];
+    const int64_t a = a_pos[j], o = arc_off[j];
+    for (int k = 0; k < n_unique[j]; ++k) {
+        o_arc_s[a + k] = arc_s[o + k];
+        o_arc_m[a + k] = arc_m[o + k];
+        o_arc_mult[a + k] = arc_mult[o + k];
+    }
+}
+
+size_t bundle_sort_bytes(int64_t ns) {
+    size_t b = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, b, (const uint64_t *)nullptr, (uint64_t *)nullptr,
+                                    (const int32_t *)nullptr, (int32_t *)nullptr, int(std::max<int64_t>(ns, 1)));
+    return b;
+}
+
+cudaError_t launch_bundle(const BundleArgs &B, cudaStream_t st) {
+    const int64_t ns = B.ns;
+    if (ns <= 0) return cudaSuccess;
+    const unsigned nb = blocks_for(ns, 256);
+    k_bundle_keys<<<nb, 256, 0, st>>>(B.n_unique, B.arc_off, B.arc_m, ns, B.keys, B.idx, B.keep);
+    size_t bytes = B.sort_bytes;
+    cudaError_t e = cub::DeviceRadixSort::SortPairs(B.sort_tmp, bytes, B.keys, B.keys2, B.idx, B.idx2, int(ns), 0,
+                                                    64, st);
+    if (e != cudaSuccess) return e;
+    k_bundle_pick<<<nb, 256, 0, st>>>(B.keys2, B.idx2, ns, B.sad32, B.f, B.f_base, B.keep);
+    k_bundle_counts<<<nb, 256, 0, st>>>(B.keep, B.n_unique, ns, B.arc_cnt);
+    if ((e = launch_scan_i32(B.keep, B.s_pos, ns, B.scan_tmp, B.scan_bytes, st)) != cudaSuccess) return e;
+    if ((e = launch_scan_i32(B.arc_cnt, B.a_pos, ns, B.scan_tmp, B.scan_bytes, st)) != cudaSuccess) return e;
+    k_bundle_emit<<<nb, 256, 0, st>>>(B.keep, B.s_pos, B.a_pos, B.arc_off, ns, B.sad64, B.sad32, B.sbeta, B.n_unique,
+                                      B.arc_s, B.arc_m, B.arc_mult, B.o_sad64, B.o_sad32, B.o_sbeta, B.o_nu,
+                                      B.o_arc_s, B.o_arc_m, B.o_arc_mult);
+    return cudaGetLastError();
+}
+
 // ------------------------------------------------- minimum graph (reading L11)
 // The minimum graph of f is the maximum graph of g[i] = -f[N-1-i]: the point
 // reflection x -> dims-1-x maps the Freudenthal grid onto itself and reverses

@@ -361,3 +361,27 @@ def test_arc_paths_csr(eg, ctx):
     off, v = g.arc_paths
     exp = _oracle_paths(o)
     assert [v[off[j]:off[j + 1]].tolist() for j in range(len(exp))] == exp
+
+
+@pytest.mark.parametrize("dims,kind,minimum", [([64, 48], "normal", False), ([40, 33, 29], "normal", False),
+                                               ([96, 64, 48], "int", False), ([9, 8, 7, 6], "normal", False),
+                                               ([40, 33, 29], "normal", True)])
+@pytest.mark.parametrize("path", PATHS)
+def test_bundled_graph(eg, ctx, dims, kind, minimum, path):
+    """EG_BUNDLE (reading L19) against the oracle's literal bundling."""
+    import torch
+    f, _ = G.random_field(dims, 51 + len(dims), kind)
+    o = O.bundle(O.grid(f, dims, minimum=minimum), f, minimum=minimum)
+    fl = eg.EG_BUNDLE | (eg.EG_MINIMUM if minimum else 0)
+    g = ctx.compute(torch.from_numpy(f).cuda(), dims=dims, flags=_flags(eg, path, fl))
+    assert_graph_equal(g, o, what=f"bundle {dims} {kind} min={minimum} {path}")
+
+
+def test_bundled_graph_csr(eg, ctx):
+    import torch
+    X, f = G.gmm_points(5000, seed=6)
+    rp, ci = G.knn_csr(X, 10)
+    o = O.bundle(O.csr(f, rp, ci), f)
+    g = ctx.compute(torch.from_numpy(f).cuda(), csr=(torch.from_numpy(rp).cuda(), torch.from_numpy(ci).cuda()),
+                    flags=eg.EG_BUNDLE)
+    assert_graph_equal(g, o, what="bundle csr")
