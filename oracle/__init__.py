@@ -12,6 +12,7 @@ single thread, built with ``gcc -O2`` by :func:`build`).
 from __future__ import annotations
 
 import ctypes as C
+import math
 import os
 import subprocess
 from dataclasses import dataclass
@@ -295,3 +296,71 @@ def bundle(g: Graph, f: np.ndarray, minimum: bool = False) -> Graph:
     return Graph(ptr=g.ptr, label=g.label, beta=g.beta, maxima=g.maxima, saddles=g.saddles[keep_s],
                  saddle_beta=g.saddle_beta[keep_s], arc_s=g.arc_s[keep_a], arc_m=g.arc_m[keep_a],
                  arc_mult=g.arc_mult[keep_a], raw_s=g.raw_s, raw_rep=g.raw_rep, raw_m=g.raw_m)
+
+
+def simplify(g: Graph, f: np.ndarray, tau: float, minimum: bool = False) -> Graph:
+    """Persistence-directed cancellation, literally, with lazy cost
+    updates (reading L20 in DESIGN.md):
+    * cost(s) = min over its two distinct maxima of f(m) - f(s) for a simple
+      saddle; f(second highest maximum) - f(s) for a multi-saddle (>= 3
+      distinct maxima); a saddle with one distinct maximum is never cancelled;
+      costs are differences of the float32 values in double precision;
+    * a min-priority queue of (cost, saddle id) holds every saddle; pop s,
+      recompute its cost: above tau -> discard (s stays); above the cost now at
+      the top -> reinsert; else cancel: every distinct maximum of s but the
+      highest (SoS order) is merged into the highest (their other arcs are
+      redirected to it, multiplicities added), and s and the merged maxima leave
+      the graph.
+    minimum=True: a minimum graph (O10): "higher" and the signs are reversed."""
+    import heapq
+    f = np.asarray(f, dtype=np.float32).reshape(-1)
+    sgn = -1.0 if minimum else 1.0
+    val = lambda v: sgn * float(f[v])
+    key = lambda v: (val(v), -v if minimum else v)          # SoS order (reversed for minima)
+    arcs = {}
+    for s, m, c in g.arcs.tolist():
+        arcs.setdefault(s, {})[m] = arcs.get(s, {}).get(m, 0) + c
+    by_max = {}
+    for s, ms in arcs.items():
+        for m in ms:
+            by_max.setdefault(m, set()).add(s)
+    maxima = set(g.maxima.tolist())
+    alive = set(g.saddles.tolist())
+
+    def cost(s):
+        ms = sorted(arcs.get(s, {}), key=key)
+        if len(ms) < 2:
+            return math.inf
+        return (val(ms[0]) if len(ms) == 2 else val(ms[-2])) - val(s)
+
+    heap = [(cost(s), s) for s in sorted(alive)]
+    heapq.heapify(heap)
+    while heap:
+        _, s = heapq.heappop(heap)
+        c = cost(s)
+        if c > tau:
+            continue
+        if heap and c > heap[0][0]:
+            heapq.heappush(heap, (c, s))
+            continue
+        ms = sorted(arcs[s], key=key)
+        top = ms[-1]
+        for m in ms[:-1]:
+            for s2 in by_max.pop(m, set()):
+                if s2 == s:
+                    continue
+                mult = arcs[s2].pop(m)
+                arcs[s2][top] = arcs[s2].get(top, 0) + mult
+                by_max.setdefault(top, set()).add(s2)
+            maxima.discard(m)
+        for m in arcs.pop(s):
+            if m in by_max:
+                by_max[m].discard(s)
+        alive.discard(s)
+    keep = np.array([s in alive for s in g.saddles.tolist()], bool)
+    out = sorted((s, m, c) for s in alive for m, c in arcs[s].items())
+    a = np.array(out, np.int64).reshape(-1, 3)
+    return Graph(ptr=g.ptr, label=g.label, beta=g.beta, maxima=np.array(sorted(maxima), np.int64),
+                 saddles=g.saddles[keep], saddle_beta=g.saddle_beta[keep], arc_s=a[:, 0].copy(),
+                 arc_m=a[:, 1].copy(), arc_mult=a[:, 2].astype(np.int32), raw_s=g.raw_s, raw_rep=g.raw_rep,
+                 raw_m=g.raw_m)

@@ -641,3 +641,70 @@ def test_bundle_invariants(dims, seed):
     bb = O.bundle(b, f)
     assert np.array_equal(bb.saddles, b.saddles) and np.array_equal(bb.arcs, b.arcs)
     assert set(b.arc_s.tolist()) <= set(b.saddles.tolist())
+
+
+# ------------------------------- persistence-directed cancellation
+
+def test_simplify_1d_hand():
+    # maxima 1 (5), 3 (9), 5 (7); saddles 2 (1), 4 (2); costs 4 and 5
+    f = np.array([0, 5, 1, 9, 2, 7, 3], np.float32)
+    g = O.grid(f, [7])
+    assert g.maxima.tolist() == [1, 3, 5] and g.saddles.tolist() == [2, 4]
+    s = O.simplify(g, f, 4.5)
+    assert s.maxima.tolist() == [3, 5] and s.saddles.tolist() == [4]
+    assert s.arcs.tolist() == [[4, 3, 1], [4, 5, 1]]
+    assert O.simplify(g, f, 3.0).maxima.tolist() == [1, 3, 5]
+    t = O.simplify(g, f, math.inf)
+    assert t.maxima.tolist() == [3] and len(t.saddles) == 0
+
+
+def _persistence_1d(h):
+    """Textbook 0-dim persistence of superlevel sets of a 1-D sequence (elder
+    rule, SoS ties by index): the persistence of every local maximum."""
+    n = len(h)
+    order = sorted(range(n), key=lambda i: (h[i], i), reverse=True)
+    parent, birth, pers = {}, {}, {}
+    def find(x):
+        while parent[x] != x:
+            parent[x] = parent[parent[x]]
+            x = parent[x]
+        return x
+    for i in order:
+        parent[i] = i
+        birth[i] = i
+        for j in (i - 1, i + 1):
+            if j in parent:
+                a, b = find(i), find(j)
+                if a == b:
+                    continue
+                young, old = (a, b) if (h[birth[a]], birth[a]) < (h[birth[b]], birth[b]) else (b, a)
+                if birth[young] != i:
+                    pers[birth[young]] = float(h[birth[young]]) - float(h[i])
+                parent[young] = old
+    root = find(order[0])
+    pers[birth[root]] = math.inf
+    return pers
+
+
+@pytest.mark.parametrize("seed", range(5))
+def test_simplify_matches_1d_persistence(seed):
+    # in 1-D the lazy cancellation keeps exactly the maxima whose elder-rule
+    # persistence exceeds tau
+    rng = np.random.default_rng(seed)
+    f = rng.standard_normal(300).astype(np.float32)
+    g = O.grid(f, [300])
+    pers = _persistence_1d(f.astype(np.float64))
+    for tau in (0.1, 0.5, 1.0, 2.0):
+        s = O.simplify(g, f, tau)
+        assert s.maxima.tolist() == sorted(m for m, p in pers.items() if p > tau and m in set(g.maxima.tolist()))
+
+
+@pytest.mark.parametrize("dims,seed", [([40, 30], 0), ([16, 16, 12], 1)])
+def test_simplify_invariants(dims, seed):
+    f, _ = G.random_field(dims, seed, "normal")
+    g = O.grid(f, dims)
+    counts = [len(O.simplify(g, f, t).maxima) for t in (0.0, 0.2, 0.5, 1.0, 2.0, math.inf)]
+    assert counts == sorted(counts, reverse=True)          # monotone in tau
+    assert counts[-1] == 1                                   # a connected graph ends with one maximum
+    z = O.simplify(g, f, -1.0)                               # nothing below a negative threshold
+    assert np.array_equal(z.maxima, g.maxima) and np.array_equal(z.arcs, g.arcs)
