@@ -127,7 +127,9 @@ enum {
      * arcs reach exactly the same two maxima, only the highest (value, then
      * index) is kept in eg_graph -- for a minimum graph the lowest.  Raw arcs
      * and paths are not filtered.  One GPU, one slab. */
-    EG_BUNDLE = 128u
+    EG_BUNDLE = 128u,
+    /* keep f at every maximum and saddle (for eg_simplify); one process */
+    EG_NODE_VALUES = 256u
 };
 /* virtual partitions: process a grid as k slabs on one GPU, exchanging
  * boundaries by device copies exactly as k ranks would (partition test). */
@@ -171,6 +173,15 @@ eg_status eg_get_raw_arcs(eg_ctx *ctx, int64_t *n, const int64_t **s, const int6
  * representative, then every gradient step to the maximum.  Host pointers
  * owned by the ctx, valid until the next compute / destroy. */
 eg_status eg_get_arc_paths(eg_ctx *ctx, int64_t *n, const int64_t **offsets, const int64_t **vertices);
+/* Persistence-directed cancellation (reading L20 in
+ * DESIGN.md) of the last graph (which needs EG_NODE_VALUES): saddles are
+ * cancelled in increasing cost (f(lower adjacent maximum) - f(s); the second
+ * highest for a multi-saddle) with lazy updates while the cost is <= tau, each
+ * merging its lower maxima into its highest.  Serial on the host, as in the
+ * paper.  The result is returned in `out` (host pointers owned by the ctx,
+ * valid until the next call); the unsimplified graph stays available through
+ * eg_get_graph.  A minimum graph is simplified in the reversed order. */
+eg_status eg_simplify(eg_ctx *ctx, double tau, eg_graph *out);
 /* labels of the owned vertices: device pointer owned by the ctx, int32 global
  * ids of maxima (N < 2^31). */
 eg_status eg_get_labels(eg_ctx *ctx, const int32_t **d_labels, int64_t *n);

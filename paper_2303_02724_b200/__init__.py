@@ -19,12 +19,12 @@ import numpy as np
 import torch
 
 from . import _abi
-from ._abi import (EG_ARC_PATHS, EG_BUNDLE, EG_CHECK_CSR, EG_CHECK_NAN, EG_FORCE_GENERIC, EG_MINIMUM, EG_NO_GRAPH_D2H,
+from ._abi import (EG_ARC_PATHS, EG_BUNDLE, EG_NODE_VALUES, EG_CHECK_CSR, EG_CHECK_NAN, EG_FORCE_GENERIC, EG_MINIMUM, EG_NO_GRAPH_D2H,
                    EG_RAW_ARCS,  # noqa: F401
                    EG_VIRTUAL_PARTS)
 
 __all__ = ["Context", "Graph", "EgError", "grid_domain", "csr_domain", "EG_CHECK_NAN", "EG_RAW_ARCS",
-           "EG_CHECK_CSR", "EG_FORCE_GENERIC", "EG_NO_GRAPH_D2H", "EG_MINIMUM", "EG_ARC_PATHS", "EG_BUNDLE",
+           "EG_CHECK_CSR", "EG_FORCE_GENERIC", "EG_NO_GRAPH_D2H", "EG_MINIMUM", "EG_ARC_PATHS", "EG_BUNDLE", "EG_NODE_VALUES",
            "EG_VIRTUAL_PARTS"]
 
 
@@ -206,6 +206,16 @@ class Context:
         return Graph(maxima=_arr(g.maxima, g.n_max, np.int64), saddles=_arr(g.saddles, g.n_saddle, np.int64),
                      saddle_beta=_arr(g.saddle_beta, g.n_saddle, np.int32), arcs=arcs, labels=self.labels(),
                      raw_arcs=raw, arc_paths=paths)
+
+    def simplify(self, tau: float) -> Graph:
+        """Persistence-directed cancellation of the last graph, which
+        must have been computed with EG_NODE_VALUES; serial on the host."""
+        g = _abi.EgGraph()
+        self._check(_abi.lib().eg_simplify(self._h, C.c_double(tau), C.byref(g)), "eg_simplify")
+        arcs = np.stack([_arr(g.arc_saddle, g.n_arc, np.int64), _arr(g.arc_max, g.n_arc, np.int64),
+                         _arr(g.arc_mult, g.n_arc, np.int64)], axis=1) if g.n_arc else np.zeros((0, 3), np.int64)
+        return Graph(maxima=_arr(g.maxima, g.n_max, np.int64), saddles=_arr(g.saddles, g.n_saddle, np.int64),
+                     saddle_beta=_arr(g.saddle_beta, g.n_saddle, np.int32), arcs=arcs, labels=None)
 
     def stats(self) -> dict:
         s = _abi.EgStats()

@@ -17,7 +17,7 @@ STATUS_NAMES = ["EG_OK", "EG_ERR_INVALID_ARG", "EG_ERR_NAN", "EG_ERR_OOM", "EG_E
                 "EG_ERR_STATE", "EG_ERR_UNSUPPORTED"]
 EG_DOMAIN_GRID, EG_DOMAIN_CSR = 0, 1
 (EG_CHECK_NAN, EG_RAW_ARCS, EG_CHECK_CSR, EG_FORCE_GENERIC, EG_NO_GRAPH_D2H, EG_MINIMUM, EG_ARC_PATHS,
- EG_BUNDLE) = 1, 2, 4, 8, 16, 32, 64, 128
+ EG_BUNDLE, EG_NODE_VALUES) = 1, 2, 4, 8, 16, 32, 64, 128, 256
 
 
 def EG_VIRTUAL_PARTS(k: int) -> int:
@@ -26,8 +26,8 @@ def EG_VIRTUAL_PARTS(k: int) -> int:
 
 # every symbol include/eg.h declares (checked by tests/test_abi_exports.py)
 EXPORTS = ["eg_create", "eg_nccl_unique_id", "eg_create_dist", "eg_compute", "eg_compute_host", "eg_gradient",
-           "eg_get_graph", "eg_get_raw_arcs", "eg_get_arc_paths", "eg_get_labels", "eg_get_stats", "eg_destroy",
-           "eg_last_error"]
+           "eg_get_graph", "eg_get_raw_arcs", "eg_get_arc_paths", "eg_simplify", "eg_get_labels", "eg_get_stats",
+           "eg_destroy", "eg_last_error"]
 
 
 class EgGrid(C.Structure):
@@ -83,6 +83,7 @@ def lib():
     L.eg_get_raw_arcs.argtypes = [vp, P64, C.POINTER(P64), C.POINTER(P64), C.POINTER(P64)]
     L.eg_get_labels.argtypes = [vp, C.POINTER(vp), P64]
     L.eg_get_arc_paths.argtypes = [vp, P64, C.POINTER(P64), C.POINTER(P64)]
+    L.eg_simplify.argtypes = [vp, C.c_double, C.POINTER(EgGraph)]
     L.eg_get_stats.argtypes = [vp, C.POINTER(EgStats)]
     L.eg_destroy.argtypes = [vp]
     L.eg_last_error.argtypes = [vp]

@@ -123,6 +123,10 @@ struct eg_ctx {
     HostBuf h_maxima, h_saddles, h_sbeta, h_arc_s, h_arc_m, h_arc_mult, h_raw_s, h_raw_rep, h_raw_m, h_counts;
     HostBuf h_stage;
     HostBuf h_path_off, h_path_v;      // EG_ARC_PATHS
+    HostBuf h_fmax, h_fsad;            // EG_NODE_VALUES: f at the maxima / saddles
+    DevBuf d_fnode;
+    bool node_values = false, last_minimum = false;
+    SimplifyResult simp;               // eg_simplify's output
     DevBuf path_len, path_off, path_v;
     int64_t n_paths = 0;
     bool paths_valid = false;
@@ -1007,6 +1011,7 @@ static eg_status compute_impl(eg_ctx *c, const eg_domain *d, const float *f, uin
     CK(cudaMemsetAsync(c->flags.p, 0, sizeof(int) * 128, c->stream));
     // EG_MINIMUM (reading L11): the maximum graph of g[i] = -f[N-1-i], mapped
     // back by i -> N-1-i (k_common.cu)
+    const float *f_user = f;           // the caller's field (device) -- f becomes the mirror for a minimum graph
     c->minimum = (flags & EG_MINIMUM) != 0;
     if (c->minimum) {
         if (!P.grid || c->world > 1 || ((flags >> 8) & 0xffffff) > 1 || (flags & EG_RAW_ARCS))
@@ -1076,6 +1081,26 @@ static eg_status compute_impl(eg_ctx *c, const eg_domain *d, const float *f, uin
     if (!(flags & EG_NO_GRAPH_D2H)) {
         ST(gather_graph(c, (flags & EG_RAW_ARCS) != 0));
         c->graph_on_host = true;
+    }
+    c->node_values = false;
+    c->last_minimum = c->minimum;
+    if ((flags & EG_NODE_VALUES) && c->world == 1 && c->graph_on_host) {
+        // f (of the caller's field) at every maximum and saddle, slab by slab
+        CK(c->d_fnode.ensure(sizeof(float) * std::max<int64_t>(c->n_max + c->n_sad, 1)));
+        CK(c->h_fmax.ensure(sizeof(float) * std::max<int64_t>(c->n_max, 1)));
+        CK(c->h_fsad.ensure(sizeof(float) * std::max<int64_t>(c->n_sad, 1)));
+        float *dm = c->d_fnode.as<float>(), *ds = dm + c->n_max;
+        int64_t om = 0, os = 0;
+        for (SlabState *S : c->slabs) {
+            CK(launch_gather_f(f_user, 0, S->maxima64.as<int64_t>(), S->n_max, dm + om, c->stream));
+            CK(launch_gather_f(f_user, 0, S->saddles64.as<int64_t>(), S->n_sad, ds + os, c->stream));
+            om += S->n_max;
+            os += S->n_sad;
+        }
+        if (c->n_max) CK(cudaMemcpyAsync(c->h_fmax.p, dm, sizeof(float) * c->n_max, cudaMemcpyDeviceToHost, c->stream));
+        if (c->n_sad) CK(cudaMemcpyAsync(c->h_fsad.p, ds, sizeof(float) * c->n_sad, cudaMemcpyDeviceToHost, c->stream));
+        c->stats.kernel_launches += 2 * int(c->slabs.size());
+        c->node_values = true;
     }
     CK(cudaEventRecord(c->ev[5], c->stream));
     CK(cudaStreamSynchronize(c->stream));
@@ -1269,6 +1294,25 @@ eg_status eg_get_raw_arcs(eg_ctx *c, int64_t *n, const int64_t **s, const int64_
     return EG_OK;
 }
 
+eg_status eg_simplify(eg_ctx *c, double tau, eg_graph *out) {
+    if (!c || !out) return EG_ERR_INVALID_ARG;
+    if (!c->have_graph || !c->graph_on_host || !c->node_values)
+        return set_err(c, EG_ERR_STATE, "eg_simplify needs the last eg_compute with EG_NODE_VALUES (one process)");
+    simplify_graph(c->n_max, c->h_maxima.as<int64_t>(), c->h_fmax.as<float>(), c->n_sad, c->h_saddles.as<int64_t>(),
+                   c->h_sbeta.as<int32_t>(), c->h_fsad.as<float>(), c->n_arc, c->h_arc_s.as<int64_t>(),
+                   c->h_arc_m.as<int64_t>(), c->h_arc_mult.as<int32_t>(), tau, c->last_minimum, c->simp);
+    out->n_max = int64_t(c->simp.maxima.size());
+    out->n_saddle = int64_t(c->simp.saddles.size());
+    out->n_arc = int64_t(c->simp.arc_s.size());
+    out->maxima = c->simp.maxima.data();
+    out->saddles = c->simp.saddles.data();
+    out->saddle_beta = c->simp.saddle_beta.data();
+    out->arc_saddle = c->simp.arc_s.data();
+    out->arc_max = c->simp.arc_m.data();
+    out->arc_mult = c->simp.arc_mult.data();
+    return EG_OK;
+}
+
 eg_status eg_get_arc_paths(eg_ctx *c, int64_t *n, const int64_t **offsets, const int64_t **vertices) {
     if (!c || !n || !offsets || !vertices) return EG_ERR_INVALID_ARG;
     if (!c->have_graph || !c->paths_valid) return set_err(c, EG_ERR_STATE, "arc paths need eg_compute with EG_ARC_PATHS");
@@ -1297,10 +1341,10 @@ eg_status eg_destroy(eg_ctx *c) {
     cudaSetDevice(c->device);
     cudaStreamSynchronize(c->stream);
     set_slab_count(c, 0);
-    DevBuf *bufs[] = {&c->bund_scratch, &c->b_sad64, &c->b_sad32, &c->b_sbeta, &c->b_nu, &c->b_arc_s, &c->b_arc_m,
+    DevBuf *bufs[] = {&c->d_fnode, &c->bund_scratch, &c->b_sad64, &c->b_sad32, &c->b_sbeta, &c->b_nu, &c->b_arc_s, &c->b_arc_m,
                       &c->b_arc_mult, &c->label_all, &c->field, &c->mirror, &c->path_len, &c->path_off, &c->path_v, &c->flags, &c->counts, &c->scratch, &c->tab, &c->gsend, &c->grecv};
     for (DevBuf *b : bufs) b->release();
-    HostBuf *hb[] = {&c->h_maxima, &c->h_saddles, &c->h_sbeta, &c->h_arc_s, &c->h_arc_m, &c->h_arc_mult,
+    HostBuf *hb[] = {&c->h_fmax, &c->h_fsad, &c->h_maxima, &c->h_saddles, &c->h_sbeta, &c->h_arc_s, &c->h_arc_m, &c->h_arc_mult,
                      &c->h_raw_s, &c->h_raw_rep, &c->h_raw_m, &c->h_counts, &c->h_stage, &c->h_path_off,
                      &c->h_path_v};
     for (HostBuf *b : hb) b->release();

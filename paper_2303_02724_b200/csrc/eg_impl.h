@@ -161,6 +161,17 @@ struct BundleArgs {
 size_t bundle_sort_bytes(int64_t ns);
 cudaError_t launch_bundle(const BundleArgs &B, cudaStream_t st);
 
+// persistence-directed cancellation (simplify.cu): host-side, serial
+struct SimplifyResult {
+    std::vector<int64_t> maxima, saddles, arc_s, arc_m;
+    std::vector<int32_t> saddle_beta, arc_mult;
+};
+void simplify_graph(int64_t n_max, const int64_t *maxima, const float *fmax, int64_t n_sad, const int64_t *saddles,
+                    const int32_t *sbeta, const float *fsad, int64_t n_arc, const int64_t *arc_s,
+                    const int64_t *arc_m, const int32_t *arc_mult, double tau, bool minimum, SimplifyResult &out);
+cudaError_t launch_gather_f(const float *f, int64_t f_base, const int64_t *ids, int64_t n, float *out,
+                            cudaStream_t st);
+
 // arc geometry (integral lines of the raw arcs): off == null -> path lengths
 // into len_or_out[j]; else the vertices at len_or_out[off[j] ..]
 cudaError_t launch_arc_paths_grid(const LinkTable &tab, int ndim, FieldView F, const int64_t *raw_s,

@@ -385,3 +385,37 @@ def test_bundled_graph_csr(eg, ctx):
     g = ctx.compute(torch.from_numpy(f).cuda(), csr=(torch.from_numpy(rp).cuda(), torch.from_numpy(ci).cuda()),
                     flags=eg.EG_BUNDLE)
     assert_graph_equal(g, o, what="bundle csr")
+
+
+@pytest.mark.parametrize("dims,kind,minimum", [([300], "normal", False), ([64, 48], "normal", False),
+                                               ([40, 33, 29], "normal", False), ([40, 33, 29], "int", True),
+                                               ([9, 8, 7, 6], "normal", False)])
+def test_simplify(eg, ctx, dims, kind, minimum):
+    """eg_simplify (reading L20) against the oracle's literal lazy cancellation."""
+    import math
+    import torch
+    f, _ = G.random_field(dims, 61 + len(dims), kind)
+    o = O.grid(f, dims, minimum=minimum)
+    fl = eg.EG_NODE_VALUES | (eg.EG_MINIMUM if minimum else 0)
+    ctx.compute(torch.from_numpy(f).cuda(), dims=dims, flags=fl)
+    for tau in (0.0, 0.3, 1.0, math.inf):
+        s = ctx.simplify(tau)
+        e = O.simplify(o, f, tau, minimum=minimum)
+        for name, a, b in [("maxima", s.maxima, e.maxima), ("saddles", s.saddles, e.saddles),
+                           ("saddle_beta", s.saddle_beta, e.saddle_beta), ("arcs", s.arcs, e.arcs)]:
+            assert first_diff(a, b) is None, f"{name} tau={tau}: {first_diff(a, b)}"
+
+
+def test_simplify_csr_and_state(eg, ctx):
+    import torch
+    X, f = G.gmm_points(4000, seed=8)
+    rp, ci = G.knn_csr(X, 10)
+    o = O.csr(f, rp, ci)
+    ctx.compute(torch.from_numpy(f).cuda(), csr=(torch.from_numpy(rp).cuda(), torch.from_numpy(ci).cuda()),
+                flags=eg.EG_NODE_VALUES)
+    s = ctx.simplify(0.5)
+    e = O.simplify(o, f, 0.5)
+    assert np.array_equal(s.maxima, e.maxima) and np.array_equal(s.arcs, e.arcs)
+    ctx.compute(torch.from_numpy(f).cuda(), csr=(torch.from_numpy(rp).cuda(), torch.from_numpy(ci).cuda()))
+    with pytest.raises(Exception):
+        ctx.simplify(0.5)                   # the last compute kept no node values
