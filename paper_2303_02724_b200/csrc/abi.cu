@@ -140,6 +140,13 @@ struct eg_ctx {
     // the arcs are computed (ev_d2h[0]: lists ready, [1]: beta ready, [2]: copies done)
     cudaStream_t d2h = nullptr;
     cudaEvent_t ev_d2h[3] = {};
+    // one slab on one GPU: the graph stage (lists, arcs, D2H) runs on `aux`
+    // while the labels are finalised on `stream` (ev_tile: local phase done,
+    // ev_graph: graph stage done); gstream = the stream of the graph stage
+    cudaStream_t aux = nullptr, gstream = nullptr;
+    int prio_lo = 0, prio_hi = 0;
+    cudaEvent_t ev_tile = nullptr, ev_graph = nullptr;
+    bool overlap = false;
     bool early_d2h = false;            // set per compute: the node-list copies are already queued
 };
 
@@ -281,7 +288,7 @@ static eg_status ensure_table(eg_ctx *c, const Problem &P) {
 static float ev_us(cudaEvent_t a, cudaEvent_t b) {
     float ms = 0.f;
     cudaEventElapsedTime(&ms, a, b);
-    return ms * 1000.f;
+    return ms > 0.f ? ms * 1000.f : 0.f;     // phases on two streams may overlap
 }
 
 static void set_slab_count(eg_ctx *c, size_t k) {
@@ -378,7 +385,7 @@ static eg_status grid_graph(eg_ctx *c, const Problem &P, SlabState &S, bool raw,
         CK(S.saddles32.ensure(sizeof(int32_t) * std::max<int64_t>(S.n_sad, 1)));
         CK(S.saddles64.ensure(sizeof(int64_t) * std::max<int64_t>(S.n_sad, 1)));
         eg_status st = tiled3d_lists(S.tiled, S.maxima64.as<int64_t>(), S.saddles32.as<int32_t>(),
-                                     S.saddles64.as<int64_t>(), c->stream, &c->stats, &c->err);
+                                     S.saddles64.as<int64_t>(), c->gstream, &c->stats, &c->err);
         if (st != EG_OK) {
             if (st == EG_ERR_CUDA) c->poisoned = true;
             return st;
@@ -389,30 +396,30 @@ static eg_status grid_graph(eg_ctx *c, const Problem &P, SlabState &S, bool raw,
             (std::max(compact_scratch_bytes(std::max<int64_t>(n, 1)), size_t(1) << 16) + 255) / 256 * 256;
         CK(c->scratch.ensure(2 * half));
         char *scr_max = c->scratch.as<char>(), *scr_sad = c->scratch.as<char>() + half;
-        CK(launch_count_bits(S.max_bits.as<uint32_t>(), n, scr_max, cnt + 0, c->stream));
-        CK(launch_count_bits(S.sad_bits.as<uint32_t>(), n, scr_sad, cnt + 1, c->stream));
+        CK(launch_count_bits(S.max_bits.as<uint32_t>(), n, scr_max, cnt + 0, c->gstream));
+        CK(launch_count_bits(S.sad_bits.as<uint32_t>(), n, scr_sad, cnt + 1, c->gstream));
         c->stats.kernel_launches += 4;
-        CK(cudaMemcpyAsync(hc, cnt, sizeof(int64_t) * 2, cudaMemcpyDeviceToHost, c->stream));
-        CK(cudaStreamSynchronize(c->stream));
+        CK(cudaMemcpyAsync(hc, cnt, sizeof(int64_t) * 2, cudaMemcpyDeviceToHost, c->gstream));
+        CK(cudaStreamSynchronize(c->gstream));
         S.n_max = hc[0];
         S.n_sad = hc[1];
         CK(S.maxima64.ensure(sizeof(int64_t) * std::max<int64_t>(S.n_max, 1)));
         CK(S.saddles32.ensure(sizeof(int32_t) * std::max<int64_t>(S.n_sad, 1)));
         CK(S.saddles64.ensure(sizeof(int64_t) * std::max<int64_t>(S.n_sad, 1)));
         CK(launch_emit_counted(S.max_bits.as<uint32_t>(), n, S.s.v0, scr_max, nullptr, S.maxima64.as<int64_t>(),
-                               c->stream));
+                               c->gstream));
         CK(launch_emit_counted(S.sad_bits.as<uint32_t>(), n, S.s.v0, scr_sad, S.saddles32.as<int32_t>(),
-                               S.saddles64.as<int64_t>(), c->stream));
+                               S.saddles64.as<int64_t>(), c->gstream));
         c->stats.kernel_launches += 2;
     }
     const int64_t ns = S.n_sad;
-    CK(cudaEventRecord(c->ev[3], c->stream));
+    CK(cudaEventRecord(c->ev[3], c->gstream));
     if (early) {
         // the node lists are final: copy them while the arcs are computed
         CK(c->h_maxima.ensure(sizeof(int64_t) * std::max<int64_t>(S.n_max, 1)));
         CK(c->h_saddles.ensure(sizeof(int64_t) * std::max<int64_t>(ns, 1)));
         CK(c->h_sbeta.ensure(sizeof(int32_t) * std::max<int64_t>(ns, 1)));
-        CK(cudaEventRecord(c->ev_d2h[0], c->stream));
+        CK(cudaEventRecord(c->ev_d2h[0], c->gstream));
         CK(cudaStreamWaitEvent(c->d2h, c->ev_d2h[0], 0));
         if (S.n_max)
             CK(cudaMemcpyAsync(c->h_maxima.p, S.maxima64.p, sizeof(int64_t) * S.n_max, cudaMemcpyDeviceToHost, c->d2h));
@@ -435,6 +442,7 @@ static eg_status grid_graph(eg_ctx *c, const Problem &P, SlabState &S, bool raw,
         lv.lo = S.has_lo ? S.hval_lo.as<int32_t>() : nullptr;
         lv.hi = S.has_hi ? S.hval_hi.as<int32_t>() : nullptr;
         lv.plane = S.s.plane;
+        lv.chase = c->overlap;
     } else {
         lv.own = c->label_all.as<int32_t>();     // CSR: labels of every vertex
         lv.v0 = 0;
@@ -450,10 +458,10 @@ static eg_status grid_graph(eg_ctx *c, const Problem &P, SlabState &S, bool raw,
         CK(S.tmp_mult.ensure(sizeof(int32_t) * std::max<int64_t>(ns * stride, 1)));
         CK(launch_arcs_grid(c->host_tab, P.ndim, S.F, S.saddles32.as<int32_t>(), ns, nullptr, lv,
                             S.tmp_m.as<int32_t>(), S.tmp_mult.as<int32_t>(), S.n_unique.as<int32_t>(), nullptr,
-                            nullptr, nullptr, c->stream, S.sbeta.as<int32_t>()));
+                            nullptr, nullptr, c->gstream, S.sbeta.as<int32_t>()));
         c->stats.kernel_launches += 1;
         if (early) {
-            CK(cudaEventRecord(c->ev_d2h[1], c->stream));
+            CK(cudaEventRecord(c->ev_d2h[1], c->gstream));
             CK(cudaStreamWaitEvent(c->d2h, c->ev_d2h[1], 0));
             if (ns)
                 CK(cudaMemcpyAsync(c->h_sbeta.p, S.sbeta.p, sizeof(int32_t) * ns, cudaMemcpyDeviceToHost, c->d2h));
@@ -461,14 +469,14 @@ static eg_status grid_graph(eg_ctx *c, const Problem &P, SlabState &S, bool raw,
     } else {
         if (P.grid)
             CK(launch_saddle_beta_grid(c->host_tab, P.ndim, S.F, S.saddles32.as<int32_t>(), ns,
-                                       S.sbeta.as<int32_t>(), c->stream));
+                                       S.sbeta.as<int32_t>(), c->gstream));
         else
             CK(launch_gather_beta(S.beta8.as<uint8_t>(), S.s.v0, S.saddles32.as<int32_t>(), ns,
-                                  S.sbeta.as<int32_t>(), c->stream));
-        CK(launch_scan_i32(S.sbeta.as<int32_t>(), S.slot_off.as<int64_t>(), ns, c->scratch.p, sb, c->stream));
+                                  S.sbeta.as<int32_t>(), c->gstream));
+        CK(launch_scan_i32(S.sbeta.as<int32_t>(), S.slot_off.as<int64_t>(), ns, c->scratch.p, sb, c->gstream));
         c->stats.kernel_launches += 2;
-        CK(cudaMemcpyAsync(hc, S.slot_off.as<int64_t>() + ns, sizeof(int64_t), cudaMemcpyDeviceToHost, c->stream));
-        CK(cudaStreamSynchronize(c->stream));
+        CK(cudaMemcpyAsync(hc, S.slot_off.as<int64_t>() + ns, sizeof(int64_t), cudaMemcpyDeviceToHost, c->gstream));
+        CK(cudaStreamSynchronize(c->gstream));
         if (early && ns)   // beta0+ is final (the stream was just synchronised)
             CK(cudaMemcpyAsync(c->h_sbeta.p, S.sbeta.p, sizeof(int32_t) * ns, cudaMemcpyDeviceToHost, c->d2h));
         const int64_t nraw = hc[0];
@@ -485,26 +493,26 @@ static eg_status grid_graph(eg_ctx *c, const Problem &P, SlabState &S, bool raw,
                                 S.slot_off.as<int64_t>(), lv, S.tmp_m.as<int32_t>(), S.tmp_mult.as<int32_t>(),
                                 S.n_unique.as<int32_t>(), raw ? S.raw_s.as<int64_t>() : nullptr,
                                 raw ? S.raw_rep.as<int64_t>() : nullptr, raw ? S.raw_m.as<int64_t>() : nullptr,
-                                c->stream));
+                                c->gstream));
         else   // the representatives were stored by classify: no second link computation
             CK(launch_arcs_csr_reps(P.row_ptr, S.rep_buf.as<int32_t>(), S.saddles32.as<int32_t>(),
                                     S.sbeta.as<int32_t>(), ns, S.slot_off.as<int64_t>(), lv, S.tmp_m.as<int32_t>(),
                                     S.tmp_mult.as<int32_t>(), S.n_unique.as<int32_t>(),
                                     raw ? S.raw_s.as<int64_t>() : nullptr, raw ? S.raw_rep.as<int64_t>() : nullptr,
-                                    raw ? S.raw_m.as<int64_t>() : nullptr, c->stream));
+                                    raw ? S.raw_m.as<int64_t>() : nullptr, c->gstream));
         c->stats.kernel_launches += 1;
     }
-    CK(launch_scan_i32(S.n_unique.as<int32_t>(), S.arc_off.as<int64_t>(), ns, c->scratch.p, sb, c->stream));
+    CK(launch_scan_i32(S.n_unique.as<int32_t>(), S.arc_off.as<int64_t>(), ns, c->scratch.p, sb, c->gstream));
     c->stats.kernel_launches += 2;
-    CK(cudaMemcpyAsync(hc, S.arc_off.as<int64_t>() + ns, sizeof(int64_t), cudaMemcpyDeviceToHost, c->stream));
-    CK(cudaStreamSynchronize(c->stream));
+    CK(cudaMemcpyAsync(hc, S.arc_off.as<int64_t>() + ns, sizeof(int64_t), cudaMemcpyDeviceToHost, c->gstream));
+    CK(cudaStreamSynchronize(c->gstream));
     S.n_arc = hc[0];
     CK(S.arc_s.ensure(sizeof(int64_t) * std::max<int64_t>(S.n_arc, 1)));
     CK(S.arc_m.ensure(sizeof(int64_t) * std::max<int64_t>(S.n_arc, 1)));
     CK(S.arc_mult.ensure(sizeof(int32_t) * std::max<int64_t>(S.n_arc, 1)));
     CK(launch_emit_arcs(S.saddles32.as<int32_t>(), ns, fused ? nullptr : S.slot_off.as<int64_t>(), S.arc_off.as<int64_t>(),
                         S.tmp_m.as<int32_t>(), S.tmp_mult.as<int32_t>(), S.n_unique.as<int32_t>(),
-                        S.arc_s.as<int64_t>(), S.arc_m.as<int64_t>(), S.arc_mult.as<int32_t>(), c->stream, stride));
+                        S.arc_s.as<int64_t>(), S.arc_m.as<int64_t>(), S.arc_mult.as<int32_t>(), c->gstream, stride));
     c->stats.kernel_launches += 1;
     return EG_OK;
 }
@@ -556,7 +564,7 @@ static eg_status gather_graph(eg_ctx *c, bool raw) {
     CK(c->h_arc_s.ensure(sizeof(int64_t) * std::max<int64_t>(na, 1)));
     CK(c->h_arc_m.ensure(sizeof(int64_t) * std::max<int64_t>(na, 1)));
     CK(c->h_arc_mult.ensure(sizeof(int32_t) * std::max<int64_t>(na, 1)));
-    cudaStream_t st = c->stream;
+    cudaStream_t st = c->gstream;
     if (c->world == 1) {
         int64_t om = 0, os = 0, oa = 0;
         for (SlabState *S : c->slabs) {
@@ -779,6 +787,18 @@ static eg_status compute_grid(eg_ctx *c, const Problem &P, const float *f, uint3
     }
     c->stats.path = tiled ? 1 : 0;
     CK(cudaEventRecord(c->ev[1], c->stream));
+    const bool raw = (flags & EG_RAW_ARCS) != 0;
+    // One slab on one GPU, plain maximum graph: the graph stage (node lists,
+    // arcs -- which follow a representative's exit pointer themselves -- and
+    // their copies to the host) runs on the aux stream while the labels are
+    // finalised on the ctx stream.  The widening flags keep the serial order.
+    c->overlap = tiled && !multi && c->world == 1 && !c->minimum && !c->bundle &&
+                 !(flags & (EG_ARC_PATHS | EG_NODE_VALUES | EG_RAW_ARCS));
+    c->gstream = c->overlap ? c->aux : c->stream;
+    if (c->overlap) {
+        CK(cudaEventRecord(c->ev_tile, c->stream));
+        CK(cudaStreamWaitEvent(c->aux, c->ev_tile, 0));
+    }
     // ---- cross-slab resolution, then every unresolved owned label
     if (multi) {
         int rounds = 0;
@@ -793,17 +813,17 @@ static eg_status compute_grid(eg_ctx *c, const Problem &P, const float *f, uint3
         c->stats.kernel_launches += 1;
     }
     CK(cudaEventRecord(c->ev[2], c->stream));
-    ST(fail_if_flags(c));
+    if (!c->overlap) ST(fail_if_flags(c));
     c->d_labels = c->label_all.as<int32_t>();
     c->n_own = nlab;
     c->have_labels = true;
-    const bool raw = (flags & EG_RAW_ARCS) != 0;
     // one GPU, one slab, graph wanted: the node lists are copied early
     c->early_d2h =
         c->world == 1 && c->slabs.size() == 1 && !raw && !(flags & EG_NO_GRAPH_D2H) && !c->minimum && !c->bundle;
     for (SlabState *S : c->slabs) ST(grid_graph(c, P, *S, raw, c->early_d2h));
     if (c->early_d2h) CK(cudaEventRecord(c->ev_d2h[2], c->d2h));
-    CK(cudaEventRecord(c->ev[4], c->stream));
+    CK(cudaEventRecord(c->ev[4], c->gstream));
+    if (c->overlap) ST(fail_if_flags(c));     // (syncs the ctx stream: the finalize pass)
     c->raw_valid = raw;
     return EG_OK;
 }
@@ -812,6 +832,8 @@ static eg_status compute_grid(eg_ctx *c, const Problem &P, const float *f, uint3
 
 static eg_status compute_csr(eg_ctx *c, const Problem &P, const float *f, uint32_t flags) {
     const int vparts = int((flags >> 8) & 0xffffff);
+    c->overlap = false;
+    c->gstream = c->stream;
     std::vector<std::pair<int64_t, int64_t>> plan;       // vertex ranges of this process
     std::vector<int64_t> all;                            // every rank's range (multi-GPU)
     if (c->world > 1) {
@@ -1082,6 +1104,10 @@ static eg_status compute_impl(eg_ctx *c, const eg_domain *d, const float *f, uin
         ST(gather_graph(c, (flags & EG_RAW_ARCS) != 0));
         c->graph_on_host = true;
     }
+    if (c->gstream != c->stream) {             // join the graph stage (aux) into the ctx stream
+        CK(cudaEventRecord(c->ev_graph, c->gstream));
+        CK(cudaStreamWaitEvent(c->stream, c->ev_graph, 0));
+    }
     c->node_values = false;
     c->last_minimum = c->minimum;
     if ((flags & EG_NODE_VALUES) && c->world == 1 && c->graph_on_host) {
@@ -1154,10 +1180,16 @@ eg_status eg_create(eg_ctx **out, int cuda_device, void *cuda_stream) {
             delete c;
             return EG_ERR_CUDA;
         }
-    if (cudaStreamCreateWithFlags(&c->d2h, cudaStreamNonBlocking) != cudaSuccess) {
+    if (cudaStreamCreateWithFlags(&c->d2h, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaDeviceGetStreamPriorityRange(&c->prio_lo, &c->prio_hi) != cudaSuccess ||
+        // high priority: the graph stage's few blocks run ahead of the finalize pass's queue
+        cudaStreamCreateWithPriority(&c->aux, cudaStreamNonBlocking, c->prio_hi) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c->ev_tile, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c->ev_graph, cudaEventDisableTiming) != cudaSuccess) {
         delete c;
         return EG_ERR_CUDA;
     }
+    c->gstream = c->stream;
     *out = c;
     return EG_OK;
 }
@@ -1356,6 +1388,12 @@ eg_status eg_destroy(eg_ctx *c) {
         cudaStreamSynchronize(c->d2h);
         cudaStreamDestroy(c->d2h);
     }
+    if (c->aux) {
+        cudaStreamSynchronize(c->aux);
+        cudaStreamDestroy(c->aux);
+    }
+    if (c->ev_tile) cudaEventDestroy(c->ev_tile);
+    if (c->ev_graph) cudaEventDestroy(c->ev_graph);
     for (auto &e : c->ev_d2h)
         if (e) cudaEventDestroy(e);
     if (c->comm) ncclCommDestroy(c->comm);

@@ -67,8 +67,17 @@ struct LabelView {
     int64_t v0, v1;
     const int32_t *lo, *hi;                // halo planes z0 - 1 and z1 (grid, multi-slab) or null
     int64_t plane;
+    // one slab whose labels are still being finalised concurrently: a label
+    // with bit 31 is an exit pointer, followed to the final value (every value
+    // read lies on the same ascending path, so stale reads are harmless)
+    bool chase;
 #ifdef __CUDACC__
     __device__ __forceinline__ int32_t at(int64_t g) const {
+        if (chase) {
+            int32_t w = *(volatile const int32_t *)(own + (g - v0));
+            while (w < 0) w = *(volatile const int32_t *)(own + ((w & 0x7fffffff) - v0));
+            return w;
+        }
         if (g >= v0 && g < v1) return own[g - v0];
         if (g < v0) return lo[g - v0 + plane];
         return hi[g - v1];
