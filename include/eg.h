@@ -152,6 +152,16 @@ eg_status eg_create_dist(eg_ctx **out, int cuda_device, void *cuda_stream, const
  * host memory owned by the ctx (unless EG_NO_GRAPH_D2H). */
 eg_status eg_compute(eg_ctx *ctx, const eg_domain *domain, const float *d_field, uint32_t flags);
 
+/* Other input types (reading L21 in DESIGN.md): every value of
+ * these types is exactly a float32, so the field is converted on the device
+ * (into a buffer owned by the ctx) and the same path runs -- outputs are
+ * identical to eg_compute on the converted values.  d_field: device, `dtype`
+ * elements in the eg_compute layout.  Types without an exact float32 image
+ * (32/64-bit integers, float64) are EG_ERR_UNSUPPORTED. */
+enum { EG_DTYPE_F32 = 0, EG_DTYPE_F16 = 1, EG_DTYPE_BF16 = 2, EG_DTYPE_U8 = 3, EG_DTYPE_I8 = 4, EG_DTYPE_U16 = 5,
+       EG_DTYPE_I16 = 6 };
+eg_status eg_compute_typed(eg_ctx *ctx, const eg_domain *domain, const void *d_field, int dtype, uint32_t flags);
+
 /* Same, end to end from HOST memory: copies h_field to the device (staged
  * through pinned memory owned by the ctx), computes, and -- if h_labels is not
  * NULL -- copies the owned labels back (int32, one per owned vertex). */

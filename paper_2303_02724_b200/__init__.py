@@ -130,13 +130,24 @@ class Context:
     # -------------------------------------------------------------- calls
     def compute(self, field: torch.Tensor, dims: Optional[Sequence[int]] = None, csr=None, flags: int = 0,
                 slab=None, v_range=None, materialize: bool = True) -> Optional[Graph]:
-        """S1..S4 on a device-resident float32 field (flat, axis 0 fastest).
+        """S1..S4 on a device-resident field (flat, axis 0 fastest): float32,
+        or float16 / bfloat16 / (u)int8 / (u)int16, which the library converts
+        exactly to float32 on the device (eg_compute_typed).
         The graph is always copied to host memory owned by the library; with
         materialize=False no numpy copies are made (use graph() later)."""
-        if not (field.is_cuda and field.dtype == torch.float32 and field.is_contiguous()):
-            raise TypeError("field must be a contiguous CUDA float32 tensor")
+        dtypes = {torch.float32: _abi.EG_DTYPE_F32, torch.float16: _abi.EG_DTYPE_F16,
+                  torch.bfloat16: _abi.EG_DTYPE_BF16, torch.uint8: _abi.EG_DTYPE_U8, torch.int8: _abi.EG_DTYPE_I8,
+                  torch.int16: _abi.EG_DTYPE_I16}
+        if hasattr(torch, "uint16"):
+            dtypes[torch.uint16] = _abi.EG_DTYPE_U16
+        if not (field.is_cuda and field.dtype in dtypes and field.is_contiguous()):
+            raise TypeError("field must be a contiguous CUDA tensor of float32, float16, bfloat16, (u)int8 or (u)int16")
         dom = self._domain(dims, csr, slab, v_range)
-        st = _abi.lib().eg_compute(self._h, C.byref(dom), C.c_void_p(field.data_ptr()), flags)
+        if field.dtype == torch.float32:
+            st = _abi.lib().eg_compute(self._h, C.byref(dom), C.c_void_p(field.data_ptr()), flags)
+        else:
+            st = _abi.lib().eg_compute_typed(self._h, C.byref(dom), C.c_void_p(field.data_ptr()),
+                                             dtypes[field.dtype], flags)
         self._check(st, "eg_compute")
         self._last_flags = flags
         return self._graph(flags) if materialize else None

@@ -16,6 +16,7 @@ EG_OK, EG_ERR_INVALID_ARG, EG_ERR_NAN, EG_ERR_OOM, EG_ERR_CUDA, EG_ERR_NCCL, EG_
 STATUS_NAMES = ["EG_OK", "EG_ERR_INVALID_ARG", "EG_ERR_NAN", "EG_ERR_OOM", "EG_ERR_CUDA", "EG_ERR_NCCL",
                 "EG_ERR_STATE", "EG_ERR_UNSUPPORTED"]
 EG_DOMAIN_GRID, EG_DOMAIN_CSR = 0, 1
+EG_DTYPE_F32, EG_DTYPE_F16, EG_DTYPE_BF16, EG_DTYPE_U8, EG_DTYPE_I8, EG_DTYPE_U16, EG_DTYPE_I16 = range(7)
 (EG_CHECK_NAN, EG_RAW_ARCS, EG_CHECK_CSR, EG_FORCE_GENERIC, EG_NO_GRAPH_D2H, EG_MINIMUM, EG_ARC_PATHS,
  EG_BUNDLE, EG_NODE_VALUES) = 1, 2, 4, 8, 16, 32, 64, 128, 256
 
@@ -26,7 +27,7 @@ def EG_VIRTUAL_PARTS(k: int) -> int:
 
 # every symbol include/eg.h declares (checked by tests/test_abi_exports.py)
 EXPORTS = ["eg_create", "eg_nccl_unique_id", "eg_create_dist", "eg_compute", "eg_compute_host", "eg_gradient",
-           "eg_get_graph", "eg_get_raw_arcs", "eg_get_arc_paths", "eg_simplify", "eg_get_labels", "eg_get_stats",
+           "eg_compute_typed", "eg_get_graph", "eg_get_raw_arcs", "eg_get_arc_paths", "eg_simplify", "eg_get_labels", "eg_get_stats",
            "eg_destroy", "eg_last_error"]
 
 
@@ -77,6 +78,7 @@ def lib():
     L.eg_create_dist.argtypes = [C.POINTER(vp), C.c_int, vp, vp, C.c_int, C.c_int]
     L.eg_compute.argtypes = [vp, C.POINTER(EgDomain), vp, u32]
     L.eg_compute_host.argtypes = [vp, C.POINTER(EgDomain), vp, vp, u32]
+    L.eg_compute_typed.argtypes = [vp, C.POINTER(EgDomain), vp, C.c_int, u32]
     L.eg_gradient.argtypes = [vp, C.POINTER(EgDomain), vp, vp, vp]
     L.eg_get_graph.argtypes = [vp, C.POINTER(EgGraph)]
     P64 = C.POINTER(C.c_int64)

@@ -108,6 +108,7 @@ struct eg_ctx {
     DevBuf label_all;                  // labels of every slab of this process
     DevBuf field;                      // eg_compute_host staging target
     DevBuf mirror;                     // EG_MINIMUM: g[i] = -f[N-1-i]
+    DevBuf typed;                      // eg_compute_typed: the field converted to float32
     bool minimum = false;              // the current compute is a minimum graph
     bool bundle = false;               // the current compute bundles arcs (EG_BUNDLE)
     DevBuf bund_scratch;               // arc bundling scratch (keys, indices, scans)
@@ -1227,6 +1228,31 @@ eg_status eg_compute(eg_ctx *c, const eg_domain *d, const float *d_field, uint32
     return compute_impl(c, d, d_field, flags, true);
 }
 
+eg_status eg_compute_typed(eg_ctx *c, const eg_domain *d, const void *d_field, int dtype, uint32_t flags) {
+    if (!c || !d) return EG_ERR_INVALID_ARG;
+    if (dtype == EG_DTYPE_F32) return compute_impl(c, d, static_cast<const float *>(d_field), flags, true);
+    if (dtype < EG_DTYPE_F16 || dtype > EG_DTYPE_I16)
+        return set_err(c, EG_ERR_UNSUPPORTED, "dtype %d has no exact float32 image", dtype);
+    if (c->poisoned) return set_err(c, EG_ERR_STATE, "context is poisoned: %s", c->err.c_str());
+    if (!is_device_ptr(d_field)) return set_err(c, EG_ERR_INVALID_ARG, "d_field must be a device pointer");
+    // the number of elements the domain covers on this rank
+    int64_t n = 0;
+    if (d->kind == EG_DOMAIN_GRID) {
+        const eg_grid &g = d->grid;
+        if (g.ndim < 1 || g.ndim > 8) return set_err(c, EG_ERR_INVALID_ARG, "ndim %d", g.ndim);
+        int64_t plane = 1;
+        for (int i = 0; i + 1 < g.ndim; ++i) plane *= g.dims[i];
+        n = plane * (g.slab_end - g.slab_begin);
+    } else {
+        n = d->csr.n_vertices;
+    }
+    if (n <= 0) return set_err(c, EG_ERR_INVALID_ARG, "empty field");
+    CK(cudaSetDevice(c->device));
+    CK(c->typed.ensure(sizeof(float) * size_t(n)));
+    CK(launch_to_f32(d_field, dtype, c->typed.as<float>(), n, c->stream));
+    return compute_impl(c, d, c->typed.as<float>(), flags, true);
+}
+
 eg_status eg_compute_host(eg_ctx *c, const eg_domain *d, const float *h_field, int32_t *h_labels, uint32_t flags) {
     if (!c) return EG_ERR_INVALID_ARG;
     if (c->poisoned) return set_err(c, EG_ERR_STATE, "context is poisoned: %s", c->err.c_str());
@@ -1373,7 +1399,7 @@ eg_status eg_destroy(eg_ctx *c) {
     cudaSetDevice(c->device);
     cudaStreamSynchronize(c->stream);
     set_slab_count(c, 0);
-    DevBuf *bufs[] = {&c->d_fnode, &c->bund_scratch, &c->b_sad64, &c->b_sad32, &c->b_sbeta, &c->b_nu, &c->b_arc_s, &c->b_arc_m,
+    DevBuf *bufs[] = {&c->typed, &c->d_fnode, &c->bund_scratch, &c->b_sad64, &c->b_sad32, &c->b_sbeta, &c->b_nu, &c->b_arc_s, &c->b_arc_m,
                       &c->b_arc_mult, &c->label_all, &c->field, &c->mirror, &c->path_len, &c->path_off, &c->path_v, &c->flags, &c->counts, &c->scratch, &c->tab, &c->gsend, &c->grecv};
     for (DevBuf *b : bufs) b->release();
     HostBuf *hb[] = {&c->h_fmax, &c->h_fsad, &c->h_maxima, &c->h_saddles, &c->h_sbeta, &c->h_arc_s, &c->h_arc_m, &c->h_arc_mult,

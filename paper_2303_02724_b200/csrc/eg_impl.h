@@ -136,6 +136,8 @@ cudaError_t launch_emit_arcs(const int32_t *saddles, int64_t n_sad, const int64_
                              int64_t *arc_s, int64_t *arc_m, int32_t *arc_mult, cudaStream_t st,
                              int slot_stride = 0);   // slot_off == null: saddle j's slots start at j * slot_stride
 
+// exact conversion of an EG_DTYPE_* field to float32 (reading L21)
+cudaError_t launch_to_f32(const void *in, int dtype, float *out, int64_t n, cudaStream_t st);
 // minimum graph (reading L11): g[i] = -f[n-1-i]; in-place reversal of an id
 // list (entries x -> N-1-x when map_ids) or of a plain array
 cudaError_t launch_reflect_negate(const float *f, float *g, int64_t n, cudaStream_t st);

@@ -2,6 +2,9 @@
 // maxima / saddles (S3 node lists), scans and arc emission (S4).
 #include <algorithm>
 
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+
 #include <cub/cub.cuh>
 #include <thrust/iterator/counting_iterator.h>
 #include <thrust/iterator/transform_iterator.h>
@@ -360,6 +363,37 @@ cudaError_t launch_bundle(const BundleArgs &B, cudaStream_t st) {
     k_bundle_emit<<<nb, 256, 0, st>>>(B.keep, B.s_pos, B.a_pos, B.arc_off, ns, B.sad64, B.sad32, B.sbeta, B.n_unique,
                                       B.arc_s, B.arc_m, B.arc_mult, B.o_sad64, B.o_sad32, B.o_sbeta, B.o_nu,
                                       B.o_arc_s, B.o_arc_m, B.o_arc_mult);
+    return cudaGetLastError();
+}
+
+// ------------------------------------------- exact conversions to float32 (L21)
+template <class T>
+__device__ __forceinline__ float to_f32(T x) { return float(x); }
+template <>
+__device__ __forceinline__ float to_f32<__half>(__half x) { return __half2float(x); }
+template <>
+__device__ __forceinline__ float to_f32<__nv_bfloat16>(__nv_bfloat16 x) { return __bfloat162float(x); }
+
+template <class T>
+__global__ void k_to_f32(const T *__restrict__ in, float *__restrict__ out, int64_t n) {
+    for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
+        out[i] = to_f32(in[i]);
+}
+
+cudaError_t launch_to_f32(const void *in, int dtype, float *out, int64_t n, cudaStream_t st) {
+    if (n <= 0) return cudaSuccess;
+    const unsigned nb = unsigned(std::min<int64_t>((n + 255) / 256, 148 * 16));
+    switch (dtype) {
+        case EG_DTYPE_F16: k_to_f32<__half><<<nb, 256, 0, st>>>(static_cast<const __half *>(in), out, n); break;
+        case EG_DTYPE_BF16:
+            k_to_f32<__nv_bfloat16><<<nb, 256, 0, st>>>(static_cast<const __nv_bfloat16 *>(in), out, n);
+            break;
+        case EG_DTYPE_U8: k_to_f32<uint8_t><<<nb, 256, 0, st>>>(static_cast<const uint8_t *>(in), out, n); break;
+        case EG_DTYPE_I8: k_to_f32<int8_t><<<nb, 256, 0, st>>>(static_cast<const int8_t *>(in), out, n); break;
+        case EG_DTYPE_U16: k_to_f32<uint16_t><<<nb, 256, 0, st>>>(static_cast<const uint16_t *>(in), out, n); break;
+        case EG_DTYPE_I16: k_to_f32<int16_t><<<nb, 256, 0, st>>>(static_cast<const int16_t *>(in), out, n); break;
+        default: return cudaErrorInvalidValue;
+    }
     return cudaGetLastError();
 }
 

@@ -419,3 +419,25 @@ def test_simplify_csr_and_state(eg, ctx):
     ctx.compute(torch.from_numpy(f).cuda(), csr=(torch.from_numpy(rp).cuda(), torch.from_numpy(ci).cuda()))
     with pytest.raises(Exception):
         ctx.simplify(0.5)                   # the last compute kept no node values
+
+
+@pytest.mark.parametrize("tdtype", ["float16", "bfloat16", "uint8", "int8", "int16", "uint16"])
+@pytest.mark.parametrize("dims", [[64, 48], [40, 33, 29]])
+def test_other_dtypes(eg, ctx, tdtype, dims):
+    """eg_compute_typed (reading L21): exact float32 images -> identical graphs."""
+    import torch
+    if not hasattr(torch, tdtype):
+        pytest.skip(f"torch has no {tdtype}")
+    dt = getattr(torch, tdtype)
+    rng = np.random.default_rng(len(dims) * 7 + len(tdtype))
+    N = int(np.prod(dims))
+    if dt.is_floating_point:
+        t = torch.from_numpy(rng.standard_normal(N).astype(np.float32)).to(dt)
+    else:
+        info = torch.iinfo(dt)
+        lo, hi = max(info.min, -300), min(info.max, 300)     # ties on purpose
+        t = torch.from_numpy(rng.integers(lo, hi + 1, N)).to(dt)
+    f = t.to(torch.float32).numpy()                           # the exact float32 image
+    o = O.grid(f, dims)
+    g = ctx.compute(t.cuda(), dims=dims, flags=eg.EG_CHECK_NAN)
+    assert_graph_equal(g, o, what=f"{tdtype} {dims}")
