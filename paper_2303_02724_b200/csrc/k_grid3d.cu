@@ -431,7 +431,8 @@ __global__ void __launch_bounds__(kThreads, 2)
     // so nothing needs settling, and chains that run into a finished cell end
     // one hop later.
     uint8_t *used = reinterpret_cast<uint8_t *>(fbox);
-    for (int i = tid; i < 2 * PBOX / 16; i += kThreads) reinterpret_cast<uint4 *>(used)[i] = make_uint4(0, 0, 0, 0);
+    if (!A.no_elist)   // exit marks are only read back when the tile appends to E
+        for (int i = tid; i < 2 * PBOX / 16; i += kThreads) reinterpret_cast<uint4 *>(used)[i] = make_uint4(0, 0, 0, 0);
 #pragma unroll 1
     for (int round = 0; round < A.rounds; ++round) {
 #pragma unroll
