@@ -152,14 +152,22 @@ eg_status eg_create_dist(eg_ctx **out, int cuda_device, void *cuda_stream, const
  * host memory owned by the ctx (unless EG_NO_GRAPH_D2H). */
 eg_status eg_compute(eg_ctx *ctx, const eg_domain *domain, const float *d_field, uint32_t flags);
 
-/* Other input types (reading L21 in DESIGN.md): every value of
- * these types is exactly a float32, so the field is converted on the device
- * (into a buffer owned by the ctx) and the same path runs -- outputs are
- * identical to eg_compute on the converted values.  d_field: device, `dtype`
- * elements in the eg_compute layout.  Types without an exact float32 image
- * (32/64-bit integers, float64) are EG_ERR_UNSUPPORTED. */
+/* Other input types (readings L21/L22 in DESIGN.md).
+ * F16, BF16, (U)INT8, (U)INT16: every value is exactly a float32, so the field
+ * is converted on the device (into a buffer owned by the ctx) and the same
+ * path runs -- outputs are identical to eg_compute on the converted values.
+ * F64, (U)INT32, (U)INT64: the field is replaced on the device by its SoS-rank
+ * image (rank of each vertex under value-then-index order, a stable radix
+ * sort); the extremum graph depends on the field only through that order
+ * (P:142-151), so outputs are exactly those of the type's own order, with no
+ * rounding.  Rank types need one GPU and a whole domain (world size 1,
+ * N < 2^31 - 2^24), are EG_ERR_UNSUPPORTED with EG_NODE_VALUES (the values at
+ * the nodes have no float32 image), and use 2 x (key + 4) bytes per vertex of
+ * ctx-owned scratch.  NaN (F64) is EG_ERR_NAN as for F32.  d_field: device,
+ * `dtype` elements in the eg_compute layout. */
 enum { EG_DTYPE_F32 = 0, EG_DTYPE_F16 = 1, EG_DTYPE_BF16 = 2, EG_DTYPE_U8 = 3, EG_DTYPE_I8 = 4, EG_DTYPE_U16 = 5,
-       EG_DTYPE_I16 = 6 };
+       EG_DTYPE_I16 = 6, EG_DTYPE_F64 = 7, EG_DTYPE_I32 = 8, EG_DTYPE_U32 = 9, EG_DTYPE_I64 = 10,
+       EG_DTYPE_U64 = 11 };
 eg_status eg_compute_typed(eg_ctx *ctx, const eg_domain *domain, const void *d_field, int dtype, uint32_t flags);
 
 /* Same, end to end from HOST memory: copies h_field to the device (staged

@@ -130,18 +130,24 @@ class Context:
     # -------------------------------------------------------------- calls
     def compute(self, field: torch.Tensor, dims: Optional[Sequence[int]] = None, csr=None, flags: int = 0,
                 slab=None, v_range=None, materialize: bool = True) -> Optional[Graph]:
-        """S1..S4 on a device-resident field (flat, axis 0 fastest): float32,
-        or float16 / bfloat16 / (u)int8 / (u)int16, which the library converts
-        exactly to float32 on the device (eg_compute_typed).
+        """S1..S4 on a device-resident field (flat, axis 0 fastest): float32;
+        float16 / bfloat16 / (u)int8 / (u)int16, which the library converts
+        exactly to float32 on the device; or float64 / (u)int32 / (u)int64,
+        which it replaces by the field's SoS-rank image (one GPU, no
+        EG_NODE_VALUES) -- both through eg_compute_typed.
         The graph is always copied to host memory owned by the library; with
         materialize=False no numpy copies are made (use graph() later)."""
         dtypes = {torch.float32: _abi.EG_DTYPE_F32, torch.float16: _abi.EG_DTYPE_F16,
                   torch.bfloat16: _abi.EG_DTYPE_BF16, torch.uint8: _abi.EG_DTYPE_U8, torch.int8: _abi.EG_DTYPE_I8,
-                  torch.int16: _abi.EG_DTYPE_I16}
-        if hasattr(torch, "uint16"):
-            dtypes[torch.uint16] = _abi.EG_DTYPE_U16
+                  torch.int16: _abi.EG_DTYPE_I16, torch.float64: _abi.EG_DTYPE_F64, torch.int32: _abi.EG_DTYPE_I32,
+                  torch.int64: _abi.EG_DTYPE_I64}
+        for name, code in (("uint16", _abi.EG_DTYPE_U16), ("uint32", _abi.EG_DTYPE_U32),
+                           ("uint64", _abi.EG_DTYPE_U64)):
+            if hasattr(torch, name):
+                dtypes[getattr(torch, name)] = code
         if not (field.is_cuda and field.dtype in dtypes and field.is_contiguous()):
-            raise TypeError("field must be a contiguous CUDA tensor of float32, float16, bfloat16, (u)int8 or (u)int16")
+            raise TypeError("field must be a contiguous CUDA tensor of float32/64, float16, bfloat16 or an "
+                            "8/16/32/64-bit integer type")
         dom = self._domain(dims, csr, slab, v_range)
         if field.dtype == torch.float32:
             st = _abi.lib().eg_compute(self._h, C.byref(dom), C.c_void_p(field.data_ptr()), flags)

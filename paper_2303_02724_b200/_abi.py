@@ -16,7 +16,8 @@ EG_OK, EG_ERR_INVALID_ARG, EG_ERR_NAN, EG_ERR_OOM, EG_ERR_CUDA, EG_ERR_NCCL, EG_
 STATUS_NAMES = ["EG_OK", "EG_ERR_INVALID_ARG", "EG_ERR_NAN", "EG_ERR_OOM", "EG_ERR_CUDA", "EG_ERR_NCCL",
                 "EG_ERR_STATE", "EG_ERR_UNSUPPORTED"]
 EG_DOMAIN_GRID, EG_DOMAIN_CSR = 0, 1
-EG_DTYPE_F32, EG_DTYPE_F16, EG_DTYPE_BF16, EG_DTYPE_U8, EG_DTYPE_I8, EG_DTYPE_U16, EG_DTYPE_I16 = range(7)
+(EG_DTYPE_F32, EG_DTYPE_F16, EG_DTYPE_BF16, EG_DTYPE_U8, EG_DTYPE_I8, EG_DTYPE_U16, EG_DTYPE_I16, EG_DTYPE_F64,
+ EG_DTYPE_I32, EG_DTYPE_U32, EG_DTYPE_I64, EG_DTYPE_U64) = range(12)
 (EG_CHECK_NAN, EG_RAW_ARCS, EG_CHECK_CSR, EG_FORCE_GENERIC, EG_NO_GRAPH_D2H, EG_MINIMUM, EG_ARC_PATHS,
  EG_BUNDLE, EG_NODE_VALUES) = 1, 2, 4, 8, 16, 32, 64, 128, 256
 

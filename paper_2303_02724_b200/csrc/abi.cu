@@ -109,6 +109,7 @@ struct eg_ctx {
     DevBuf field;                      // eg_compute_host staging target
     DevBuf mirror;                     // EG_MINIMUM: g[i] = -f[N-1-i]
     DevBuf typed;                      // eg_compute_typed: the field converted to float32
+    DevBuf rank_scratch;               // eg_compute_typed, rank types: sort keys / indices / cub scratch
     bool minimum = false;              // the current compute is a minimum graph
     bool bundle = false;               // the current compute bundles arcs (EG_BUNDLE)
     DevBuf bund_scratch;               // arc bundling scratch (keys, indices, scans)
@@ -1231,8 +1232,12 @@ eg_status eg_compute(eg_ctx *c, const eg_domain *d, const float *d_field, uint32
 eg_status eg_compute_typed(eg_ctx *c, const eg_domain *d, const void *d_field, int dtype, uint32_t flags) {
     if (!c || !d) return EG_ERR_INVALID_ARG;
     if (dtype == EG_DTYPE_F32) return compute_impl(c, d, static_cast<const float *>(d_field), flags, true);
-    if (dtype < EG_DTYPE_F16 || dtype > EG_DTYPE_I16)
-        return set_err(c, EG_ERR_UNSUPPORTED, "dtype %d has no exact float32 image", dtype);
+    if (dtype < EG_DTYPE_F16 || dtype > EG_DTYPE_U64) return set_err(c, EG_ERR_INVALID_ARG, "dtype %d", dtype);
+    const bool rank = dtype >= EG_DTYPE_F64;   // SoS-rank image (reading L22)
+    if (rank && c->world != 1)
+        return set_err(c, EG_ERR_UNSUPPORTED, "dtype %d: the rank image needs the whole field on one GPU", dtype);
+    if (rank && (flags & EG_NODE_VALUES))
+        return set_err(c, EG_ERR_UNSUPPORTED, "dtype %d: node values have no float32 image", dtype);
     if (c->poisoned) return set_err(c, EG_ERR_STATE, "context is poisoned: %s", c->err.c_str());
     if (!is_device_ptr(d_field)) return set_err(c, EG_ERR_INVALID_ARG, "d_field must be a device pointer");
     // the number of elements the domain covers on this rank
@@ -1249,7 +1254,15 @@ eg_status eg_compute_typed(eg_ctx *c, const eg_domain *d, const void *d_field, i
     if (n <= 0) return set_err(c, EG_ERR_INVALID_ARG, "empty field");
     CK(cudaSetDevice(c->device));
     CK(c->typed.ensure(sizeof(float) * size_t(n)));
-    CK(launch_to_f32(d_field, dtype, c->typed.as<float>(), n, c->stream));
+    if (rank) {
+        if (n > kRankMaxN) return set_err(c, EG_ERR_UNSUPPORTED, "rank image: N = %lld too large", (long long)n);
+        size_t bytes = 0;
+        CK(launch_rank_f32(d_field, dtype, nullptr, n, nullptr, &bytes, c->stream));
+        CK(c->rank_scratch.ensure(bytes));
+        CK(launch_rank_f32(d_field, dtype, c->typed.as<float>(), n, c->rank_scratch.p, &bytes, c->stream));
+    } else {
+        CK(launch_to_f32(d_field, dtype, c->typed.as<float>(), n, c->stream));
+    }
     return compute_impl(c, d, c->typed.as<float>(), flags, true);
 }
 
@@ -1399,7 +1412,7 @@ eg_status eg_destroy(eg_ctx *c) {
     cudaSetDevice(c->device);
     cudaStreamSynchronize(c->stream);
     set_slab_count(c, 0);
-    DevBuf *bufs[] = {&c->typed, &c->d_fnode, &c->bund_scratch, &c->b_sad64, &c->b_sad32, &c->b_sbeta, &c->b_nu, &c->b_arc_s, &c->b_arc_m,
+    DevBuf *bufs[] = {&c->typed, &c->rank_scratch, &c->d_fnode, &c->bund_scratch, &c->b_sad64, &c->b_sad32, &c->b_sbeta, &c->b_nu, &c->b_arc_s, &c->b_arc_m,
                       &c->b_arc_mult, &c->label_all, &c->field, &c->mirror, &c->path_len, &c->path_off, &c->path_v, &c->flags, &c->counts, &c->scratch, &c->tab, &c->gsend, &c->grecv};
     for (DevBuf *b : bufs) b->release();
     HostBuf *hb[] = {&c->h_fmax, &c->h_fsad, &c->h_maxima, &c->h_saddles, &c->h_sbeta, &c->h_arc_s, &c->h_arc_m, &c->h_arc_mult,

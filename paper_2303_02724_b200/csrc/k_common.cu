@@ -397,6 +397,111 @@ cudaError_t launch_to_f32(const void *in, int dtype, float *out, int64_t n, cuda
     return cudaGetLastError();
 }
 
+// ----------------------------- SoS-rank image of a wider type (reading L22)
+// The method only ever compares values under the SoS order (a
+// total order with ties broken by the vertex index), so a field and the
+// permutation that ranks its vertices in that order have the same extremum
+// graph.  A stable radix sort of order-preserving unsigned keys (the index
+// order survives among equal keys) gives the rank p of every vertex; its
+// float image is the normal float with bit pattern p + 2^23, a strictly
+// increasing map on [0, 2^31 - 2^24 - 2^23), so every comparison downstream
+// is exact and free of ties.  NaN inputs become NaN (the path flags them).
+template <class T>
+struct OrderKey;
+template <>
+struct OrderKey<double> {
+    using K = uint64_t;
+    __device__ static K key(double x) {
+        const uint64_t b = uint64_t(__double_as_longlong(x));
+        return (b >> 63) ? ~b : (b | (uint64_t(1) << 63));
+    }
+    __device__ static bool nan(double x) { return x != x; }
+};
+template <>
+struct OrderKey<int32_t> {
+    using K = uint32_t;
+    __device__ static K key(int32_t x) { return uint32_t(x) ^ 0x80000000u; }
+    __device__ static bool nan(int32_t) { return false; }
+};
+template <>
+struct OrderKey<uint32_t> {
+    using K = uint32_t;
+    __device__ static K key(uint32_t x) { return x; }
+    __device__ static bool nan(uint32_t) { return false; }
+};
+template <>
+struct OrderKey<int64_t> {
+    using K = uint64_t;
+    __device__ static K key(int64_t x) { return uint64_t(x) ^ (uint64_t(1) << 63); }
+    __device__ static bool nan(int64_t) { return false; }
+};
+template <>
+struct OrderKey<uint64_t> {
+    using K = uint64_t;
+    __device__ static K key(uint64_t x) { return x; }
+    __device__ static bool nan(uint64_t) { return false; }
+};
+
+template <class T>
+__global__ void k_rank_keys(const T *__restrict__ in, typename OrderKey<T>::K *__restrict__ key,
+                            int32_t *__restrict__ idx, int64_t n) {
+    for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
+        key[i] = OrderKey<T>::key(in[i]);
+        idx[i] = int32_t(i);
+    }
+}
+
+template <class T>
+__global__ void k_rank_scatter(const T *__restrict__ in, const int32_t *__restrict__ idx, float *__restrict__ out,
+                               int64_t n) {
+    for (int64_t p = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; p < n; p += int64_t(gridDim.x) * blockDim.x) {
+        const int32_t v = idx[p];
+        out[v] = OrderKey<T>::nan(in[v]) ? __int_as_float(0x7fc00000) : __int_as_float(int32_t(p) + (1 << 23));
+    }
+}
+
+template <class T>
+static cudaError_t rank_typed(const T *in, float *out, int64_t n, void *scratch, size_t *bytes, cudaStream_t st) {
+    using K = typename OrderKey<T>::K;
+    auto al = [](size_t b) { return (b + 255) & ~size_t(255); };
+    const size_t kb = al(sizeof(K) * size_t(n)), ib = al(sizeof(int32_t) * size_t(n));
+    size_t sort_bytes = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, sort_bytes, (const K *)nullptr, (K *)nullptr, (const int32_t *)nullptr,
+                                    (int32_t *)nullptr, int(n));
+    const size_t need = 2 * kb + 2 * ib + al(sort_bytes);
+    if (!scratch) {
+        *bytes = need;
+        return cudaSuccess;
+    }
+    if (*bytes < need) return cudaErrorInvalidValue;
+    char *p = static_cast<char *>(scratch);
+    K *k0 = reinterpret_cast<K *>(p), *k1 = reinterpret_cast<K *>(p + kb);
+    int32_t *i0 = reinterpret_cast<int32_t *>(p + 2 * kb), *i1 = reinterpret_cast<int32_t *>(p + 2 * kb + ib);
+    void *tmp = p + 2 * kb + 2 * ib;
+    const unsigned nb = unsigned(std::min<int64_t>((n + 255) / 256, 148 * 16));
+    k_rank_keys<T><<<nb, 256, 0, st>>>(in, k0, i0, n);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    size_t tb = sort_bytes;
+    e = cub::DeviceRadixSort::SortPairs(tmp, tb, k0, k1, i0, i1, int(n), 0, int(sizeof(K) * 8), st);
+    if (e != cudaSuccess) return e;
+    k_rank_scatter<T><<<nb, 256, 0, st>>>(in, i1, out, n);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_rank_f32(const void *in, int dtype, float *out, int64_t n, void *scratch, size_t *bytes,
+                            cudaStream_t st) {
+    if (n <= 0 || n > kRankMaxN) return cudaErrorInvalidValue;
+    switch (dtype) {
+        case EG_DTYPE_F64: return rank_typed(static_cast<const double *>(in), out, n, scratch, bytes, st);
+        case EG_DTYPE_I32: return rank_typed(static_cast<const int32_t *>(in), out, n, scratch, bytes, st);
+        case EG_DTYPE_U32: return rank_typed(static_cast<const uint32_t *>(in), out, n, scratch, bytes, st);
+        case EG_DTYPE_I64: return rank_typed(static_cast<const int64_t *>(in), out, n, scratch, bytes, st);
+        case EG_DTYPE_U64: return rank_typed(static_cast<const uint64_t *>(in), out, n, scratch, bytes, st);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
 // ------------------------------------------------- minimum graph (reading L11)
 // The minimum graph of f is the maximum graph of g[i] = -f[N-1-i]: the point
 // reflection x -> dims-1-x maps the Freudenthal grid onto itself and reverses

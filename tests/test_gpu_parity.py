@@ -441,3 +441,70 @@ def test_other_dtypes(eg, ctx, tdtype, dims):
     o = O.grid(f, dims)
     g = ctx.compute(t.cuda(), dims=dims, flags=eg.EG_CHECK_NAN)
     assert_graph_equal(g, o, what=f"{tdtype} {dims}")
+
+
+def _rank_image(x):
+    """SoS rank of every vertex (value, then index) as float32 -- exact for the
+    test sizes; the extremum graph depends on the field only through this
+    order (SURVEY 8(c) order invariance, pinned in
+    test_oracle_pins.py)."""
+    r = np.empty(len(x), dtype=np.int64)
+    r[np.argsort(x, kind="stable")] = np.arange(len(x))
+    return r.astype(np.float32)
+
+
+def _wide_field(tdtype, N, rng):
+    """Values f32 cannot tell apart, plus exact ties."""
+    if tdtype == "float64":
+        x = 1.0 + 1e-12 * rng.standard_normal(N)
+    elif tdtype == "int32":
+        x = rng.integers(-100, 100, N) * 16777259 + rng.integers(0, 3, N)
+    elif tdtype == "uint32":
+        x = (np.uint64(0xFFFFFF00) + rng.integers(0, 200, N).astype(np.uint64)).astype(np.uint32)
+    elif tdtype == "int64":
+        x = (rng.integers(-50, 50, N) << 40) + rng.integers(0, 3, N)
+    else:
+        x = (np.uint64(1) << np.uint64(63)) + rng.integers(0, 40, N).astype(np.uint64) * np.uint64(1 << 20)
+    x = np.asarray(x).astype(getattr(np, tdtype))
+    x[rng.integers(0, N, N // 8)] = x[rng.integers(0, N, N // 8)]      # exact ties
+    return x
+
+
+@pytest.mark.parametrize("tdtype", ["float64", "int32", "uint32", "int64", "uint64"])
+@pytest.mark.parametrize("dims,path", [([64, 48], 0), ([40, 33, 29], 0), ([40, 33, 29], "generic")])
+def test_rank_dtypes(eg, ctx, tdtype, dims, path):
+    """eg_compute_typed, types without an exact float32 image (reading L22):
+    the graph is that of the type's own order -- the oracle run on the rank
+    image -- where a float32 cast would merge values."""
+    import torch
+    if not hasattr(torch, tdtype):
+        pytest.skip(f"torch has no {tdtype}")
+    rng = np.random.default_rng(len(dims) * 11 + len(tdtype))
+    N = int(np.prod(dims))
+    x = _wide_field(tdtype, N, rng)
+    assert len(np.unique(x.astype(np.float32))) < len(np.unique(x))   # the cast would lose order
+    try:
+        t = torch.from_numpy(x).cuda()
+    except (TypeError, RuntimeError) as e:
+        pytest.skip(f"torch cannot move {tdtype} to the device: {e}")
+    fr = _rank_image(x)
+    for minimum in (False, True):
+        o = O.grid(fr, dims, minimum=minimum)
+        g = ctx.compute(t, dims=dims, flags=_flags(eg, path, eg.EG_CHECK_NAN | (eg.EG_MINIMUM if minimum else 0)))
+        assert_graph_equal(g, o, what=f"{tdtype} {dims} {path} minimum={minimum}")
+
+
+def test_rank_dtype_errors(eg, ctx):
+    """float64 NaN -> EG_ERR_NAN; EG_NODE_VALUES with a rank type -> unsupported."""
+    import torch
+    x = np.linspace(0.0, 1.0, 64 * 48)
+    x[100] = np.nan
+    with pytest.raises(eg.EgError) as e:
+        ctx.compute(torch.from_numpy(x).cuda(), dims=[64, 48], flags=eg.EG_CHECK_NAN)
+    assert e.value.status == 2
+    with pytest.raises(eg.EgError) as e:
+        ctx.compute(torch.from_numpy(np.arange(64 * 48, dtype=np.int64)).cuda(), dims=[64, 48],
+                    flags=eg.EG_NODE_VALUES)
+    assert e.value.status == 7
+    g = ctx.compute(torch.from_numpy(np.arange(64 * 48, dtype=np.int64)).cuda(), dims=[64, 48])
+    assert list(g.maxima) == [64 * 48 - 1] and len(g.saddles) == 0      # context still usable
