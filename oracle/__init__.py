@@ -164,7 +164,12 @@ def grid(f: np.ndarray, dims, minimum: bool = False) -> Graph:
     return _take(res)
 
 
-def csr(f: np.ndarray, row_ptr: np.ndarray, col_idx: np.ndarray) -> Graph:
+def csr(f: np.ndarray, row_ptr: np.ndarray, col_idx: np.ndarray, minimum: bool = False) -> Graph:
+    """Extremum graph of a float32 field on a CSR graph; minimum=True: the
+    minimum graph (O10)."""
+    if minimum:
+        with reversed_order():
+            return csr(f, row_ptr, col_idx)
     f = np.ascontiguousarray(f, dtype=np.float32)
     rp = np.ascontiguousarray(row_ptr, dtype=np.int64)
     ci = np.ascontiguousarray(col_idx, dtype=np.int32)

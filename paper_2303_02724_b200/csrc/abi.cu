@@ -1037,12 +1037,27 @@ static eg_status compute_impl(eg_ctx *c, const eg_domain *d, const float *f, uin
     // back by i -> N-1-i (k_common.cu)
     const float *f_user = f;           // the caller's field (device) -- f becomes the mirror for a minimum graph
     c->minimum = (flags & EG_MINIMUM) != 0;
+    // On a CSR graph (no reflection maps it onto itself) the maximum graph of
+    // the field's reversed SoS-rank image (reading L22) is the minimum graph,
+    // with vertex ids unchanged.
     if (c->minimum) {
-        if (!P.grid || c->world > 1 || ((flags >> 8) & 0xffffff) > 1 || (flags & EG_RAW_ARCS))
-            return set_err(c, EG_ERR_UNSUPPORTED, "EG_MINIMUM: grids on one GPU and one slab, without raw arcs");
+        if (c->world > 1 || ((flags >> 8) & 0xffffff) > 1 || (flags & EG_RAW_ARCS))
+            return set_err(c, EG_ERR_UNSUPPORTED, "EG_MINIMUM: one GPU and one slab, without raw arcs");
+        if (!P.grid && (P.v0 != 0 || P.v1 != P.N))
+            return set_err(c, EG_ERR_UNSUPPORTED, "EG_MINIMUM on a CSR graph: the whole vertex range");
         CK(c->mirror.ensure(sizeof(float) * std::max<int64_t>(P.N, 1)));
-        CK(launch_reflect_negate(f, c->mirror.as<float>(), P.N, c->stream));
-        c->stats.kernel_launches += 1;
+        if (P.grid) {
+            CK(launch_reflect_negate(f, c->mirror.as<float>(), P.N, c->stream));
+            c->stats.kernel_launches += 1;
+        } else {
+            if (P.N > kRankMaxN) return set_err(c, EG_ERR_UNSUPPORTED, "EG_MINIMUM on a CSR graph: N too large");
+            size_t bytes = 0;
+            CK(launch_rank_f32(f, EG_DTYPE_F32, nullptr, P.N, nullptr, &bytes, true, c->stream));
+            CK(c->rank_scratch.ensure(bytes));
+            CK(launch_rank_f32(f, EG_DTYPE_F32, c->mirror.as<float>(), P.N, c->rank_scratch.p, &bytes, true,
+                               c->stream));
+            c->stats.kernel_launches += 2 + 4;   // keys, scatter + the radix sort's passes (approx.)
+        }
         f = c->mirror.as<float>();
     }
     c->paths_valid = false;
@@ -1089,7 +1104,7 @@ static eg_status compute_impl(eg_ctx *c, const eg_domain *d, const float *f, uin
         c->paths_valid = true;
     }
     if (c->bundle) ST(bundle_arcs(c));
-    if (c->minimum) {
+    if (c->minimum && P.grid) {
         SlabState &S = *c->slabs[0];
         const int64_t N = P.N;
         CK(launch_reverse_i32(c->label_all.as<int32_t>(), N, N, true, c->stream));
@@ -1257,9 +1272,9 @@ eg_status eg_compute_typed(eg_ctx *c, const eg_domain *d, const void *d_field, i
     if (rank) {
         if (n > kRankMaxN) return set_err(c, EG_ERR_UNSUPPORTED, "rank image: N = %lld too large", (long long)n);
         size_t bytes = 0;
-        CK(launch_rank_f32(d_field, dtype, nullptr, n, nullptr, &bytes, c->stream));
+        CK(launch_rank_f32(d_field, dtype, nullptr, n, nullptr, &bytes, false, c->stream));
         CK(c->rank_scratch.ensure(bytes));
-        CK(launch_rank_f32(d_field, dtype, c->typed.as<float>(), n, c->rank_scratch.p, &bytes, c->stream));
+        CK(launch_rank_f32(d_field, dtype, c->typed.as<float>(), n, c->rank_scratch.p, &bytes, false, c->stream));
     } else {
         CK(launch_to_f32(d_field, dtype, c->typed.as<float>(), n, c->stream));
     }

@@ -138,11 +138,12 @@ cudaError_t launch_emit_arcs(const int32_t *saddles, int64_t n_sad, const int64_
 
 // exact conversion of an EG_DTYPE_* field to float32 (reading L21)
 cudaError_t launch_to_f32(const void *in, int dtype, float *out, int64_t n, cudaStream_t st);
-// SoS-rank image of a field of a wider type (reading L22): out[v] = the float
-// with bit pattern rank(v) + 2^23.  scratch == null: *bytes = the scratch size.
+// SoS-rank image of a field (reading L22; F32 too): out[v] = the float with bit
+// pattern rank(v) + 2^23 (reverse: N-1-rank(v), the reversed order of L11).
+// scratch == null: *bytes = the scratch size.
 constexpr int64_t kRankMaxN = 0x7F000000;
 cudaError_t launch_rank_f32(const void *in, int dtype, float *out, int64_t n, void *scratch, size_t *bytes,
-                            cudaStream_t st);
+                            bool reverse, cudaStream_t st);
 // minimum graph (reading L11): g[i] = -f[n-1-i]; in-place reversal of an id
 // list (entries x -> N-1-x when map_ids) or of a plain array
 cudaError_t launch_reflect_negate(const float *f, float *g, int64_t n, cudaStream_t st);

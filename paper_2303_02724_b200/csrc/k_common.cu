@@ -406,13 +406,25 @@ cudaError_t launch_to_f32(const void *in, int dtype, float *out, int64_t n, cuda
 // float image is the normal float with bit pattern p + 2^23, a strictly
 // increasing map on [0, 2^31 - 2^24 - 2^23), so every comparison downstream
 // is exact and free of ties.  NaN inputs become NaN (the path flags them).
+// reverse: rank N-1-p instead -- the reversed total order of reading L11,
+// whose maximum graph is the minimum graph of the input.
+// (IEEE: -0 == +0, so both map to the key of +0 and tie by index.)
 template <class T>
 struct OrderKey;
+template <>
+struct OrderKey<float> {
+    using K = uint32_t;
+    __device__ static K key(float x) {
+        const uint32_t b = uint32_t(__float_as_int(x == 0.0f ? 0.0f : x));
+        return (b >> 31) ? ~b : (b | 0x80000000u);
+    }
+    __device__ static bool nan(float x) { return x != x; }
+};
 template <>
 struct OrderKey<double> {
     using K = uint64_t;
     __device__ static K key(double x) {
-        const uint64_t b = uint64_t(__double_as_longlong(x));
+        const uint64_t b = uint64_t(__double_as_longlong(x == 0.0 ? 0.0 : x));
         return (b >> 63) ? ~b : (b | (uint64_t(1) << 63));
     }
     __device__ static bool nan(double x) { return x != x; }
@@ -453,15 +465,17 @@ __global__ void k_rank_keys(const T *__restrict__ in, typename OrderKey<T>::K *_
 
 template <class T>
 __global__ void k_rank_scatter(const T *__restrict__ in, const int32_t *__restrict__ idx, float *__restrict__ out,
-                               int64_t n) {
+                               int64_t n, bool reverse) {
     for (int64_t p = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; p < n; p += int64_t(gridDim.x) * blockDim.x) {
         const int32_t v = idx[p];
-        out[v] = OrderKey<T>::nan(in[v]) ? __int_as_float(0x7fc00000) : __int_as_float(int32_t(p) + (1 << 23));
+        const int32_t r = int32_t(reverse ? n - 1 - p : p);
+        out[v] = OrderKey<T>::nan(in[v]) ? __int_as_float(0x7fc00000) : __int_as_float(r + (1 << 23));
     }
 }
 
 template <class T>
-static cudaError_t rank_typed(const T *in, float *out, int64_t n, void *scratch, size_t *bytes, cudaStream_t st) {
+static cudaError_t rank_typed(const T *in, float *out, int64_t n, void *scratch, size_t *bytes, bool reverse,
+                              cudaStream_t st) {
     using K = typename OrderKey<T>::K;
     auto al = [](size_t b) { return (b + 255) & ~size_t(255); };
     const size_t kb = al(sizeof(K) * size_t(n)), ib = al(sizeof(int32_t) * size_t(n));
@@ -485,19 +499,20 @@ static cudaError_t rank_typed(const T *in, float *out, int64_t n, void *scratch,
     size_t tb = sort_bytes;
     e = cub::DeviceRadixSort::SortPairs(tmp, tb, k0, k1, i0, i1, int(n), 0, int(sizeof(K) * 8), st);
     if (e != cudaSuccess) return e;
-    k_rank_scatter<T><<<nb, 256, 0, st>>>(in, i1, out, n);
+    k_rank_scatter<T><<<nb, 256, 0, st>>>(in, i1, out, n, reverse);
     return cudaGetLastError();
 }
 
 cudaError_t launch_rank_f32(const void *in, int dtype, float *out, int64_t n, void *scratch, size_t *bytes,
-                            cudaStream_t st) {
+                            bool reverse, cudaStream_t st) {
     if (n <= 0 || n > kRankMaxN) return cudaErrorInvalidValue;
     switch (dtype) {
-        case EG_DTYPE_F64: return rank_typed(static_cast<const double *>(in), out, n, scratch, bytes, st);
-        case EG_DTYPE_I32: return rank_typed(static_cast<const int32_t *>(in), out, n, scratch, bytes, st);
-        case EG_DTYPE_U32: return rank_typed(static_cast<const uint32_t *>(in), out, n, scratch, bytes, st);
-        case EG_DTYPE_I64: return rank_typed(static_cast<const int64_t *>(in), out, n, scratch, bytes, st);
-        case EG_DTYPE_U64: return rank_typed(static_cast<const uint64_t *>(in), out, n, scratch, bytes, st);
+        case EG_DTYPE_F32: return rank_typed(static_cast<const float *>(in), out, n, scratch, bytes, reverse, st);
+        case EG_DTYPE_F64: return rank_typed(static_cast<const double *>(in), out, n, scratch, bytes, reverse, st);
+        case EG_DTYPE_I32: return rank_typed(static_cast<const int32_t *>(in), out, n, scratch, bytes, reverse, st);
+        case EG_DTYPE_U32: return rank_typed(static_cast<const uint32_t *>(in), out, n, scratch, bytes, reverse, st);
+        case EG_DTYPE_I64: return rank_typed(static_cast<const int64_t *>(in), out, n, scratch, bytes, reverse, st);
+        case EG_DTYPE_U64: return rank_typed(static_cast<const uint64_t *>(in), out, n, scratch, bytes, reverse, st);
         default: return cudaErrorInvalidValue;
     }
 }

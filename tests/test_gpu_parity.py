@@ -313,6 +313,41 @@ def test_minimum_graph(eg, ctx, dims, kind, path):
     assert_graph_equal(ctx.compute(torch.from_numpy(f).cuda(), dims=dims, flags=_flags(eg, path)), O.grid(f, dims))
 
 
+@pytest.mark.parametrize("n,p,seed,kind", [(12, 0.3, 0, "normal"), (300, 0.05, 2, "int"), (500, 0.02, 3, "normal")])
+def test_minimum_graph_csr(eg, ctx, n, p, seed, kind):
+    """EG_MINIMUM on a CSR graph: the maximum graph of the reversed rank image
+    (reading L22), against the oracle's reversed-order transcription (O10)."""
+    import torch
+    rp, ci = G.random_csr(n, p, seed)
+    f, _ = G.random_field([n], seed, kind, levels=3)
+    if kind == "normal":                                    # -0 ties with +0 (reading L2)
+        f[::7], f[3::7] = -0.0, 0.0
+    o = O.csr(f, rp, ci, minimum=True)
+    csr = (torch.from_numpy(rp).cuda(), torch.from_numpy(ci).cuda())
+    g = ctx.compute(torch.from_numpy(f).cuda(), csr=csr, flags=eg.EG_MINIMUM | eg.EG_CHECK_NAN)
+    assert_graph_equal(g, o, what=f"csr minimum {n} {kind}")
+
+
+def test_minimum_graph_csr_knn(eg, ctx):
+    """kNN graph (C5 recipe, 20K points): minimum graph, bundled minimum graph,
+    and the simplified minimum graph (node values from the caller's field)."""
+    import torch
+    X, f = G.gmm_points(20000, seed=12)
+    rp, ci = G.knn_csr(X, 12)
+    csr = (torch.from_numpy(rp).cuda(), torch.from_numpy(ci).cuda())
+    t = torch.from_numpy(f).cuda()
+    o = O.csr(f, rp, ci, minimum=True)
+    assert_graph_equal(ctx.compute(t, csr=csr, flags=eg.EG_MINIMUM), o, what="knn minimum")
+    assert_graph_equal(ctx.compute(t, csr=csr, flags=eg.EG_MINIMUM | eg.EG_BUNDLE),
+                       O.bundle(o, f, minimum=True), what="knn minimum bundled")
+    ctx.compute(t, csr=csr, flags=eg.EG_MINIMUM | eg.EG_NODE_VALUES)
+    for tau in (0.0, 0.5):
+        s = ctx.simplify(tau)
+        e = O.simplify(o, f, tau, minimum=True)
+        assert np.array_equal(s.maxima, e.maxima) and np.array_equal(s.arcs, e.arcs), tau
+    assert_graph_equal(ctx.compute(t, csr=csr), O.csr(f, rp, ci), what="knn maximum after minimum")
+
+
 def test_minimum_graph_unsupported(eg, ctx):
     import torch
     f, dims = G.random_field([20, 20, 20], 3, "normal")
@@ -467,6 +502,8 @@ def _wide_field(tdtype, N, rng):
         x = (np.uint64(1) << np.uint64(63)) + rng.integers(0, 40, N).astype(np.uint64) * np.uint64(1 << 20)
     x = np.asarray(x).astype(getattr(np, tdtype))
     x[rng.integers(0, N, N // 8)] = x[rng.integers(0, N, N // 8)]      # exact ties
+    if tdtype == "float64":
+        x[::11], x[5::11] = -0.0, 0.0                                  # -0 ties with +0 (reading L2)
     return x
 
 

@@ -519,6 +519,38 @@ def test_csr_equals_grid_on_freudenthal_graph(dims, kind):
     assert np.array_equal(a.saddles, c.saddles) and a.arcs.tolist() == c.arcs.tolist()
 
 
+@pytest.mark.parametrize("dims,kind", [([6, 5], "int"), ([5, 4, 4], "normal")])
+def test_csr_minimum_equals_grid_minimum(dims, kind):
+    # L11 + L14: the minimum graph on the Freudenthal adjacency graph is the grid's
+    f, _ = G.random_field(dims, 6, kind)
+    row_ptr, col_idx = brute.freudenthal_csr(dims)
+    a = O.grid(f, dims, minimum=True)
+    c = O.csr(f, row_ptr, col_idx, minimum=True)
+    assert np.array_equal(a.label, c.label) and np.array_equal(a.maxima, c.maxima)
+    assert np.array_equal(a.saddles, c.saddles) and a.arcs.tolist() == c.arcs.tolist()
+
+
+@pytest.mark.parametrize("n,p,seed,kind", [(40, 0.2, 1, "int"), (200, 0.05, 2, "normal")])
+def test_csr_minimum_by_relabelled_reflection(n, p, seed, kind):
+    # L11 on any graph: relabel every vertex i -> n-1-i and negate f; the
+    # maximum graph of that, mapped back, is the minimum graph (the reversed
+    # order's index tie-break is the relabelled index order).
+    row_ptr, col_idx = G.random_csr(n, p, seed)
+    f, _ = G.random_field([n], seed, kind, levels=3)
+    adj = [sorted(n - 1 - int(u) for u in col_idx[row_ptr[n - 1 - i]:row_ptr[n - i]]) for i in range(n)]
+    rp2 = np.zeros(n + 1, np.int64)
+    rp2[1:] = np.cumsum([len(a) for a in adj])
+    ci2 = np.array([u for a in adj for u in a], np.int32)
+    g = np.ascontiguousarray(-f[::-1])
+    mx = O.csr(g, rp2, ci2)
+    mn = O.csr(f, row_ptr, col_idx, minimum=True)
+    assert np.array_equal(mn.label, (n - 1 - mx.label)[::-1])
+    assert np.array_equal(mn.maxima, np.sort(n - 1 - mx.maxima))
+    assert np.array_equal(mn.saddles, np.sort(n - 1 - mx.saddles))
+    back = sorted((n - 1 - int(s), n - 1 - int(m), int(k)) for s, m, k in mx.arcs.tolist())
+    assert mn.arcs.tolist() == [list(a) for a in back]
+
+
 def test_knn_small_sanity():
     # C5 recipe at 2,000 points: symmetric sorted CSR, degree >= k, Euler
     # identity on the kNN graph, sampled walks agree with labels.
