@@ -116,10 +116,10 @@ enum {
      * minimum graph"; reading L11): minima, 1-saddles (beta0 of the lower link
      * >= 2) and the descending arcs / labels -- the maximum graph under the
      * reversed total order.  eg_graph's "maxima" then hold the minima, labels
-     * the minimum each descending path reaches.  Grids (by point reflection)
-     * and CSR graphs (by the field's reversed SoS-rank image, reading L22;
-     * the whole vertex range, N < 2^31 - 2^24); one GPU, one slab, no
-     * EG_RAW_ARCS / EG_ARC_PATHS (EG_ERR_UNSUPPORTED otherwise). */
+     * the minimum each descending path reaches.  Grids by point reflection;
+     * CSR graphs, and grids with EG_RAW_ARCS / EG_ARC_PATHS, by the field's
+     * reversed SoS-rank image (reading L22; the whole vertex range,
+     * N < 2^31 - 2^24).  One GPU, one slab (EG_ERR_UNSUPPORTED otherwise). */
     EG_MINIMUM = 32u,
     /* Arc geometry (Fig. 4): the integral line of
      * every raw arc -- s, rep, then steepest-ascent steps to m -- available

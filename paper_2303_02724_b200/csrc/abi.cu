@@ -111,6 +111,7 @@ struct eg_ctx {
     DevBuf typed;                      // eg_compute_typed: the field converted to float32
     DevBuf rank_scratch;               // eg_compute_typed, rank types: sort keys / indices / cub scratch
     bool minimum = false;              // the current compute is a minimum graph
+    bool min_reflect = false;          // ... by point reflection (ids mapped back afterwards)
     bool bundle = false;               // the current compute bundles arcs (EG_BUNDLE)
     DevBuf bund_scratch;               // arc bundling scratch (keys, indices, scans)
     DevBuf b_sad64, b_sad32, b_sbeta, b_nu, b_arc_s, b_arc_m, b_arc_mult;   // bundled outputs (swapped in)
@@ -794,7 +795,7 @@ static eg_status compute_grid(eg_ctx *c, const Problem &P, const float *f, uint3
     // arcs -- which follow a representative's exit pointer themselves -- and
     // their copies to the host) runs on the aux stream while the labels are
     // finalised on the ctx stream.  The widening flags keep the serial order.
-    c->overlap = tiled && !multi && c->world == 1 && !c->minimum && !c->bundle &&
+    c->overlap = tiled && !multi && c->world == 1 && !c->min_reflect && !c->bundle &&
                  !(flags & (EG_ARC_PATHS | EG_NODE_VALUES | EG_RAW_ARCS));
     c->gstream = c->overlap ? c->aux : c->stream;
     if (c->overlap) {
@@ -821,7 +822,7 @@ static eg_status compute_grid(eg_ctx *c, const Problem &P, const float *f, uint3
     c->have_labels = true;
     // one GPU, one slab, graph wanted: the node lists are copied early
     c->early_d2h =
-        c->world == 1 && c->slabs.size() == 1 && !raw && !(flags & EG_NO_GRAPH_D2H) && !c->minimum && !c->bundle;
+        c->world == 1 && c->slabs.size() == 1 && !raw && !(flags & EG_NO_GRAPH_D2H) && !c->min_reflect && !c->bundle;
     for (SlabState *S : c->slabs) ST(grid_graph(c, P, *S, raw, c->early_d2h));
     if (c->early_d2h) CK(cudaEventRecord(c->ev_d2h[2], c->d2h));
     CK(cudaEventRecord(c->ev[4], c->gstream));
@@ -1037,20 +1038,23 @@ static eg_status compute_impl(eg_ctx *c, const eg_domain *d, const float *f, uin
     // back by i -> N-1-i (k_common.cu)
     const float *f_user = f;           // the caller's field (device) -- f becomes the mirror for a minimum graph
     c->minimum = (flags & EG_MINIMUM) != 0;
-    // On a CSR graph (no reflection maps it onto itself) the maximum graph of
-    // the field's reversed SoS-rank image (reading L22) is the minimum graph,
-    // with vertex ids unchanged.
+    // On a CSR graph (no reflection maps it onto itself), and for raw arcs /
+    // arc paths (whose ids and order the reflection would have to map back),
+    // the maximum graph of the field's reversed SoS-rank image (reading L22)
+    // is the minimum graph, with vertex ids unchanged.
+    c->min_reflect = false;
     if (c->minimum) {
-        if (c->world > 1 || ((flags >> 8) & 0xffffff) > 1 || (flags & EG_RAW_ARCS))
-            return set_err(c, EG_ERR_UNSUPPORTED, "EG_MINIMUM: one GPU and one slab, without raw arcs");
+        if (c->world > 1 || ((flags >> 8) & 0xffffff) > 1)
+            return set_err(c, EG_ERR_UNSUPPORTED, "EG_MINIMUM: one GPU and one slab");
         if (!P.grid && (P.v0 != 0 || P.v1 != P.N))
             return set_err(c, EG_ERR_UNSUPPORTED, "EG_MINIMUM on a CSR graph: the whole vertex range");
         CK(c->mirror.ensure(sizeof(float) * std::max<int64_t>(P.N, 1)));
-        if (P.grid) {
+        c->min_reflect = P.grid && !(flags & (EG_RAW_ARCS | EG_ARC_PATHS));
+        if (c->min_reflect) {
             CK(launch_reflect_negate(f, c->mirror.as<float>(), P.N, c->stream));
             c->stats.kernel_launches += 1;
         } else {
-            if (P.N > kRankMaxN) return set_err(c, EG_ERR_UNSUPPORTED, "EG_MINIMUM on a CSR graph: N too large");
+            if (P.N > kRankMaxN) return set_err(c, EG_ERR_UNSUPPORTED, "EG_MINIMUM by rank image: N too large");
             size_t bytes = 0;
             CK(launch_rank_f32(f, EG_DTYPE_F32, nullptr, P.N, nullptr, &bytes, true, c->stream));
             CK(c->rank_scratch.ensure(bytes));
@@ -1065,8 +1069,8 @@ static eg_status compute_impl(eg_ctx *c, const eg_domain *d, const float *f, uin
     if (c->bundle && (c->world > 1 || ((flags >> 8) & 0xffffff) > 1))
         return set_err(c, EG_ERR_UNSUPPORTED, "EG_BUNDLE: one GPU, one slab");
     if (flags & EG_ARC_PATHS) {
-        if (c->world > 1 || ((flags >> 8) & 0xffffff) > 1 || c->minimum)
-            return set_err(c, EG_ERR_UNSUPPORTED, "EG_ARC_PATHS: one GPU, one slab, maximum graph");
+        if (c->world > 1 || ((flags >> 8) & 0xffffff) > 1)
+            return set_err(c, EG_ERR_UNSUPPORTED, "EG_ARC_PATHS: one GPU, one slab");
         flags |= EG_RAW_ARCS;
     }
     if (P.grid) ST(compute_grid(c, P, f, flags));
@@ -1104,7 +1108,7 @@ static eg_status compute_impl(eg_ctx *c, const eg_domain *d, const float *f, uin
         c->paths_valid = true;
     }
     if (c->bundle) ST(bundle_arcs(c));
-    if (c->minimum && P.grid) {
+    if (c->min_reflect) {
         SlabState &S = *c->slabs[0];
         const int64_t N = P.N;
         CK(launch_reverse_i32(c->label_all.as<int32_t>(), N, N, true, c->stream));

@@ -353,8 +353,6 @@ def test_minimum_graph_unsupported(eg, ctx):
     f, dims = G.random_field([20, 20, 20], 3, "normal")
     with pytest.raises(Exception):
         ctx.compute(torch.from_numpy(f).cuda(), dims=dims, flags=eg.EG_MINIMUM | eg.EG_VIRTUAL_PARTS(2))
-    with pytest.raises(Exception):
-        ctx.compute(torch.from_numpy(f).cuda(), dims=dims, flags=eg.EG_MINIMUM | eg.EG_RAW_ARCS)
 
 
 def _oracle_paths(o):
@@ -393,6 +391,29 @@ def test_arc_paths_csr(eg, ctx):
     o = O.csr(f, rp, ci)
     g = ctx.compute(torch.from_numpy(f).cuda(), csr=(torch.from_numpy(rp).cuda(), torch.from_numpy(ci).cuda()),
                     flags=eg.EG_ARC_PATHS)
+    off, v = g.arc_paths
+    exp = _oracle_paths(o)
+    assert [v[off[j]:off[j + 1]].tolist() for j in range(len(exp))] == exp
+
+
+@pytest.mark.parametrize("dims,kind", [([64, 48], "int"), ([40, 33, 29], "normal"), ([9, 8, 7, 6], "int"),
+                                       ("csr", "normal")])
+def test_minimum_raw_arcs_and_paths(eg, ctx, dims, kind):
+    """EG_MINIMUM with EG_RAW_ARCS / EG_ARC_PATHS (the reversed rank image,
+    reading L22): raw descending arcs and every descending integral line."""
+    import torch
+    if dims == "csr":
+        X, f = G.gmm_points(3000, seed=5)
+        rp, ci = G.knn_csr(X, 8)
+        o = O.csr(f, rp, ci, minimum=True)
+        kw = dict(csr=(torch.from_numpy(rp).cuda(), torch.from_numpy(ci).cuda()))
+    else:
+        f, _ = G.random_field(dims, 43 + len(dims), kind)
+        o = O.grid(f, dims, minimum=True)
+        kw = dict(dims=dims)
+    g = ctx.compute(torch.from_numpy(f).cuda(), flags=eg.EG_MINIMUM | eg.EG_RAW_ARCS, **kw)
+    assert_graph_equal(g, o, raw=True, what=f"minimum raw {dims}")
+    g = ctx.compute(torch.from_numpy(f).cuda(), flags=eg.EG_MINIMUM | eg.EG_ARC_PATHS, **kw)
     off, v = g.arc_paths
     exp = _oracle_paths(o)
     assert [v[off[j]:off[j + 1]].tolist() for j in range(len(exp))] == exp
