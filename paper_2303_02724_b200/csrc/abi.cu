@@ -826,7 +826,7 @@ static eg_status compute_grid(eg_ctx *c, const Problem &P, const float *f, uint3
     for (SlabState *S : c->slabs) ST(grid_graph(c, P, *S, raw, c->early_d2h));
     if (c->early_d2h) CK(cudaEventRecord(c->ev_d2h[2], c->d2h));
     CK(cudaEventRecord(c->ev[4], c->gstream));
-    if (c->overlap) ST(fail_if_flags(c));     // (syncs the ctx stream: the finalize pass)
+    // (overlap: the flags are checked once the graph copies are queued, compute_impl)
     c->raw_valid = raw;
     return EG_OK;
 }
@@ -1129,6 +1129,9 @@ static eg_status compute_impl(eg_ctx *c, const eg_domain *d, const float *f, uin
         CK(cudaEventRecord(c->ev_graph, c->gstream));
         CK(cudaStreamWaitEvent(c->stream, c->ev_graph, 0));
     }
+    // overlap: the arc copies above were queued while the finalize pass still
+    // runs (checking the flags first would hold them until it ends)
+    if (c->overlap) ST(fail_if_flags(c));
     c->node_values = false;
     c->last_minimum = c->minimum;
     if ((flags & EG_NODE_VALUES) && c->world == 1 && c->graph_on_host) {
