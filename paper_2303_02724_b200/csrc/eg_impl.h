@@ -74,8 +74,8 @@ struct LabelView {
 #ifdef __CUDACC__
     __device__ __forceinline__ int32_t at(int64_t g) const {
         if (chase) {
-            int32_t w = *(volatile const int32_t *)(own + (g - v0));
-            while (w < 0) w = *(volatile const int32_t *)(own + ((w & 0x7fffffff) - v0));
+            int32_t w = __ldca(own + (g - v0));
+            while (w < 0) w = __ldca(own + ((w & 0x7fffffff) - v0));
             return w;
         }
         if (g >= v0 && g < v1) return own[g - v0];

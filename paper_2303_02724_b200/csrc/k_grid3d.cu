@@ -546,7 +546,8 @@ __global__ void __launch_bounds__(kThreads, 2)
 }
 
 // Pass E: resolve every owned exit target through the exit graph (bit 31 =
-// not final), one dependent load per tile hop.  A path that leaves the slab
+// not final), one dependent load per tile hop (L1-cached: a stale value is an
+// earlier vertex of the same path, so it only lengthens the walk).  A path that leaves the slab
 // stops at its first remote vertex (resolved later by the boundary exchange).
 __global__ void __launch_bounds__(256) k_resolve_exits(int32_t *label, const int32_t *__restrict__ elist,
                                                        const unsigned long long *ecount, int64_t ecap, int64_t v0,
@@ -555,12 +556,12 @@ __global__ void __launch_bounds__(256) k_resolve_exits(int32_t *label, const int
     for (int64_t j = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; j < n; j += int64_t(gridDim.x) * blockDim.x) {
         const int64_t e = elist[j];
         if (e < v0 || e >= v1) continue;                 // a halo vertex: another slab's
-        int32_t w = *(volatile int32_t *)(label + (e - v0));
+        int32_t w = __ldca(label + (e - v0));
         if (w >= 0) continue;
         for (;;) {
             const int64_t x = w & 0x7fffffff;
             if (x < v0 || x >= v1) break;                 // remote: stays unresolved
-            const int32_t nw = *(volatile int32_t *)(label + (x - v0));
+            const int32_t nw = __ldca(label + (x - v0));
             w = nw;
             if (w >= 0) break;
         }
@@ -578,7 +579,7 @@ __global__ void __launch_bounds__(256) k_exit_chase(int32_t *label, int64_t v0, 
     while (w < 0) {
         const int64_t x = w & 0x7fffffff;
         if (x < v0 || x >= v1) break;
-        w = *(volatile int32_t *)(label + (x - v0));
+        w = __ldca(label + (x - v0));
     }
     label[i] = w;
 }
