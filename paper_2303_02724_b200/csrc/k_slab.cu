@@ -90,9 +90,10 @@ cudaError_t launch_bval_update(int32_t *bval, const int32_t *hval_lo, const int3
 // Final pass.  A warp owns kW words of owned vertices (32 kW vertices); the
 // loads of all of them are issued before any is used (memory-level
 // parallelism for the dependent gather), and only changed labels are stored.
-// (kW = 4 words per warp at full occupancy measured best for the one-slab
-// chase: 3.08 ms on C3 vs 3.48 at kW = 8, 4.04 at 2, 4.48 at 16)
-constexpr int kW = 4;
+// (kW = 6 words per warp at full occupancy measured best for the one-slab
+// chase with L1-cached loads: C3 3.09 ms vs 3.15 at kW = 4, 3.17 at 8, 3.95
+// at 2; the smooth F1-1024 field 6.0 vs 7.0 ms at kW = 4)
+constexpr int kW = 6;
 __global__ void __launch_bounds__(256, 8) k_finalize(int32_t *label, const uint32_t *__restrict__ bits, int64_t v0,
                                                   int64_t v1, const int32_t *__restrict__ hlo,
                                                   const int32_t *__restrict__ hhi, int64_t plane) {
