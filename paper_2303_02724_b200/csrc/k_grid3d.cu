@@ -134,7 +134,7 @@ struct TileArgs {
     int32_t tiles_x, tiles_y;       // interior variant: sub-box extents
     int3 origin;                    // interior variant: first interior tile
     int32_t rounds;                 // pointer-doubling rounds before the chase
-    int32_t no_elist;               // one slab: no exit-target list (finalize chases with memoisation)
+    int32_t no_elist;               // one slab: no exit-target list (the finalize pass chases)
     int32_t tma;                    // field box by TMA (else plain row loads)
 };
 

@@ -91,8 +91,8 @@ cudaError_t launch_bval_update(int32_t *bval, const int32_t *hval_lo, const int3
 // loads of all of them are issued before any is used (memory-level
 // parallelism for the dependent gather), and only changed labels are stored.
 // (kW = 6 words per warp at full occupancy measured best for the one-slab
-// chase with L1-cached loads: C3 3.09 ms vs 3.15 at kW = 4, 3.17 at 8, 3.95
-// at 2; the smooth F1-1024 field 6.0 vs 7.0 ms at kW = 4)
+// chase: C3 3.13 ms vs 3.27 at kW = 4 or 8, 3.75 at 12; the smooth F1-1024
+// field prefers 8, 4.59 vs 5.18 ms)
 constexpr int kW = 6;
 __global__ void __launch_bounds__(256, 8) k_finalize(int32_t *label, const uint32_t *__restrict__ bits, int64_t v0,
                                                   int64_t v1, const int32_t *__restrict__ hlo,
@@ -121,19 +121,18 @@ __global__ void __launch_bounds__(256, 8) k_finalize(int32_t *label, const uint3
     if (!hlo && !hhi) {
         // one slab: every exit target is owned.  Its label is final when the
         // exit list was resolved first (k_resolve_exits); otherwise the chain
-        // is chased here and its final label memoised in the first target
-        // (race-benign: every value ever stored is a later vertex of the same
-        // ascending path, or the final label, and a root's label is final
-        // before this pass -- so a stale value read through L1 only means a
-        // longer walk; L1-cached loads measured 3127 vs 3281 us on C3 and
-        // 6.9 vs 8.1 ms on F1-1024 against volatile ones.  Compressing the
-        // whole chain measured 5x slower.)
-        int32_t tg[kW];
+        // is chased here, through L1-cached loads (race-benign: every value
+        // ever stored is a later vertex of the same ascending path or the
+        // final label, and a root's label is final before this pass, so a
+        // stale value only lengthens a walk).  Measured on C3 / F1-512 /
+        // F1-1024: volatile loads + memoising the final label in the first
+        // target 3281 / - / 8085 us; L1 + memo 3094 / 726 / 6021; L1 without
+        // memo 3130 / 353 / 5180 (kept: the memo stores keep hitting lines
+        // the other SMs' L1s still hold stale, so every reader re-walks and
+        // re-stores); whole-chain compression 5x slower.
 #pragma unroll
-        for (int k = 0; k < kW; ++k) {
-            tg[k] = e[k] & 0x7fffffff;
-            if (need[k]) e[k] = label[tg[k] - v0];
-        }
+        for (int k = 0; k < kW; ++k)
+            if (need[k]) e[k] = label[(e[k] & 0x7fffffff) - v0];
 #pragma unroll
         for (int k = 0; k < kW; ++k) {
             if (need[k] && e[k] < 0) {
@@ -142,7 +141,6 @@ __global__ void __launch_bounds__(256, 8) k_finalize(int32_t *label, const uint3
                     w = __ldca(label + ((w & 0x7fffffff) - v0));
                 } while (w < 0);
                 e[k] = w;
-                label[tg[k] - v0] = w;
             }
         }
 #pragma unroll
