@@ -566,3 +566,23 @@ def test_rank_dtype_errors(eg, ctx):
     assert e.value.status == 7
     g = ctx.compute(torch.from_numpy(np.arange(64 * 48, dtype=np.int64)).cuda(), dims=[64, 48])
     assert list(g.maxima) == [64 * 48 - 1] and len(g.saddles) == 0      # context still usable
+
+
+def test_rank_dtype_beyond_2p24(eg, ctx):
+    """The rank image past 2^24 vertices (ranks no float32 integer holds; the
+    bit-pattern image stays exact): a float64 copy of a float32 field has the
+    same SoS order, so its graph equals the float32 path's (itself pinned to
+    the oracle by the sampled C3 checks) -- also for an int64 rank-equivalent."""
+    import torch
+    dims = [320, 256, 256]                         # 20,971,520 > 2^24 vertices
+    f = torch.randn(int(np.prod(dims)), generator=torch.Generator().manual_seed(5)).to(torch.float32)
+    f[::13] = 0.25                                # ties
+    a = ctx.compute(f.cuda(), dims=dims)
+    la = a.labels.cpu().numpy().copy()
+    order = np.argsort(f.numpy(), kind="stable")
+    rank = np.empty(len(order), np.int64)
+    rank[order] = np.arange(len(order))
+    for t in (f.to(torch.float64), torch.from_numpy(rank * 3 - 7)):
+        b = ctx.compute(t.cuda(), dims=dims)
+        assert_graph_equal(b, a, labels=False, what=f"rank image {t.dtype}")
+        assert np.array_equal(b.labels.cpu().numpy(), la)
