@@ -353,6 +353,14 @@ def test_minimum_graph_unsupported(eg, ctx):
     f, dims = G.random_field([20, 20, 20], 3, "normal")
     with pytest.raises(Exception):
         ctx.compute(torch.from_numpy(f).cuda(), dims=dims, flags=eg.EG_MINIMUM | eg.EG_VIRTUAL_PARTS(2))
+    rp, ci = G.random_csr(200, 0.05, 4)
+    fc, _ = G.random_field([200], 4, "normal")
+    csr = (torch.from_numpy(rp).cuda(), torch.from_numpy(ci).cuda())
+    with pytest.raises(eg.EgError) as e:          # one GPU owns every vertex (the rank image needs them all)
+        ctx.compute(torch.from_numpy(fc).cuda(), csr=csr, v_range=(0, 100), flags=eg.EG_MINIMUM)
+    assert e.value.status == 1
+    assert_graph_equal(ctx.compute(torch.from_numpy(fc).cuda(), csr=csr, flags=eg.EG_MINIMUM),
+                       O.csr(fc, rp, ci, minimum=True), what="csr minimum after a refused call")
 
 
 def _oracle_paths(o):
