@@ -775,13 +775,12 @@ eg_status tiled3d_local(Tiled3D *t, int ndim, const int64_t *dims, const Slab &s
         A.shell = t->d_shell;
         A.btiles = t->d_btiles;
         A.rounds = t->rounds;
-        // One slab whose labels do not fit in L2: no exit list, the finalize
-        // pass chases (C3: 0.6 ms faster).  L2-resident label arrays resolve
-        // the list faster (C2: finalize + resolve 42 us vs a 157 us chase).
-        // EG_ELIST=1 / 0 forces either.
+        // One slab: no exit list, the finalize pass chases (C3: 0.6 ms faster;
+        // with L1-cached chase loads also for L2-resident label arrays: C2
+        // 2.95 vs 2.97 ms, F1-256 0.30 vs 0.34 ms).  EG_ELIST=1 / 0 forces
+        // either.
         const char *el = std::getenv("EG_ELIST");
-        const bool big = nown * 4 > (int64_t(96) << 20);
-        A.no_elist = (!F.lo && !F.hi && (el ? el[0] == '0' : big)) ? 1 : 0;
+        A.no_elist = (!F.lo && !F.hi && (el ? el[0] == '0' : true)) ? 1 : 0;
         A.tma = tma ? 1 : 0;
         if (ev_main0) cudaEventRecord(ev_main0, st);
         if (t->n_btiles > 0) {
