@@ -92,9 +92,10 @@ cudaError_t launch_bval_update(int32_t *bval, const int32_t *hval_lo, const int3
 // parallelism for the dependent gather), and only changed labels are stored.
 // (kW = 6 words per warp at full occupancy measured best for the one-slab
 // chase: C3 3.13 ms vs 3.27 at kW = 4 or 8, 3.75 at 12; the smooth F1-1024
-// field prefers 8, 4.59 vs 5.18 ms)
+// field prefers 8, 4.59 vs 5.18 ms; 128-thread blocks retire a block held by
+// one long chain sooner: C3 3.09 vs 3.12 ms at 256 or 64)
 constexpr int kW = 6;
-__global__ void __launch_bounds__(256, 8) k_finalize(int32_t *label, const uint32_t *__restrict__ bits, int64_t v0,
+__global__ void __launch_bounds__(128, 16) k_finalize(int32_t *label, const uint32_t *__restrict__ bits, int64_t v0,
                                                   int64_t v1, const int32_t *__restrict__ hlo,
                                                   const int32_t *__restrict__ hhi, int64_t plane) {
     const int64_t n = v1 - v0;
@@ -172,7 +173,7 @@ cudaError_t launch_finalize(int32_t *label, const uint32_t *bits, int64_t v0, in
                             const int32_t *hval_hi, int64_t plane, cudaStream_t st) {
     const int64_t words = (v1 - v0 + 31) / 32;
     if (words <= 0) return cudaSuccess;
-    k_finalize<<<blocks_for(words, 8 * kW), 256, 0, st>>>(label, bits, v0, v1, hval_lo, hval_hi, plane);
+    k_finalize<<<blocks_for(words, 4 * kW), 128, 0, st>>>(label, bits, v0, v1, hval_lo, hval_hi, plane);
     return cudaGetLastError();
 }
 
