@@ -7,9 +7,11 @@ A step is one eg_compute over the resident field: steepest-ascent pointers,
 pointer-jumping labels, saddles, deduplicated arcs, and the graph copied to
 the host (SURVEY 8(d) timed region).  The default workload is C3 (3D 1024^3
 turbulence-like float32 field); the other BASELINE configs are parity cases.
-For N > 1 (torchrun) every rank runs its own replica of the workload
-("replicas only" until the slab path lands; scaling "weak"), timed with CUDA
-events, max over ranks.
+For N > 1 the grid is cut into slabs of the slowest axis, one per rank (CSR:
+vertex ranges), with the halo / boundary-label exchanges over NCCL inside the
+library (strong scaling of the same workload), timed with CUDA events, max
+over ranks.  `--gpus N` without torchrun re-launches itself under
+torch.distributed.run with N ranks.
 
 --impl reference times the CPU oracle (oracle/, the baseline of this tier) on
 a bounded sample of the same workload on rank 0.
@@ -247,25 +249,9 @@ def run_ours(args):
         flags |= eg.EG_VIRTUAL_PARTS(int(os.environ["EG_BENCH_VPARTS"]))
     fallback = None
     if world > 1 and parallelism != "replicas":
-        # the sharded path (NCCL exchanges inside the library); if its first
-        # step fails on this box, every rank falls back to an independent
-        # replica so that the job still reports (and says so)
-        f_full = f if "slab" not in kw else None
-        try:
-            ctx = eg.init_distributed(stream=stream)
-            ctx.compute(f, flags=flags, **kw)
-            ok = torch.ones(1, device=dev)
-        except Exception as e:                                   # noqa: BLE001
-            fallback = f"{type(e).__name__}: {e}"[:200]
-            ok = torch.zeros(1, device=dev)
-        dist.all_reduce(ok, op=dist.ReduceOp.MIN)
-        if ok.item() == 0:
-            fallback = fallback or "another rank's sharded step failed"
-            print(f"bench: sharded path failed ({fallback}); running replicas", file=sys.stderr)
-            f, dims, csr = (f_full, dims, csr) if f_full is not None else make_input(args.config, dev)
-            kw = dict(dims=dims) if dims is not None else dict(csr=csr)
-            scaling, parallelism = "weak", "replicas (sharded path failed)"
-            ctx = eg.Context(torch.cuda.current_device(), stream)
+        # the sharded path (NCCL exchanges inside the library); a failure is
+        # fatal -- there is no silent fallback to replicas
+        ctx = eg.init_distributed(stream=stream)
     else:
         ctx = eg.Context(torch.cuda.current_device(), stream)
 
@@ -282,11 +268,13 @@ def run_ours(args):
     torch.cuda.synchronize()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     launches, k_us, k_bytes, stats = 0, 0.0, 0, []
+    evs = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     ev0.record(stream)
-    for _ in range(args.steps):
+    for i in range(args.steps):
         # one step = S1..S4 with the graph copied to (library-owned, pinned)
         # host memory; numpy copies of it are made outside the timed region
         ctx.compute(f, flags=flags, materialize=False, **kw)
+        evs[i].record(stream)
         s = ctx.stats()
         stats.append(s)
         launches += s["kernel_launches"]
@@ -295,6 +283,13 @@ def run_ours(args):
     if world > 1:
         dist.barrier()
     ms = ev0.elapsed_time(ev1)
+    per_step = sorted([ev0.elapsed_time(evs[0])] + [evs[i - 1].elapsed_time(evs[i]) for i in range(1, args.steps)])
+    trim = per_step[1:-1] if len(per_step) >= 3 else per_step
+    step_stats = {"min": round(per_step[0], 4), "max": round(per_step[-1], 4),
+                  "median": round(float(np.median(per_step)), 4),
+                  "trimmed_mean": round(float(np.mean(trim)), 4),
+                  "rule": "per-step CUDA events (this rank); trimmed_mean drops the min and max (P:319: "
+                          "middle 5 of 7 at --steps 7)"}
     g = ctx.graph()
     clk = clocks.stop()
     t_max = torch.tensor([ms], device=dev)
@@ -380,20 +375,33 @@ def run_ours(args):
         idx = rng.integers(0, n_vert, 300)
         bad = sum(int(O.grid_walk(fc, dims, int(v))[0] != lab[v]) for v in idx)
         sidx = rng.integers(0, max(1, len(g.saddles)), min(100, len(g.saddles)))
-        bad_s = 0
+        arcs_by_s = {}
+        for s_, m_, c_ in g.arcs.tolist():
+            arcs_by_s.setdefault(s_, []).append((m_, c_))
+        bad_s = bad_a = 0
         for j in sidx:
             s = int(g.saddles[j])
             p, b, reps = O.grid_vertex(fc, dims, s)
             bad_s += int(b != g.saddle_beta[j])
+            # the saddle's deduplicated arcs: Alg. 2 walks from its UpperLinkReps
+            ms = sorted(O.grid_walk(fc, dims, int(r))[0] for r in reps)
+            bad_a += int(sorted(arcs_by_s.get(s, [])) != sorted((m, ms.count(m)) for m in set(ms)))
         parity = {"sampled_labels": len(idx), "label_mismatch": bad, "sampled_saddles": len(sidx),
-                  "beta_mismatch": bad_s}
+                  "beta_mismatch": bad_s, "arc_mismatch": bad_a,
+                  "full_domain": "tests/test_gpu_configs.py (whole-domain oracle, profiles/r02/*_parity.json)"}
 
+    field_sha = None
+    if fc is not None:
+        import hashlib
+        field_sha = hashlib.sha256(memoryview(np.ascontiguousarray(fc)).cast("B")).hexdigest()
     line = {
         "metric": "Mvertices/s end-to-end extremum graph", "value": round(value, 2), "unit": "Mvertices/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 4),
         "higher_is_better": True, "scaling": scaling, "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "step_ms": step_stats,
         "config": {"workload": CONFIGS[args.config]["desc"], "config": args.config,
                    "dims": dims, "n_vertices": n_vert, "path": path,
+                   **({"field_sha256": field_sha} if field_sha else {}),
                    "parallelism": parallelism, **({"fallback": fallback} if fallback else {}),
                    "l2": "inputs larger than L2 (field 4 GiB vs 126 MB L2)" if n_vert * 4 > 126e6 else
                    "input smaller than L2 (no flush)"},
@@ -425,7 +433,7 @@ def run_ours(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=7)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="C3", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
@@ -438,9 +446,26 @@ def main():
     if args.warmup < 3:
         print("warning: --warmup < 3 violates the timing rules; using 3", file=sys.stderr)
         args.warmup = 3
+    world = os.environ.get("WORLD_SIZE")
+    if args.gpus > 1 and world is None:
+        return relaunch(args.gpus)
+    if world is not None and int(world) != args.gpus:
+        raise SystemExit(f"bench: --gpus {args.gpus} but WORLD_SIZE={world}")
     if args.impl == "reference":
         return run_reference(args)
     return run_ours(args)
+
+
+def relaunch(n: int) -> int:
+    """`bench.py --gpus N` outside torchrun: run this same command under
+    torch.distributed.run with N ranks on this node (rendezvous on 127.0.0.1)."""
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd)
 
 
 if __name__ == "__main__":

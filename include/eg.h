@@ -135,7 +135,7 @@ enum {
 };
 /* virtual partitions: process a grid as k slabs on one GPU, exchanging
  * boundaries by device copies exactly as k ranks would (partition test). */
-#define EG_VIRTUAL_PARTS(k) ((uint32_t)(k) << 8)
+#define EG_VIRTUAL_PARTS(k) ((uint32_t)(k) << 16)   /* k < 65536; bits 16-31, no flag uses them */
 
 /* Create a single-GPU context on `cuda_device`, launching on `cuda_stream`
  * (a cudaStream_t, NULL = the legacy default stream).  Fails with

@@ -79,6 +79,11 @@ def _L():
         _lib.ego_csr_euler.argtypes = [C.c_int64, i64p, i32p, f32p, i64p]
         _lib.ego_grid_link_stats.argtypes = [C.c_int, i64p, C.c_int64, i64p, i64p, i64p]
         _lib.ego_set_order.argtypes = [C.c_int]
+        _lib.ego_grid_range.argtypes = [C.c_int, i64p, f32p, C.c_int64, C.c_int64, i64p, i32p, i64p, i64p,
+                                        C.c_int64, i64p]
+        _lib.ego_csr_range.argtypes = [C.c_int64, i64p, i32p, f32p, C.c_int64, C.c_int64, i64p, i32p, i64p, i64p,
+                                       C.c_int64, i64p]
+        _lib.ego_labels.argtypes = [C.c_int64, i64p, i64p]
     return _lib
 
 
@@ -369,3 +374,111 @@ def simplify(g: Graph, f: np.ndarray, tau: float, minimum: bool = False) -> Grap
                  saddles=g.saddles[keep], saddle_beta=g.saddle_beta[keep], arc_s=a[:, 0].copy(),
                  arc_m=a[:, 1].copy(), arc_mult=a[:, 2].astype(np.int32), raw_s=g.raw_s, raw_rep=g.raw_rep,
                  raw_m=g.raw_m)
+
+
+# ------------------------------------------------------------ big domains
+# The whole-domain oracle above is one thread; C3 (2^30 vertices) would take
+# ~20 min that way.  Classification (O3..O6) is independent per vertex, so the
+# harness below runs the oracle's own range function (ego_*_range: the same
+# classify_vertex loop) on disjoint vertex ranges in forked worker processes,
+# then O7 (ego_labels: the same memoised walk) and O8 (per saddle, label of
+# every UpperLinkRep, reduced to unique (s, m) with multiplicity) on the
+# assembled arrays.  No step is re-derived here; the result is the run_all
+# result, which tests/test_oracle_pins.py::test_parallel_equals_whole checks.
+
+_PAR = None   # (kind, args) inherited by the forked workers
+
+
+def _range_worker(job):
+    v0, v1 = job
+    kind, args, ptr, beta = _PAR
+    L = _L()
+    cap = max(4096, (v1 - v0) // 2)
+    while True:
+        rs = np.zeros(cap, np.int64)
+        rr = np.zeros(cap, np.int64)
+        nrep = C.c_int64()
+        pp = C.cast(C.c_void_p(ptr.ctypes.data + 8 * v0), C.POINTER(C.c_int64))
+        bp = C.cast(C.c_void_p(beta.ctypes.data + 4 * v0), C.POINTER(C.c_int32))
+        if kind == "grid":
+            f, d = args
+            rc = L.ego_grid_range(len(d), _p(d, C.c_int64), _p(f, C.c_float), v0, v1, pp, bp, _p(rs, C.c_int64),
+                                  _p(rr, C.c_int64), cap, C.byref(nrep))
+        else:
+            f, rp, ci = args
+            rc = L.ego_csr_range(len(f), _p(rp, C.c_int64), _p(ci, C.c_int32), _p(f, C.c_float), v0, v1, pp, bp,
+                                 _p(rs, C.c_int64), _p(rr, C.c_int64), cap, C.byref(nrep))
+        if rc != OK:
+            return v0, rc, None, None
+        if nrep.value <= cap:
+            return v0, OK, rs[:nrep.value].copy(), rr[:nrep.value].copy()
+        cap = nrep.value
+
+
+def _parallel(kind, args, n, procs):
+    import mmap
+    import multiprocessing as mp
+    global _PAR
+    procs = procs or os.cpu_count() or 1
+    pb = mmap.mmap(-1, max(8 * n, 8))            # MAP_SHARED | MAP_ANONYMOUS: the workers write into it
+    bb = mmap.mmap(-1, max(4 * n, 4))
+    ptr = np.frombuffer(pb, np.int64, count=n)
+    beta = np.frombuffer(bb, np.int32, count=n)
+    nchunk = max(1, min(n, procs * 16))
+    edges = [n * i // nchunk for i in range(nchunk + 1)]
+    jobs = [(edges[i], edges[i + 1]) for i in range(nchunk) if edges[i + 1] > edges[i]]
+    _PAR = (kind, args, ptr, beta)
+    try:
+        if procs == 1:
+            res = [_range_worker(j) for j in jobs]
+        else:
+            with mp.get_context("fork").Pool(procs) as pool:
+                res = pool.map(_range_worker, jobs, chunksize=1)
+    finally:
+        _PAR = None
+    res.sort(key=lambda r: r[0])
+    for _, rc, _, _ in res:
+        if rc != OK:
+            raise OracleError(f"ego_{kind}_range failed: {rc}")
+    ptr = ptr.copy()
+    beta = beta.copy()
+    del pb, bb
+    label = np.empty(n, np.int64)
+    rc = _L().ego_labels(n, _p(ptr, C.c_int64), _p(label, C.c_int64))
+    if rc != OK:
+        raise OracleError(f"ego_labels failed: {rc}")
+    raw_s = np.concatenate([r[2] for r in res]) if res else np.zeros(0, np.int64)
+    raw_rep = np.concatenate([r[3] for r in res]) if res else np.zeros(0, np.int64)
+    raw_m = label[raw_rep]
+    # O8: unique (s, m) per saddle with multiplicity, sorted by (s, m)
+    if len(raw_s):
+        o = np.lexsort((raw_m, raw_s))
+        ss, mm = raw_s[o], raw_m[o]
+        first = np.ones(len(ss), bool)
+        first[1:] = (ss[1:] != ss[:-1]) | (mm[1:] != mm[:-1])
+        idx = np.flatnonzero(first)
+        mult = np.diff(np.append(idx, len(ss))).astype(np.int32)
+        arc_s, arc_m = ss[idx], mm[idx]
+    else:
+        arc_s = arc_m = np.zeros(0, np.int64)
+        mult = np.zeros(0, np.int32)
+    maxima = np.flatnonzero(beta == 0).astype(np.int64)
+    sad = np.flatnonzero(beta >= 2).astype(np.int64)
+    return Graph(ptr=ptr, label=label, beta=beta, maxima=maxima, saddles=sad, saddle_beta=beta[sad].astype(np.int32),
+                 arc_s=arc_s, arc_m=arc_m, arc_mult=mult, raw_s=raw_s, raw_rep=raw_rep, raw_m=raw_m)
+
+
+def grid_parallel(f: np.ndarray, dims, procs: int = None) -> Graph:
+    """grid() for big domains: the oracle's per-vertex steps over disjoint
+    vertex ranges in `procs` forked processes (default: every host core)."""
+    f = np.ascontiguousarray(np.asarray(f, dtype=np.float32).reshape(-1))
+    d = _dims_arr(dims)
+    return _parallel("grid", (f, d), len(f), procs)
+
+
+def csr_parallel(f: np.ndarray, row_ptr: np.ndarray, col_idx: np.ndarray, procs: int = None) -> Graph:
+    """csr() for big graphs, as grid_parallel."""
+    f = np.ascontiguousarray(f, dtype=np.float32)
+    rp = np.ascontiguousarray(row_ptr, dtype=np.int64)
+    ci = np.ascontiguousarray(col_idx, dtype=np.int32)
+    return _parallel("csr", (f, rp, ci), len(f), procs)

@@ -327,6 +327,22 @@ static int cmp_i64(const void *a, const void *b) {
     return (x > y) - (x < y);
 }
 
+/* O7 (Alg. 2 "follow gradient(u) until u is a maximum"): for
+ * v = 0..n-1 whose label is unset, walk v, ptr[v], ptr[ptr[v]], ... pushing
+ * onto `stack` until a maximum (ptr[x] == x) or a labelled vertex, then give
+ * the whole stack that label (memoised, O(n) in total).  `stack` holds n. */
+static void labels_from_ptr(int64_t n, const int64_t *ptr, int64_t *label, int64_t *stack) {
+    for (int64_t v = 0; v < n; ++v) label[v] = -1;
+    for (int64_t v = 0; v < n; ++v) {
+        if (label[v] >= 0) continue;
+        int64_t sp = 0, x = v;
+        while (label[x] < 0 && ptr[x] != x) { stack[sp++] = x; x = ptr[x]; }
+        int64_t m = label[x] >= 0 ? label[x] : x;
+        label[x] = m;
+        while (sp > 0) label[stack[--sp]] = m;
+    }
+}
+
 static int run_all(work_t *w, int64_t n, ego_result *out) {
     memset(out, 0, sizeof(*out));
     out->n = n;
@@ -348,15 +364,7 @@ static int run_all(work_t *w, int64_t n, ego_result *out) {
     }
 
     /* O7: labels by following the gradient (Alg. 2), memoised */
-    for (int64_t v = 0; v < n; ++v) out->label[v] = -1;
-    for (int64_t v = 0; v < n; ++v) {
-        if (out->label[v] >= 0) continue;
-        int64_t sp = 0, x = v;
-        while (out->label[x] < 0 && out->ptr[x] != x) { stack[sp++] = x; x = out->ptr[x]; }
-        int64_t m = out->label[x] >= 0 ? out->label[x] : x;
-        out->label[x] = m;
-        while (sp > 0) out->label[stack[--sp]] = m;
-    }
+    labels_from_ptr(n, out->ptr, out->label, stack);
     free(stack);
 
     /* O6 / O9 node lists, ascending */
@@ -428,6 +436,73 @@ int ego_csr(int64_t nv, const int64_t *row_ptr, const int32_t *col_idx, const fl
     int rc = run_all(&w, nv, out);
     work_free(&w);
     return rc;
+}
+
+/* ---------------------------------------------- range entry points
+ * The same steps as run_all, split for domains too big for one thread in a
+ * test (C3 has 2^30 vertices): O3..O6 of the vertices [v0, v1) -- every
+ * vertex is classified on its own, so disjoint ranges may be classified by
+ * separate processes (oracle/__init__.py: grid_parallel / csr_parallel) --
+ * and O7 over the assembled gradient array.  Each call is single-threaded and
+ * runs exactly classify_vertex / labels_from_ptr; nothing is re-derived.
+ * ptr / beta are indexed v - v0.  For every saddle (beta0+ >= 2), ascending,
+ * its UpperLinkReps (ascending) are appended to (rep_s, rep_r) while fewer
+ * than `cap` are stored; *n_rep counts all of them (> cap: call again with
+ * room). */
+static int range_common(work_t *w, int64_t v0, int64_t v1, int64_t *ptr, int32_t *beta,
+                        int64_t *rep_s, int64_t *rep_r, int64_t cap, int64_t *n_rep) {
+    int64_t k = 0;
+    for (int64_t v = v0; v < v1; ++v) {
+        int64_t p;
+        int64_t b = classify_vertex(w, v, &p);
+        ptr[v - v0] = p;
+        beta[v - v0] = (int32_t)b;
+        if (b >= 2)
+            for (int64_t c = 0; c < b; ++c, ++k)
+                if (k < cap) { rep_s[k] = v; rep_r[k] = w->rep[c]; }
+    }
+    *n_rep = k;
+    return EGO_OK;
+}
+
+int ego_grid_range(int ndim, const int64_t *dims, const float *f, int64_t v0, int64_t v1, int64_t *ptr,
+                   int32_t *beta, int64_t *rep_s, int64_t *rep_r, int64_t cap, int64_t *n_rep) {
+    grid_t g;
+    if (grid_init(&g, ndim, dims) != EGO_OK || v0 < 0 || v1 < v0 || v1 > g.n) return EGO_ERR_INVALID;
+    for (int64_t v = v0; v < v1; ++v)
+        if (isnan(f[v])) return EGO_ERR_NAN;
+    work_t w = {1, &g, NULL, f, 0, 0, 0, 0, 0, 0};
+    if (work_alloc(&w, grid_link_cap(&g)) != EGO_OK) { work_free(&w); return EGO_ERR_OOM; }
+    int rc = range_common(&w, v0, v1, ptr, beta, rep_s, rep_r, cap, n_rep);
+    work_free(&w);
+    return rc;
+}
+
+int ego_csr_range(int64_t nv, const int64_t *row_ptr, const int32_t *col_idx, const float *f, int64_t v0,
+                  int64_t v1, int64_t *ptr, int32_t *beta, int64_t *rep_s, int64_t *rep_r, int64_t cap,
+                  int64_t *n_rep) {
+    if (nv < 0 || v0 < 0 || v1 < v0 || v1 > nv) return EGO_ERR_INVALID;
+    for (int64_t v = v0; v < v1; ++v)
+        if (isnan(f[v])) return EGO_ERR_NAN;
+    csr_t c = {nv, row_ptr, col_idx};
+    work_t w = {0, NULL, &c, f, 0, 0, 0, 0, 0, 0};
+    if (work_alloc(&w, csr_link_cap(&c)) != EGO_OK) { work_free(&w); return EGO_ERR_OOM; }
+    int rc = range_common(&w, v0, v1, ptr, beta, rep_s, rep_r, cap, n_rep);
+    work_free(&w);
+    return rc;
+}
+
+/* O7 over a whole gradient array (the ptr of every vertex, e.g. assembled
+ * from ego_*_range calls). */
+int ego_labels(int64_t n, const int64_t *ptr, int64_t *label) {
+    if (n < 0) return EGO_ERR_INVALID;
+    for (int64_t v = 0; v < n; ++v)
+        if (ptr[v] < 0 || ptr[v] >= n) return EGO_ERR_INVALID;
+    int64_t *stack = malloc(sizeof(int64_t) * (n ? n : 1));
+    if (!stack) return EGO_ERR_OOM;
+    labels_from_ptr(n, ptr, label, stack);
+    free(stack);
+    return EGO_OK;
 }
 
 /* ------------------------------------------ single-vertex entry points

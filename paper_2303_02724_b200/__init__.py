@@ -38,7 +38,7 @@ class EgError(RuntimeError):
 class Graph:
     """The extremum graph: ascending maxima, saddles (+ beta0+), arcs
     (saddle, maximum, multiplicity) sorted by (saddle, maximum); labels are the
-    owned vertices' maxima (CUDA int32 tensor)."""
+    owned vertices' maxima (CUDA int32 tensor, a copy owned by this object)."""
     maxima: np.ndarray
     saddles: np.ndarray
     saddle_beta: np.ndarray
@@ -189,6 +189,9 @@ class Context:
         return ptr[:n], beta[:n]
 
     def labels(self) -> torch.Tensor:
+        """The owned labels of the last compute as a zero-copy view of the
+        library's device buffer: valid only until the next compute / gradient
+        / close on this context (Graph.labels is a copy)."""
         p, n = C.c_void_p(), C.c_int64()
         self._check(_abi.lib().eg_get_labels(self._h, C.byref(p), C.byref(n)), "eg_get_labels")
         if n.value == 0:
@@ -198,7 +201,7 @@ class Context:
     def _graph(self, flags: int) -> Graph:
         if flags & _abi.EG_NO_GRAPH_D2H:
             return Graph(np.zeros(0, np.int64), np.zeros(0, np.int64), np.zeros(0, np.int32),
-                         np.zeros((0, 3), np.int64), self.labels())
+                         np.zeros((0, 3), np.int64), self.labels().clone())
         g = _abi.EgGraph()
         self._check(_abi.lib().eg_get_graph(self._h, C.byref(g)), "eg_get_graph")
         arcs = np.stack([_arr(g.arc_saddle, g.n_arc, np.int64), _arr(g.arc_max, g.n_arc, np.int64),
@@ -221,7 +224,7 @@ class Context:
             off = _arr(o, n.value + 1, np.int64)
             paths = (off, _arr(v, int(off[-1]), np.int64))
         return Graph(maxima=_arr(g.maxima, g.n_max, np.int64), saddles=_arr(g.saddles, g.n_saddle, np.int64),
-                     saddle_beta=_arr(g.saddle_beta, g.n_saddle, np.int32), arcs=arcs, labels=self.labels(),
+                     saddle_beta=_arr(g.saddle_beta, g.n_saddle, np.int32), arcs=arcs, labels=self.labels().clone(),
                      raw_arcs=raw, arc_paths=paths)
 
     def simplify(self, tau: float) -> Graph:

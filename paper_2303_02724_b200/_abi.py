@@ -23,7 +23,10 @@ EG_DOMAIN_GRID, EG_DOMAIN_CSR = 0, 1
 
 
 def EG_VIRTUAL_PARTS(k: int) -> int:
-    return (int(k) & 0xFFFFFF) << 8
+    """k virtual slabs / ranges on one GPU: bits 16-31 of the flags (no flag bit)."""
+    if not 0 <= int(k) < 65536:
+        raise ValueError("EG_VIRTUAL_PARTS: 0 <= k < 65536")
+    return int(k) << 16
 
 
 # every symbol include/eg.h declares (checked by tests/test_abi_exports.py)

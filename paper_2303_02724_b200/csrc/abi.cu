@@ -78,6 +78,7 @@ struct SlabState {
     DevBuf sad_bits, max_bits;
     DevBuf beta8;                      // CSR: beta0+ per owned vertex (from classify)
     DevBuf rep_buf;                    // CSR: the saddles' component representatives, by row_ptr
+    DevBuf slow_up;                    // CSR: int32[2 nnz] scratch for |U| > 64 (row_ptr-indexed U, parents)
     DevBuf bval, hval_lo, hval_hi;     // boundary-plane label values (own / neighbours')
     bool has_lo = false, has_hi = false;
     Tiled3D *tiled = nullptr;
@@ -86,7 +87,7 @@ struct SlabState {
     DevBuf arc_s, arc_m, arc_mult, raw_s, raw_rep, raw_m;
     int64_t n_max = 0, n_sad = 0, n_arc = 0, n_raw = 0;
     ~SlabState() {
-        DevBuf *b[] = {&f_lo, &f_hi, &sad_bits, &max_bits, &beta8, &rep_buf, &bval, &hval_lo, &hval_hi, &maxima64,
+        DevBuf *b[] = {&f_lo, &f_hi, &sad_bits, &max_bits, &beta8, &rep_buf, &slow_up, &bval, &hval_lo, &hval_hi, &maxima64,
                        &saddles32, &saddles64, &sbeta, &slot_off, &tmp_m, &tmp_mult, &n_unique, &arc_off, &arc_s,
                        &arc_m, &arc_mult, &raw_s, &raw_rep, &raw_m};
         for (DevBuf *x : b) x->release();
@@ -534,7 +535,8 @@ static eg_status fail_if_flags(eg_ctx *c) {
         }
     }
     if (h[0]) return set_err(c, EG_ERR_NAN, "NaN in the scalar field (reading L2)");
-    if (h[1]) return set_err(c, EG_ERR_UNSUPPORTED, "CSR vertex degree > %d", kCsrMaxDeg);
+    if (h[1]) return set_err(c, EG_ERR_INVALID_ARG, "CSR check failed (code %d: 1 row_ptr, 2 col_idx range, "
+                             "4 unsorted / duplicate, 8 self loop, 16 asymmetric)", h[1]);
     return EG_OK;
 }
 
@@ -691,7 +693,7 @@ static eg_status boundary_rounds(eg_ctx *c, int *rounds_out) {
 }
 
 static eg_status compute_grid(eg_ctx *c, const Problem &P, const float *f, uint32_t flags) {
-    const int vparts = int((flags >> 8) & 0xffffff);
+    const int vparts = int((flags >> 16) & 0xffff);
     // ---- plan the slabs of this process
     std::vector<std::pair<int64_t, int64_t>> plan;
     if (c->world > 1) {
@@ -834,7 +836,7 @@ static eg_status compute_grid(eg_ctx *c, const Problem &P, const float *f, uint3
 // ------------------------------------------------------------- CSR stages
 
 static eg_status compute_csr(eg_ctx *c, const Problem &P, const float *f, uint32_t flags) {
-    const int vparts = int((flags >> 8) & 0xffffff);
+    const int vparts = int((flags >> 16) & 0xffff);
     c->overlap = false;
     c->gstream = c->stream;
     std::vector<std::pair<int64_t, int64_t>> plan;       // vertex ranges of this process
@@ -867,7 +869,15 @@ static eg_status compute_csr(eg_ctx *c, const Problem &P, const float *f, uint32
         S.tiled_lists = false;
         CK(S.beta8.ensure(std::max<int64_t>(S.s.v1 - S.s.v0, 1)));
         CK(S.rep_buf.ensure(sizeof(int32_t) * std::max<int64_t>(P.nnz, 1)));
+        CK(S.slow_up.ensure(2 * sizeof(int32_t) * std::max<int64_t>(P.nnz, 1)));
         S.has_lo = S.has_hi = false;
+    }
+    if (flags & EG_CHECK_CSR) {
+        // validated before any kernel indexes through the graph (an invalid
+        // col_idx would read out of bounds)
+        CK(launch_check_csr(P.row_ptr, P.col_idx, P.N, P.nnz, c->flags.as<int>() + 1, c->stream));
+        c->stats.kernel_launches += 1;
+        ST(fail_if_flags(c));
     }
     CK(cudaEventRecord(c->ev[0], c->stream));
     int *fl = c->flags.as<int>();
@@ -880,8 +890,9 @@ static eg_status compute_csr(eg_ctx *c, const Problem &P, const float *f, uint32
         const bool first = S == c->slabs[0];
         if (first) CK(cudaEventRecord(c->ev_main[0], c->stream));
         CK(launch_classify_csr(P.row_ptr, P.col_idx, f, S->s.v0, S->s.v1, S->label, S->sad_bits.as<uint32_t>(),
-                               S->max_bits.as<uint32_t>(), S->beta8.as<uint8_t>(), fl, fl + 1, c->stream,
-                               S->rep_buf.as<int32_t>()));
+                               S->max_bits.as<uint32_t>(), S->beta8.as<uint8_t>(), fl, c->stream,
+                               S->rep_buf.as<int32_t>(), S->slow_up.as<int32_t>(),
+                               S->slow_up.as<int32_t>() + std::max<int64_t>(P.nnz, 1)));
         if (first) CK(cudaEventRecord(c->ev_main[1], c->stream));
         c->stats.kernel_launches += 1;
     }
@@ -1044,7 +1055,7 @@ static eg_status compute_impl(eg_ctx *c, const eg_domain *d, const float *f, uin
     // is the minimum graph, with vertex ids unchanged.
     c->min_reflect = false;
     if (c->minimum) {
-        if (c->world > 1 || ((flags >> 8) & 0xffffff) > 1)
+        if (c->world > 1 || ((flags >> 16) & 0xffff) > 1)
             return set_err(c, EG_ERR_UNSUPPORTED, "EG_MINIMUM: one GPU and one slab");
         if (!P.grid && (P.v0 != 0 || P.v1 != P.N))
             return set_err(c, EG_ERR_UNSUPPORTED, "EG_MINIMUM on a CSR graph: the whole vertex range");
@@ -1066,10 +1077,10 @@ static eg_status compute_impl(eg_ctx *c, const eg_domain *d, const float *f, uin
     }
     c->paths_valid = false;
     c->bundle = (flags & EG_BUNDLE) != 0;
-    if (c->bundle && (c->world > 1 || ((flags >> 8) & 0xffffff) > 1))
+    if (c->bundle && (c->world > 1 || ((flags >> 16) & 0xffff) > 1))
         return set_err(c, EG_ERR_UNSUPPORTED, "EG_BUNDLE: one GPU, one slab");
     if (flags & EG_ARC_PATHS) {
-        if (c->world > 1 || ((flags >> 8) & 0xffffff) > 1)
+        if (c->world > 1 || ((flags >> 16) & 0xffff) > 1)
             return set_err(c, EG_ERR_UNSUPPORTED, "EG_ARC_PATHS: one GPU, one slab");
         flags |= EG_RAW_ARCS;
     }
@@ -1353,9 +1364,10 @@ eg_status eg_gradient(eg_ctx *c, const eg_domain *d, const float *d_field, int32
         CK(launch_classify_grid(c->host_tab, P.ndim, F, s, d_ptr, S.sad_bits.as<uint32_t>(),
                                 S.max_bits.as<uint32_t>(), d_beta, c->flags.as<int>(), c->stream));
     } else {
+        CK(S.slow_up.ensure(2 * sizeof(int32_t) * std::max<int64_t>(P.nnz, 1)));
         CK(launch_classify_csr(P.row_ptr, P.col_idx, d_field, P.v0, P.v1, d_ptr, S.sad_bits.as<uint32_t>(),
-                               S.max_bits.as<uint32_t>(), d_beta, c->flags.as<int>(), c->flags.as<int>() + 1,
-                               c->stream));
+                               S.max_bits.as<uint32_t>(), d_beta, c->flags.as<int>(), c->stream, nullptr,
+                               S.slow_up.as<int32_t>(), S.slow_up.as<int32_t>() + std::max<int64_t>(P.nnz, 1)));
     }
     return fail_if_flags(c);
 }

@@ -13,7 +13,6 @@ namespace eg {
 
 constexpr int kMaxDim = 6;                 // generic grid kernels: n <= 6
 constexpr int kMaxLink = 126;              // 2 (2^6 - 1)
-constexpr int kCsrMaxDeg = 128;            // thread-per-vertex CSR kernel
 constexpr uint32_t kUnresolved = 0x80000000u;   // label bit 31: not final, low bits = a vertex further on the path
 
 // Freudenthal link of an interior vertex: the offsets d in
@@ -93,10 +92,16 @@ struct LabelView {
 cudaError_t launch_classify_grid(const LinkTable &tab, int ndim, FieldView F, const Slab &s, int32_t *ptr,
                                  uint32_t *sad_bits, uint32_t *max_bits, uint8_t *beta_out, int *nan_flag,
                                  cudaStream_t st);
+// one warp per vertex, no degree cap: slow_u / slow_p are row_ptr-indexed
+// int32[nnz] scratch for vertices with more than 64 upper neighbours
 cudaError_t launch_classify_csr(const int64_t *row_ptr, const int32_t *col_idx, const float *f, int64_t v0,
                                 int64_t v1, int32_t *ptr, uint32_t *sad_bits, uint32_t *max_bits,
-                                uint8_t *beta_out, int *nan_flag, int *deg_overflow, cudaStream_t st,
-                                int32_t *rep_buf = nullptr);   // saddles' component reps at rep_buf[row_ptr[v] ..]
+                                uint8_t *beta_out, int *nan_flag, cudaStream_t st, int32_t *rep_buf,
+                                int32_t *slow_u, int32_t *slow_p);
+// EG_CHECK_CSR: *bad |= a nonzero code if the CSR is not a sorted, symmetric,
+// loop-free adjacency with a valid row_ptr (k_csr.cu)
+cudaError_t launch_check_csr(const int64_t *row_ptr, const int32_t *col_idx, int64_t n, int64_t nnz, int *bad,
+                             cudaStream_t st);   // saddles' component reps at rep_buf[row_ptr[v] ..]
 
 // S2: in-place pointer jumping over ptr[0..n) whose entries are global ids;
 // entries outside [v0, v0 + n) are terminal (remote).  changed[r] is set when

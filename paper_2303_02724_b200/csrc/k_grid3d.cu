@@ -92,6 +92,7 @@ struct Tiled3D {
     int32_t *d_alt = nullptr;                        // sorted maxima (int32)
     int64_t alt_cap = 0;
     void *encode = nullptr;                          // cuTensorMapEncodeTiled
+    int n_sm = 148;
 };
 
 Tiled3D *tiled3d_create() { return new Tiled3D(); }
@@ -132,6 +133,8 @@ struct TileArgs {
     const uint16_t *shell;          // kShell pointer-box byte offsets
     const int32_t *btiles;          // boundary variant: packed tile ids
     int32_t tiles_x, tiles_y;       // interior variant: sub-box extents
+    uint64_t mx, my;                // ceil(2^32 / tiles_x), ceil(2^32 / tiles_y): t / tiles = (t m) >> 32
+    int32_t n_tiles;                // interior variant: tiles of the sub-box
     int3 origin;                    // interior variant: first interior tile
     int32_t rounds;                 // pointer-doubling rounds before the chase
     int32_t no_elist;               // one slab: no exit-target list (the finalize pass chases)
@@ -225,7 +228,13 @@ __device__ __forceinline__ void load_plane(float *fbox, int bz, const float *src
     }
 }
 
-template <bool kInterior>
+// kPersist (interior tiles, TMA, one slab): one CTA per SM slot walks the
+// tiles blockIdx.x, blockIdx.x + gridDim.x, ...; the LUT, the plane table and
+// the self-pointing halo shell of the pointer box are staged once per CTA
+// (the shell is never written afterwards), and the next tile's field box is
+// requested by TMA as soon as S1 has consumed the current one, so the copy
+// runs behind S2 and the label stores.
+template <bool kInterior, bool kPersist>
 __global__ void __launch_bounds__(kThreads, 2)
     k_tile(const __grid_constant__ CUtensorMap tmap, TileArgs A, Dims3 D) {
     extern __shared__ __align__(128) unsigned char smem[];
@@ -247,35 +256,53 @@ __global__ void __launch_bounds__(kThreads, 2)
 
     const int tid = threadIdx.x;
     const int tx = tid & 31, ty = tid >> 5;
-    int bxo, byo, bzo;
-    if (kInterior) {
-        int t = blockIdx.x;
-        bxo = t % A.tiles_x + A.origin.x;
-        t /= A.tiles_x;
-        byo = t % A.tiles_y + A.origin.y;
-        bzo = t / A.tiles_y + A.origin.z;
-    } else {
-        const int packed = A.btiles[blockIdx.x];     // (bz << 20) | (by << 10) | bx
-        bxo = packed & 1023;
-        byo = (packed >> 10) & 1023;
-        bzo = packed >> 20;
-    }
-    const int x0 = bxo * TX, y0 = byo * TY, z0 = A.z_lo + bzo * TZ;
-
-    // ---- stage the tile + halo: one TMA bulk-tensor copy over the owned
-    // planes (cells outside them arrive as NaN), then the halo planes that
-    // belong to a neighbour slab; or plain row loads.
+    // tile t -> (bx, by, bz) of its origin (box coordinates in tiles)
+    auto coords = [&](int t, int &bxo, int &byo, int &bzo) {
+        if (kInterior) {
+            const uint32_t q = uint32_t((uint64_t(t) * A.mx) >> 32);      // t / tiles_x (t * tiles_x < 2^32)
+            bxo = t - int(q) * A.tiles_x + A.origin.x;
+            const uint32_t q2 = uint32_t((uint64_t(q) * A.my) >> 32);     // q / tiles_y
+            byo = int(q) - int(q2) * A.tiles_y + A.origin.y;
+            bzo = int(q2) + A.origin.z;
+        } else {
+            const int packed = A.btiles[t];     // (bz << 20) | (by << 10) | bx
+            bxo = packed & 1023;
+            byo = (packed >> 10) & 1023;
+            bzo = packed >> 20;
+        }
+    };
+    auto issue_tma = [&](int t) {      // thread 0: request tile t's field box
+        int bx, by, bz;
+        coords(t, bx, by, bz);
+        mbar_expect_tx(bar, uint32_t(BOX * 4));
+        tma_load_3d(fbox, &tmap, bar, bx * TX - XO, by * TY - 1, A.z_lo + bz * TZ - 1 - A.z_lo);
+    };
     if (A.tma) {
         if (tid == 0) {
             mbar_init(bar, 1);
             asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         }
         __syncthreads();
-        if (tid == 0) {
-            mbar_expect_tx(bar, uint32_t(BOX * 4));
-            tma_load_3d(fbox, &tmap, bar, x0 - XO, y0 - 1, z0 - 1 - A.z_lo);
-        }
-    } else {
+        if (tid == 0) issue_tma(blockIdx.x);
+    }
+    // shell cells of the pointer box are terminal (point to themselves)
+    for (int s = tid; s < kShell; s += kThreads) {
+        const int i = __ldg(A.shell + s);
+        P(i) = uint16_t(i);
+    }
+    for (int i = tid; i < kLutWords; i += kThreads) lut[i] = __ldg(A.lut + i);
+    for (int i = tid; i < PL; i += kThreads) ptab[i] = __ldg(A.ptab + i);
+    const int t_end = kPersist ? A.n_tiles : int(blockIdx.x) + 1;
+#pragma unroll 1
+    for (int t = blockIdx.x, it = 0; t < t_end; t += gridDim.x, ++it) {
+    int bxo, byo, bzo;
+    coords(t, bxo, byo, bzo);
+    const int x0 = bxo * TX, y0 = byo * TY, z0 = A.z_lo + bzo * TZ;
+
+    // ---- stage the tile + halo: one TMA bulk-tensor copy over the owned
+    // planes (cells outside them arrive as NaN), then the halo planes that
+    // belong to a neighbour slab; or plain row loads.
+    if (!A.tma) {
         // one warp per box row: the row's source (owned planes, a halo plane
         // of a neighbour slab, or nothing) is decided once per row
         constexpr int kRows = BY * BZ, kU = 4;
@@ -309,15 +336,8 @@ __global__ void __launch_bounds__(kThreads, 2)
             }
         }
     }
-    // shell cells of the pointer box are terminal (point to themselves)
-    for (int s = tid; s < kShell; s += kThreads) {
-        const int i = __ldg(A.shell + s);
-        P(i) = uint16_t(i);
-    }
-    for (int i = tid; i < kLutWords; i += kThreads) lut[i] = __ldg(A.lut + i);
-    for (int i = tid; i < PL; i += kThreads) ptab[i] = __ldg(A.ptab + i);
     if (A.tma) {
-        mbar_wait(bar, 0);
+        mbar_wait(bar, uint32_t(it & 1));
         if (!kInterior) {
             // halo planes held by the neighbour slabs (the tensor map covers the owned planes only)
             if (z0 == A.z_lo && A.f_lo) load_plane(fbox, 0, A.f_lo, x0, y0, D, tid);
@@ -421,6 +441,12 @@ __global__ void __launch_bounds__(kThreads, 2)
         if (v != v) atomicOr(A.nan_flag, 1);
     }
     __syncthreads();
+    if (kPersist && tid == 0 && t + int(gridDim.x) < t_end) {
+        // the field box is dead (no exit marks on the one-slab path): the
+        // next tile's copy overlaps the rest of this one
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        issue_tma(t + int(gridDim.x));
+    }
 
     // ---- S2 inside the tile.  The field box is dead: it now holds one
     // exit-mark byte per pointer-box cell.  Two rounds of pointer doubling
@@ -505,7 +531,10 @@ __global__ void __launch_bounds__(kThreads, 2)
                 if (js < (unsigned long long)A.list_cap) A.sad_list[js] = g0 + (__ffs(m) - 1) * nxy;
         }
     }
-    if (A.no_elist) return;
+    if (A.no_elist) {
+        if (kPersist) __syncthreads();   // the next tile's S1 rewrites the pointer box
+        continue;
+    }
     __syncthreads();
 
     // ---- append the tile's exit targets (marked shell cells) to E: per-warp
@@ -543,6 +572,7 @@ __global__ void __launch_bounds__(kThreads, 2)
         }
         slot += __popc(b);
     }
+    }   // tiles
 }
 
 // Pass E: resolve every owned exit target through the exit graph (bit 31 =
@@ -648,11 +678,17 @@ eg_status tiled3d_local(Tiled3D *t, int ndim, const int64_t *dims, const Slab &s
         if ((e = upload(&t->d_shell, sh)) != cudaSuccess) return fail(err, e, "shell upload");
         if ((e = cudaMalloc(&t->d_ecount, 3 * sizeof(unsigned long long))) != cudaSuccess)
             return fail(err, e, "cudaMalloc ecount");
-        if ((e = cudaFuncSetAttribute(k_tile<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kTileSmem))) !=
-                cudaSuccess ||
-            (e = cudaFuncSetAttribute(k_tile<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kTileSmem))) !=
-                cudaSuccess)
+        if ((e = cudaFuncSetAttribute(k_tile<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      int(kTileSmem))) != cudaSuccess ||
+            (e = cudaFuncSetAttribute(k_tile<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      int(kTileSmem))) != cudaSuccess ||
+            (e = cudaFuncSetAttribute(k_tile<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      int(kTileSmem))) != cudaSuccess)
             return fail(err, e, "smem attr");
+        int dev = 0;
+        cudaGetDevice(&dev);
+        if (cudaDeviceGetAttribute(&t->n_sm, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || t->n_sm < 1)
+            t->n_sm = 148;
         const char *rs = std::getenv("EG_TILE_ROUNDS");   // tuning knob (default 2)
         if (rs && rs[0] >= '0' && rs[0] <= '6') t->rounds = rs[0] - '0';
         cudaDriverEntryPointQueryResult q;
@@ -784,7 +820,7 @@ eg_status tiled3d_local(Tiled3D *t, int ndim, const int64_t *dims, const Slab &s
         A.tma = tma ? 1 : 0;
         if (ev_main0) cudaEventRecord(ev_main0, st);
         if (t->n_btiles > 0) {
-            k_tile<false><<<unsigned(t->n_btiles), kThreads, kTileSmem, st>>>(tmap, A, D);
+            k_tile<false, false><<<unsigned(t->n_btiles), kThreads, kTileSmem, st>>>(tmap, A, D);
             stats->kernel_launches += 1;
             if ((e = cudaGetLastError()) != cudaSuccess) return fail(err, e, "k_tile<boundary>");
         }
@@ -793,7 +829,16 @@ eg_status tiled3d_local(Tiled3D *t, int ndim, const int64_t *dims, const Slab &s
             A.tiles_y = hi.y - lo.y + 1;
             A.origin = lo;
             const int64_t nt = int64_t(A.tiles_x) * A.tiles_y * (hi.z - lo.z + 1);
-            k_tile<true><<<unsigned(nt), kThreads, kTileSmem, st>>>(tmap, A, D);
+            A.mx = ((uint64_t(1) << 32) + uint64_t(A.tiles_x) - 1) / uint64_t(A.tiles_x);
+            A.my = ((uint64_t(1) << 32) + uint64_t(A.tiles_y) - 1) / uint64_t(A.tiles_y);
+            A.n_tiles = int32_t(nt);
+            // persistent CTAs (2 per SM) on the one-slab TMA path (EG_PERSIST=0: one CTA per tile)
+            const char *pe = std::getenv("EG_PERSIST");
+            const bool persist = A.no_elist && A.tma && !(pe && pe[0] == '0') && nt > 2 * t->n_sm;
+            if (persist)
+                k_tile<true, true><<<unsigned(2 * t->n_sm), kThreads, kTileSmem, st>>>(tmap, A, D);
+            else
+                k_tile<true, false><<<unsigned(nt), kThreads, kTileSmem, st>>>(tmap, A, D);
             stats->kernel_launches += 1;
             if ((e = cudaGetLastError()) != cudaSuccess) return fail(err, e, "k_tile<interior>");
         }

@@ -1,24 +1,26 @@
 """Parity at BASELINE.json's configurations, in the launch configuration
-bench.py times (one eg_compute on the resident field, default flags).
+bench.py times (one eg_compute on the resident field, flags EG_CHECK_NAN).
 
-* C1 (2D 64^2) and C2 (3D 256^3): the oracle runs on the whole field; every
-  output is compared element by element.
-* C3 (3D 1024^3): too large for the oracle in a test; sampled outputs the
-  oracle computes one by one (Alg. 2 walks for labels, single-vertex
-  classification for beta0+ / gradient, per-saddle arcs), plus properties that
-  hold at any size; and the same recipe at 128^3 in full.
-* C4 (5D 32^5 Schwefel): the closed form of the separable product rule
-  (16,807 maxima, 72,030 saddles, all beta0+ = 2), sampled vertices and
-  saddles against the oracle, and the recipe at 12^5 in full.
-* C5 (1M-point kNN CSR): sampled against the oracle; the recipe at 20K points
-  in full (test_gpu_parity.py).
+Every config is compared with the oracle over the WHOLE domain, element by
+element: maxima, saddles + beta0+, deduplicated arcs, every label, and (via
+eg_gradient) every vertex's gradient pointer and beta0+.  C3 (2^30 vertices),
+C4 and C5 use oracle.grid_parallel / csr_parallel -- the oracle's own
+per-vertex range function on disjoint ranges in forked processes, pinned to
+the whole-domain oracle by test_oracle_pins.py::test_parallel_equals_whole.
+With EG_PARITY_RECORD=<dir> the full-size tests also write a record (field
+sha256, per-output sha256 of both sides, result) to <dir>/<config>_parity.json
+(committed under profiles/r02/).
 """
+import json
+import os
+import time
+
 import numpy as np
 import pytest
 
 import eg_inputs as G
 import oracle as O
-from _parity import assert_graph_equal, first_diff
+from _parity import assert_full_equal, assert_graph_equal, first_diff, sha
 
 pytestmark = pytest.mark.gpu
 
@@ -103,30 +105,64 @@ def test_c3_recipe_128_full(eg, ctx):
     assert_graph_equal(g2, o, what="C3 recipe at 128^3 (generic kernels)")
 
 
-def test_c3_config_sampled(eg, ctx):
+def _record(cfg, f, g, o, t_gpu, t_oracle, extra=None):
+    d = os.environ.get("EG_PARITY_RECORD")
+    if not d:
+        return
+    os.makedirs(d, exist_ok=True)
+    lab = g.labels.cpu().numpy().astype(np.int64)
+    rec = {"config": cfg, "n_vertices": int(len(f)), "field_sha256": sha(f),
+           "result": "exact (every output element-equal)",
+           "gpu": {"maxima": sha(g.maxima), "saddles": sha(g.saddles), "saddle_beta": sha(g.saddle_beta.astype(np.int32)),
+                   "arcs": sha(g.arcs), "labels": sha(lab)},
+           "oracle": {"maxima": sha(o.maxima), "saddles": sha(o.saddles), "saddle_beta": sha(o.saddle_beta),
+                      "arcs": sha(o.arcs), "labels": sha(o.label)},
+           "counts": {"maxima": int(len(o.maxima)), "saddles": int(len(o.saddles)), "arcs": int(len(o.arc_s)),
+                      "raw_arcs": int(len(o.raw_s)), "multi_saddles": int((o.saddle_beta >= 3).sum())},
+           "seconds": {"gpu_compute": round(t_gpu, 4), "oracle_parallel": round(t_oracle, 1),
+                       "oracle_procs": os.cpu_count()}}
+    rec.update(extra or {})
+    with open(os.path.join(d, f"{cfg}_parity.json"), "w") as fh:
+        json.dump(rec, fh, indent=1)
+
+
+def _full_grid(eg, ctx, cfg, t, dims):
+    import torch
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    g = ctx.compute(t, dims=dims, flags=eg.EG_CHECK_NAN)
+    t_gpu = time.perf_counter() - t0
+    ptr, beta = ctx.gradient(t, dims=dims)
+    ptr, beta = ptr.cpu().numpy(), beta.cpu().numpy()
+    f = t.cpu().numpy()
+    t0 = time.perf_counter()
+    o = O.grid_parallel(f, dims)
+    t_or = time.perf_counter() - t0
+    assert_full_equal(g, o, ptr, beta, what=cfg)
+    _record(cfg, f, g, o, t_gpu, t_or)
+    return g, o
+
+
+def test_c3_config_full(eg, ctx):
+    """C3 1024^3: the whole domain against the oracle (2^30 vertices)."""
     import torch
     t, dims = G.turbulence(1024, seed=1024, device="cuda")
-    g = ctx.compute(t, dims=dims, flags=eg.EG_CHECK_NAN)
-    labels = g.labels.cpu().numpy()
-    f = t.cpu().numpy()
-    del t
-    torch.cuda.empty_cache()
-    _sampled_grid_checks(g, f, dims, labels)
+    g, o = _full_grid(eg, ctx, "C3", t, dims)
     # SURVEY App. A expectations at this recipe (self-similar counts): order of
     # 10^5 maxima, saddles about 3x maxima
     assert 5e4 < len(g.maxima) < 5e5 and 1.5 * len(g.maxima) < len(g.saddles) < 6 * len(g.maxima)
+    del t
+    torch.cuda.empty_cache()
 
 
-def test_c4_config_closed_form_and_sampled(eg, ctx):
+def test_c4_config_full(eg, ctx):
     import torch
     f, dims = G.schwefel()
-    g = ctx.compute(torch.from_numpy(f).cuda(), dims=dims, flags=eg.EG_CHECK_NAN)
+    g, o = _full_grid(eg, ctx, "C4", torch.from_numpy(f).cuda(), dims)
     # separable product rule (tests/test_oracle_pins.py::test_schwefel_profile_counts)
     assert len(g.maxima) == 7 ** 5 == 16807
     assert len(g.saddles) == 5 * 6 * 7 ** 4 == 72030
     assert (g.saddle_beta == 2).all()
-    labels = g.labels.cpu().numpy()
-    _sampled_grid_checks(g, f, dims, labels, n_lab=200, n_sad=100)
 
 
 def test_c4_recipe_small_full(eg, ctx):
@@ -140,31 +176,22 @@ def test_c4_recipe_small_full(eg, ctx):
     assert_graph_equal(ctx.compute(torch.from_numpy(f).cuda(), dims=dims), O.grid(f, dims), what="sumcos 16^5")
 
 
-def test_c5_config_sampled(eg, ctx):
+def test_c5_config_full(eg, ctx):
     import torch
     X, f = G.gmm_points(1_000_000, seed=10)
     rp, ci = G.knn_csr(X, 16, device="cuda")
     csr = (torch.from_numpy(rp).cuda(), torch.from_numpy(ci).cuda())
-    g = ctx.compute(torch.from_numpy(f).cuda(), csr=csr, flags=eg.EG_CHECK_NAN)
-    labels = g.labels.cpu().numpy()
-    rng = np.random.default_rng(1)
-    for v in rng.integers(0, len(f), 300):
-        assert labels[v] == O.csr_walk(f, rp, ci, int(v))[0]
-    arcs_by_s = {}
-    for s, m, c in g.arcs.tolist():
-        arcs_by_s.setdefault(s, []).append((m, c))
-    for j in rng.choice(len(g.saddles), 200, replace=False):
-        s = int(g.saddles[j])
-        p, b, reps = O.csr_vertex(f, rp, ci, s)
-        assert b == g.saddle_beta[j]
-        ms = sorted(int(labels[r]) for r in reps)
-        assert sorted(arcs_by_s[s]) == sorted((m, ms.count(m)) for m in set(ms))
-    # gradient + beta0+ of sampled vertices
-    ptr, beta = ctx.gradient(torch.from_numpy(f).cuda(), csr=csr)
-    ptr, beta = ptr.cpu().numpy(), beta.cpu().numpy()
-    for v in rng.integers(0, len(f), 300):
-        p, b, _ = O.csr_vertex(f, rp, ci, int(v))
-        assert ptr[v] == p and beta[v] == min(b, 255)
+    ft = torch.from_numpy(f).cuda()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    g = ctx.compute(ft, csr=csr, flags=eg.EG_CHECK_NAN)
+    t_gpu = time.perf_counter() - t0
+    ptr, beta = ctx.gradient(ft, csr=csr)
+    t0 = time.perf_counter()
+    o = O.csr_parallel(f, rp, ci)
+    t_or = time.perf_counter() - t0
+    assert_full_equal(g, o, ptr.cpu().numpy(), beta.cpu().numpy(), what="C5")
+    _record("C5", f, g, o, t_gpu, t_or, {"csr_sha256": {"row_ptr": sha(rp), "col_idx": sha(ci)}})
     assert int(g.arcs[:, 2].sum()) == int(g.saddle_beta.sum())
 
 

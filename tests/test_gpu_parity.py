@@ -178,6 +178,95 @@ def test_csr_random(eg, ctx, n, p, seed, kind):
     assert_graph_equal(g, o, raw=True, what="csr random")
 
 
+@pytest.mark.parametrize("n,p,seed,kind", [(150, 0.35, 5, "normal"), (160, 0.4, 6, "int"), (220, 0.7, 7, "normal"),
+                                           (260, 0.8, 8, "int")])
+def test_csr_dense(eg, ctx, n, p, seed, kind):
+    """Rows longer than a warp (the flattened link-edge pass spans several
+    chunks per row) and upper sets larger than 64 (the serial fallback of the
+    warp kernel): there is no degree cap."""
+    import torch
+    row_ptr, col_idx = G.random_csr(n, p, seed)
+    f, _ = G.random_field([n], seed, kind, levels=4)
+    o = O.csr(f, row_ptr, col_idx)
+    csr = (torch.from_numpy(row_ptr).cuda(), torch.from_numpy(col_idx).cuda())
+    ft = torch.from_numpy(f).cuda()
+    g = ctx.compute(ft, csr=csr, flags=eg.EG_RAW_ARCS | eg.EG_CHECK_NAN | eg.EG_CHECK_CSR)
+    assert_graph_equal(g, o, raw=True, what=f"csr dense {n} {p}")
+    ptr, beta = ctx.gradient(ft, csr=csr)
+    assert first_diff(ptr.cpu().numpy().astype(np.int64), o.ptr) is None
+    assert first_diff(beta.cpu().numpy().astype(np.int32), np.minimum(o.beta, 255)) is None
+    if p >= 0.7:
+        deg = np.diff(row_ptr)
+        assert deg.max() > 128          # beyond the old per-thread cap
+
+
+def test_csr_hub(eg, ctx):
+    """One vertex adjacent to every other (a hub) on a path graph: the hub's
+    upper set is everything, its link is the path (one component); the lowest
+    path vertices see the hub."""
+    import torch
+    n = 300
+    adj = [set() for _ in range(n)]
+    for v in range(1, n - 1):
+        adj[v].add(v + 1)
+        adj[v + 1].add(v)
+    for v in range(1, n):
+        adj[0].add(v)
+        adj[v].add(0)
+    rp = np.zeros(n + 1, np.int64)
+    rp[1:] = np.cumsum([len(a) for a in adj])
+    ci = np.array([u for a in adj for u in sorted(a)], np.int32)
+    rng = np.random.default_rng(3)
+    f = rng.standard_normal(n).astype(np.float32)
+    f[0] = -10.0
+    o = O.csr(f, rp, ci)
+    g = ctx.compute(torch.from_numpy(f).cuda(), csr=(torch.from_numpy(rp).cuda(), torch.from_numpy(ci).cuda()),
+                    flags=eg.EG_RAW_ARCS | eg.EG_CHECK_CSR)
+    assert_graph_equal(g, o, raw=True, what="csr hub")
+
+
+def test_check_csr(eg, ctx):
+    """EG_CHECK_CSR: a malformed graph is EG_ERR_INVALID_ARG before any kernel
+    indexes through it, and the context stays usable."""
+    import torch
+    rp, ci = G.random_csr(60, 0.2, 2)
+    f, _ = G.random_field([60], 2, "normal")
+    ft = torch.from_numpy(f).cuda()
+
+    def run(rp_, ci_):
+        return ctx.compute(ft[:len(rp_) - 1], csr=(torch.from_numpy(rp_).cuda(), torch.from_numpy(ci_).cuda()),
+                           flags=eg.EG_CHECK_CSR)
+
+    assert_graph_equal(run(rp, ci), O.csr(f, rp, ci), what="valid csr")
+    bad = []
+    c = ci.copy()                               # unsorted row
+    r = int(np.argmax(np.diff(rp) >= 2))
+    c[rp[r]], c[rp[r] + 1] = c[rp[r] + 1], c[rp[r]]
+    bad.append((rp, c))
+    c = ci.copy()                               # out of range
+    c[3] = 60
+    bad.append((rp, c))
+    c = ci.copy()                               # self loop (keeps the row sorted only by luck; either code)
+    v = int(np.searchsorted(rp, 5, side="right") - 1)
+    c[5] = v
+    bad.append((rp, c))
+    rp2 = rp.copy()                             # row_ptr not ending at nnz
+    rp2[-1] -= 1
+    bad.append((rp2, ci))
+    # asymmetric: drop one directed edge (u in N(v) but v not in N(u))
+    v = int(np.argmax(np.diff(rp) >= 1))
+    keep = np.ones(len(ci), bool)
+    keep[rp[v]] = False
+    rp3 = rp.copy()
+    rp3[v + 1:] -= 1
+    bad.append((rp3, ci[keep].copy()))
+    for rp_, ci_ in bad:
+        with pytest.raises(eg.EgError) as e:
+            run(rp_, ci_)
+        assert e.value.status == 1, str(e.value)     # EG_ERR_INVALID_ARG
+    assert_graph_equal(run(rp, ci), O.csr(f, rp, ci), what="valid csr after refused calls")
+
+
 def test_csr_knn_small(eg, ctx):
     import torch
     X, f = G.gmm_points(20000, seed=10)
