@@ -327,6 +327,18 @@ def run_ours(args):
                "steps": e_steps, "source": "pinned host memory via eg_compute_host (per rank)"}
         del hf
 
+    # ---- S2 statistics (pointer-jump / chase counts), one extra untimed step (collective)
+    ctx.compute(f, flags=flags | eg.EG_STATS, materialize=False, **kw)
+    st2 = ctx.stats()
+    n_own = int(ctx.labels().numel())
+    s2 = {"tile_rounds": int(st2["tile_rounds"]), "jump_rounds": int(st2["jump_rounds"]),
+          "boundary_rounds": int(st2["boundary_rounds"]),
+          "exit_fraction": round(st2["n_exit"] / max(1, n_own), 4) if st2["path"] == 1 else None,
+          "chase_hist": st2["chase_hist"], "chase_max": int(st2["chase_max"]),
+          "note": "tiled path: in-tile pointer-doubling rounds, fraction of vertices whose in-tile path exits "
+                  "the tile, histogram of exit pointers each exiting vertex's label pass followed (bin 15 = 15+); "
+                  "generic / CSR paths: rounds of the bounded (32-hop) pointer-jumping kernel"}
+
     if rank != 0:
         if world > 1:
             dist.barrier()
@@ -412,10 +424,12 @@ def run_ours(args):
         "roofline_step": {"alg_bytes": int(bytes_alg), "achieved": round(step_gbs, 1), "peak": peak,
                           "frac": round(step_gbs / peak, 4), "unit": "GB/s"},
         "phases_us": {k[3:]: round(float(np.mean([s[k] for s in stats])), 2) for k in
-                      ["us_main", "us_classify", "us_boundary", "us_arcs", "us_graph", "us_total"]},
+                      ["us_main", "us_classify", "us_jump", "us_boundary", "us_label", "us_arcs", "us_graph",
+                       "us_total"]},
         "graph": {"maxima": int(len(g.maxima)), "saddles": int(len(g.saddles)), "arcs": int(len(g.arcs)),
                   "jump_rounds": int(s0["jump_rounds"]), "boundary_rounds": int(s0["boundary_rounds"]),
                   "exit_targets": int(s0["n_exit_targets"])},
+        "s2_stats": s2,
         "gpu_launches": int(launches),
         "clocks": clk,
         "e2e": e2e,

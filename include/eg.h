@@ -94,7 +94,11 @@ typedef struct {
 } eg_graph;
 
 typedef struct {
-    double us_classify, us_jump, us_boundary, us_label, us_arcs, us_graph, us_total;  /* device time */
+    /* device time (us): classify = the per-vertex pass(es); jump = pointer-
+     * jumping rounds (generic / CSR paths); boundary = cross-slab exchange
+     * rounds; label = the tiled path's exit-pointer label pass; arcs, graph
+     * (node lists, arcs and their host copies), total */
+    double us_classify, us_jump, us_boundary, us_label, us_arcs, us_graph, us_total;
     int32_t jump_rounds;            /* pointer-jumping rounds (or exit-graph rounds) */
     int32_t boundary_rounds;        /* cross-partition label rounds              */
     int32_t kernel_launches;        /* kernels launched by the last eg_compute   */
@@ -103,6 +107,15 @@ typedef struct {
     int64_t bytes_alg;              /* algorithmic HBM bytes   */
     double us_main;                 /* device time of the main per-vertex kernel(s) */
     int64_t bytes_main;             /* their algorithmic bytes */
+    /* S2 statistics (the gradient walk).
+     * tile_rounds: pointer-doubling rounds inside a tile (tiled path);
+     * with EG_STATS also: n_exit = vertices whose ascending path leaves their
+     * tile (tiled path); chase_hist[k] = vertices whose label pass followed k
+     * exit pointers (k >= 15 in the last bin), chase_max the longest. */
+    int32_t tile_rounds;
+    int32_t chase_max;
+    int64_t n_exit;
+    int64_t chase_hist[16];
 } eg_stats;
 
 /* eg_compute flags */
@@ -131,7 +144,10 @@ enum {
      * and paths are not filtered.  One GPU, one slab. */
     EG_BUNDLE = 128u,
     /* keep f at every maximum and saddle (for eg_simplify); one process */
-    EG_NODE_VALUES = 256u
+    EG_NODE_VALUES = 256u,
+    /* collect the S2 statistics of eg_stats (exit counts, chase histogram);
+     * costs a few instructions per vertex, so it is off in timed runs */
+    EG_STATS = 1024u
 };
 /* virtual partitions: process a grid as k slabs on one GPU, exchanging
  * boundaries by device copies exactly as k ranks would (partition test). */

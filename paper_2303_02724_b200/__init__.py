@@ -20,12 +20,12 @@ import torch
 
 from . import _abi
 from ._abi import (EG_ARC_PATHS, EG_BUNDLE, EG_NODE_VALUES, EG_CHECK_CSR, EG_CHECK_NAN, EG_FORCE_GENERIC, EG_MINIMUM, EG_NO_GRAPH_D2H,
-                   EG_RAW_ARCS,  # noqa: F401
+                   EG_RAW_ARCS, EG_STATS,  # noqa: F401
                    EG_VIRTUAL_PARTS)
 
 __all__ = ["Context", "Graph", "EgError", "grid_domain", "csr_domain", "EG_CHECK_NAN", "EG_RAW_ARCS",
            "EG_CHECK_CSR", "EG_FORCE_GENERIC", "EG_NO_GRAPH_D2H", "EG_MINIMUM", "EG_ARC_PATHS", "EG_BUNDLE", "EG_NODE_VALUES",
-           "EG_VIRTUAL_PARTS"]
+           "EG_STATS", "EG_VIRTUAL_PARTS"]
 
 
 class EgError(RuntimeError):
@@ -240,7 +240,9 @@ class Context:
     def stats(self) -> dict:
         s = _abi.EgStats()
         self._check(_abi.lib().eg_get_stats(self._h, C.byref(s)), "eg_get_stats")
-        return {k: getattr(s, k) for k, _ in _abi.EgStats._fields_}
+        d = {k: getattr(s, k) for k, _ in _abi.EgStats._fields_}
+        d["chase_hist"] = list(s.chase_hist)
+        return d
 
     def close(self):
         if getattr(self, "_h", None):

@@ -19,7 +19,7 @@ EG_DOMAIN_GRID, EG_DOMAIN_CSR = 0, 1
 (EG_DTYPE_F32, EG_DTYPE_F16, EG_DTYPE_BF16, EG_DTYPE_U8, EG_DTYPE_I8, EG_DTYPE_U16, EG_DTYPE_I16, EG_DTYPE_F64,
  EG_DTYPE_I32, EG_DTYPE_U32, EG_DTYPE_I64, EG_DTYPE_U64) = range(12)
 (EG_CHECK_NAN, EG_RAW_ARCS, EG_CHECK_CSR, EG_FORCE_GENERIC, EG_NO_GRAPH_D2H, EG_MINIMUM, EG_ARC_PATHS,
- EG_BUNDLE, EG_NODE_VALUES) = 1, 2, 4, 8, 16, 32, 64, 128, 256
+ EG_BUNDLE, EG_NODE_VALUES, EG_STATS) = 1, 2, 4, 8, 16, 32, 64, 128, 256, 1024
 
 
 def EG_VIRTUAL_PARTS(k: int) -> int:
@@ -61,7 +61,8 @@ class EgStats(C.Structure):
                 ("us_total", C.c_double), ("jump_rounds", C.c_int32), ("boundary_rounds", C.c_int32),
                 ("kernel_launches", C.c_int32), ("path", C.c_int32), ("n_vertices", C.c_int64),
                 ("n_raw_arcs", C.c_int64), ("n_exit_targets", C.c_int64), ("bytes_alg", C.c_int64),
-                ("us_main", C.c_double), ("bytes_main", C.c_int64)]
+                ("us_main", C.c_double), ("bytes_main", C.c_int64), ("tile_rounds", C.c_int32),
+                ("chase_max", C.c_int32), ("n_exit", C.c_int64), ("chase_hist", C.c_int64 * 16)]
 
 
 _lib = None

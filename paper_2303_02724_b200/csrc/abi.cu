@@ -78,7 +78,6 @@ struct SlabState {
     DevBuf sad_bits, max_bits;
     DevBuf beta8;                      // CSR: beta0+ per owned vertex (from classify)
     DevBuf rep_buf;                    // CSR: the saddles' component representatives, by row_ptr
-    DevBuf slow_up;                    // CSR: int32[2 nnz] scratch for |U| > 64 (row_ptr-indexed U, parents)
     DevBuf bval, hval_lo, hval_hi;     // boundary-plane label values (own / neighbours')
     bool has_lo = false, has_hi = false;
     Tiled3D *tiled = nullptr;
@@ -87,7 +86,7 @@ struct SlabState {
     DevBuf arc_s, arc_m, arc_mult, raw_s, raw_rep, raw_m;
     int64_t n_max = 0, n_sad = 0, n_arc = 0, n_raw = 0;
     ~SlabState() {
-        DevBuf *b[] = {&f_lo, &f_hi, &sad_bits, &max_bits, &beta8, &rep_buf, &slow_up, &bval, &hval_lo, &hval_hi, &maxima64,
+        DevBuf *b[] = {&f_lo, &f_hi, &sad_bits, &max_bits, &beta8, &rep_buf, &bval, &hval_lo, &hval_hi, &maxima64,
                        &saddles32, &saddles64, &sbeta, &slot_off, &tmp_m, &tmp_mult, &n_unique, &arc_off, &arc_s,
                        &arc_m, &arc_mult, &raw_s, &raw_rep, &raw_m};
         for (DevBuf *x : b) x->release();
@@ -107,6 +106,7 @@ struct eg_ctx {
 
     std::vector<SlabState *> slabs;
     DevBuf label_all;                  // labels of every slab of this process
+    DevBuf csr_scratch;                // CSR: int32[2 nnz + N]: upper lists, union-find parents, |U| per vertex
     DevBuf field;                      // eg_compute_host staging target
     DevBuf mirror;                     // EG_MINIMUM: g[i] = -f[N-1-i]
     DevBuf typed;                      // eg_compute_typed: the field converted to float32
@@ -140,6 +140,9 @@ struct eg_ctx {
     eg_stats stats{};
     cudaEvent_t ev[8] = {};
     cudaEvent_t ev_main[2] = {};       // around the main per-vertex kernel(s) of one slab
+    cudaEvent_t ev_s2[6] = {};         // S2 phases: jump rounds [0,1), boundary rounds [2,3), label pass [4,5)
+    bool s2_timed[3] = {false, false, false};
+    DevBuf stat_buf;                   // EG_STATS: [0] exiting vertices, [1..16] chase histogram, [17] max
     // one GPU, one slab: the node lists go to the host on a copy stream while
     // the arcs are computed (ev_d2h[0]: lists ready, [1]: beta ready, [2]: copies done)
     cudaStream_t d2h = nullptr;
@@ -348,6 +351,10 @@ static eg_status generic_local(eg_ctx *c, const Problem &P, SlabState &S, bool m
     // costs a sync.
     int *changed = flags + 2;
     CK(cudaMemsetAsync(changed, 0, sizeof(int) * 64, c->stream));
+    if (timed) {
+        CK(cudaEventRecord(c->ev_s2[0], c->stream));
+        c->s2_timed[0] = true;
+    }
     int rounds = 0;
     const int kBatch = 3;   // bounded chains: one or two rounds usually finish
     int hflag[64];
@@ -369,6 +376,7 @@ static eg_status generic_local(eg_ctx *c, const Problem &P, SlabState &S, bool m
         if (first_zero >= 0) break;
     }
     c->stats.jump_rounds = std::max(c->stats.jump_rounds, rounds);
+    if (timed) CK(cudaEventRecord(c->ev_s2[1], c->stream));
     if (multi) {
         CK(launch_flag_remote(S.label, n, S.s.v0, c->stream));
         c->stats.kernel_launches += 1;
@@ -781,7 +789,8 @@ static eg_status compute_grid(eg_ctx *c, const Problem &P, const float *f, uint3
         if (tiled) {
             eg_status s = tiled3d_local(S->tiled, P.ndim, P.dims, S->s, S->F, S->label, c->flags.as<int>(),
                                         c->stream, &c->stats, &c->err, first ? c->ev_main[0] : nullptr,
-                                        first ? c->ev_main[1] : nullptr);
+                                        first ? c->ev_main[1] : nullptr,
+                                        (flags & EG_STATS) ? c->stat_buf.as<unsigned long long>() : nullptr);
             if (s != EG_OK) {
                 if (s == EG_ERR_CUDA) c->poisoned = true;
                 return s;
@@ -807,16 +816,25 @@ static eg_status compute_grid(eg_ctx *c, const Problem &P, const float *f, uint3
     // ---- cross-slab resolution, then every unresolved owned label
     if (multi) {
         int rounds = 0;
+        CK(cudaEventRecord(c->ev_s2[2], c->stream));
         ST(boundary_rounds(c, &rounds));
+        CK(cudaEventRecord(c->ev_s2[3], c->stream));
+        c->s2_timed[1] = true;
         c->stats.boundary_rounds = rounds;
+    }
+    if (tiled || multi) {
+        CK(cudaEventRecord(c->ev_s2[4], c->stream));
+        c->s2_timed[2] = true;
     }
     for (SlabState *S : c->slabs) {
         if (!tiled && !multi) continue;           // generic single slab: already final
         CK(launch_finalize(S->label, nullptr, S->s.v0, S->s.v1,
                            S->has_lo ? S->hval_lo.as<int32_t>() : nullptr,
-                           S->has_hi ? S->hval_hi.as<int32_t>() : nullptr, P.plane, c->stream));
+                           S->has_hi ? S->hval_hi.as<int32_t>() : nullptr, P.plane, c->stream,
+                           (flags & EG_STATS) ? c->stat_buf.as<unsigned long long>() + 1 : nullptr));
         c->stats.kernel_launches += 1;
     }
+    if (tiled || multi) CK(cudaEventRecord(c->ev_s2[5], c->stream));
     CK(cudaEventRecord(c->ev[2], c->stream));
     if (!c->overlap) ST(fail_if_flags(c));
     c->d_labels = c->label_all.as<int32_t>();
@@ -869,9 +887,11 @@ static eg_status compute_csr(eg_ctx *c, const Problem &P, const float *f, uint32
         S.tiled_lists = false;
         CK(S.beta8.ensure(std::max<int64_t>(S.s.v1 - S.s.v0, 1)));
         CK(S.rep_buf.ensure(sizeof(int32_t) * std::max<int64_t>(P.nnz, 1)));
-        CK(S.slow_up.ensure(2 * sizeof(int32_t) * std::max<int64_t>(P.nnz, 1)));
         S.has_lo = S.has_hi = false;
     }
+    const int64_t cap = std::max<int64_t>(P.nnz, 1);
+    CK(c->csr_scratch.ensure(sizeof(int32_t) * (2 * cap + std::max<int64_t>(P.N, 1))));
+    int32_t *upl = c->csr_scratch.as<int32_t>(), *par = upl + cap, *nup = upl + 2 * cap;
     if (flags & EG_CHECK_CSR) {
         // validated before any kernel indexes through the graph (an invalid
         // col_idx would read out of bounds)
@@ -886,32 +906,40 @@ static eg_status compute_csr(eg_ctx *c, const Problem &P, const float *f, uint32
         // f, the CSR rows of the range, the gradient written once
         c->stats.bytes_main = 8 * n0 + 8 * (n0 + 1) + 4 * (P.nnz * n0 / std::max<int64_t>(P.N, 1));
     }
+    // S1 for every vertex of the graph on every rank (the S3 pass of a range
+    // reads the upper lists of the range's neighbours, and the gradients of
+    // the whole graph feed S2): cheap next to S3, and no exchange is needed
+    CK(cudaEventRecord(c->ev_main[0], c->stream));
+    int64_t covered = 0;
     for (SlabState *S : c->slabs) {
-        const bool first = S == c->slabs[0];
-        if (first) CK(cudaEventRecord(c->ev_main[0], c->stream));
-        CK(launch_classify_csr(P.row_ptr, P.col_idx, f, S->s.v0, S->s.v1, S->label, S->sad_bits.as<uint32_t>(),
-                               S->max_bits.as<uint32_t>(), S->beta8.as<uint8_t>(), fl, c->stream,
-                               S->rep_buf.as<int32_t>(), S->slow_up.as<int32_t>(),
-                               S->slow_up.as<int32_t>() + std::max<int64_t>(P.nnz, 1)));
-        if (first) CK(cudaEventRecord(c->ev_main[1], c->stream));
+        if (covered < S->s.v0) {        // ranges owned by other ranks
+            CK(launch_csr_upper(P.row_ptr, P.col_idx, f, covered, S->s.v0, c->label_all.as<int32_t>() + covered,
+                                nullptr, upl, nup, fl, c->stream));
+            c->stats.kernel_launches += 1;
+        }
+        CK(launch_csr_upper(P.row_ptr, P.col_idx, f, S->s.v0, S->s.v1, S->label, S->max_bits.as<uint32_t>(), upl, nup,
+                            fl, c->stream));
+        c->stats.kernel_launches += 1;
+        covered = S->s.v1;
+    }
+    if (covered < P.N) {
+        CK(launch_csr_upper(P.row_ptr, P.col_idx, f, covered, P.N, c->label_all.as<int32_t>() + covered, nullptr, upl,
+                            nup, fl, c->stream));
         c->stats.kernel_launches += 1;
     }
-    if (c->world > 1) {
-        // the one exchange step: every rank's gradients to every rank
-        NK(ncclGroupStart());
-        for (int r = 0; r < c->world; ++r) {
-            const int64_t a = all[2 * r], b = all[2 * r + 1];
-            if (b > a)
-                NK(ncclBroadcast(c->label_all.as<int32_t>() + a, c->label_all.as<int32_t>() + a, size_t(b - a),
-                                 ncclInt32, r, c->comm, c->stream));
-        }
-        NK(ncclGroupEnd());
+    for (SlabState *S : c->slabs) {
+        CK(launch_csr_link(P.row_ptr, P.col_idx, f, S->s.v0, S->s.v1, upl, nup, S->sad_bits.as<uint32_t>(),
+                           S->beta8.as<uint8_t>(), S->rep_buf.as<int32_t>(), par, c->stream));
+        c->stats.kernel_launches += 1;
     }
+    CK(cudaEventRecord(c->ev_main[1], c->stream));
     CK(cudaEventRecord(c->ev[1], c->stream));
     // S2 on the full array (every rank; N is small for CSR workloads)
     SlabState whole;
     whole.s = Slab{0, 0, 0, 0, P.N};
     whole.label = c->label_all.as<int32_t>();
+    CK(cudaEventRecord(c->ev_s2[0], c->stream));
+    c->s2_timed[0] = true;
     {
         int *changed = fl + 2;
         CK(cudaMemsetAsync(changed, 0, sizeof(int) * 64, c->stream));
@@ -935,6 +963,7 @@ static eg_status compute_csr(eg_ctx *c, const Problem &P, const float *f, uint32
         }
         c->stats.jump_rounds = rounds;
     }
+    CK(cudaEventRecord(c->ev_s2[1], c->stream));
     whole.label = nullptr;
     CK(cudaEventRecord(c->ev[2], c->stream));
     ST(fail_if_flags(c));
@@ -1045,6 +1074,11 @@ static eg_status compute_impl(eg_ctx *c, const eg_domain *d, const float *f, uin
     CK(c->flags.ensure(sizeof(int) * 128));
     CK(c->counts.ensure(sizeof(int64_t) * 16 * (c->world + 1)));
     CK(cudaMemsetAsync(c->flags.p, 0, sizeof(int) * 128, c->stream));
+    c->s2_timed[0] = c->s2_timed[1] = c->s2_timed[2] = false;
+    if (flags & EG_STATS) {
+        CK(c->stat_buf.ensure(sizeof(unsigned long long) * 32));
+        CK(cudaMemsetAsync(c->stat_buf.p, 0, sizeof(unsigned long long) * 32, c->stream));
+    }
     // EG_MINIMUM (reading L11): the maximum graph of g[i] = -f[N-1-i], mapped
     // back by i -> N-1-i (k_common.cu)
     const float *f_user = f;           // the caller's field (device) -- f becomes the mirror for a minimum graph
@@ -1167,9 +1201,16 @@ static eg_status compute_impl(eg_ctx *c, const eg_domain *d, const float *f, uin
     CK(cudaStreamSynchronize(c->stream));
     c->have_graph = true;
     c->stats.us_classify = ev_us(c->ev[0], c->ev[1]);
-    c->stats.us_jump = 0;
-    c->stats.us_boundary = ev_us(c->ev[1], c->ev[2]);
-    c->stats.us_label = 0;
+    c->stats.us_jump = c->s2_timed[0] ? ev_us(c->ev_s2[0], c->ev_s2[1]) : 0.0;
+    c->stats.us_boundary = c->s2_timed[1] ? ev_us(c->ev_s2[2], c->ev_s2[3]) : 0.0;
+    c->stats.us_label = c->s2_timed[2] ? ev_us(c->ev_s2[4], c->ev_s2[5]) : 0.0;
+    if (flags & EG_STATS) {
+        unsigned long long h[32];
+        CK(cudaMemcpy(h, c->stat_buf.p, sizeof(h), cudaMemcpyDeviceToHost));
+        c->stats.n_exit = int64_t(h[0]);
+        for (int k = 0; k < 16; ++k) c->stats.chase_hist[k] = int64_t(h[1 + k]);
+        c->stats.chase_max = int32_t(h[17]);
+    }
     c->stats.us_arcs = ev_us(c->ev[2], c->ev[4]);
     c->stats.us_graph = ev_us(c->ev[4], c->ev[5]);
     c->stats.us_total = ev_us(c->ev[0], c->ev[5]);
@@ -1206,6 +1247,11 @@ eg_status eg_create(eg_ctx **out, int cuda_device, void *cuda_stream) {
             return EG_ERR_CUDA;
         }
     for (auto &e : c->ev_main)
+        if (cudaEventCreate(&e) != cudaSuccess) {
+            delete c;
+            return EG_ERR_CUDA;
+        }
+    for (auto &e : c->ev_s2)
         if (cudaEventCreate(&e) != cudaSuccess) {
             delete c;
             return EG_ERR_CUDA;
@@ -1364,10 +1410,13 @@ eg_status eg_gradient(eg_ctx *c, const eg_domain *d, const float *d_field, int32
         CK(launch_classify_grid(c->host_tab, P.ndim, F, s, d_ptr, S.sad_bits.as<uint32_t>(),
                                 S.max_bits.as<uint32_t>(), d_beta, c->flags.as<int>(), c->stream));
     } else {
-        CK(S.slow_up.ensure(2 * sizeof(int32_t) * std::max<int64_t>(P.nnz, 1)));
-        CK(launch_classify_csr(P.row_ptr, P.col_idx, d_field, P.v0, P.v1, d_ptr, S.sad_bits.as<uint32_t>(),
-                               S.max_bits.as<uint32_t>(), d_beta, c->flags.as<int>(), c->stream, nullptr,
-                               S.slow_up.as<int32_t>(), S.slow_up.as<int32_t>() + std::max<int64_t>(P.nnz, 1)));
+        const int64_t cap = std::max<int64_t>(P.nnz, 1);
+        CK(c->csr_scratch.ensure(sizeof(int32_t) * (2 * cap + std::max<int64_t>(P.N, 1))));
+        int32_t *upl = c->csr_scratch.as<int32_t>(), *par = upl + cap, *nup = upl + 2 * cap;
+        CK(launch_csr_upper(P.row_ptr, P.col_idx, d_field, P.v0, P.v1, d_ptr, S.max_bits.as<uint32_t>(), upl, nup,
+                            c->flags.as<int>(), c->stream));
+        CK(launch_csr_link(P.row_ptr, P.col_idx, d_field, P.v0, P.v1, upl, nup, S.sad_bits.as<uint32_t>(), d_beta,
+                           nullptr, par, c->stream));
     }
     return fail_if_flags(c);
 }
@@ -1447,13 +1496,15 @@ eg_status eg_destroy(eg_ctx *c) {
     cudaStreamSynchronize(c->stream);
     set_slab_count(c, 0);
     DevBuf *bufs[] = {&c->typed, &c->rank_scratch, &c->d_fnode, &c->bund_scratch, &c->b_sad64, &c->b_sad32, &c->b_sbeta, &c->b_nu, &c->b_arc_s, &c->b_arc_m,
-                      &c->b_arc_mult, &c->label_all, &c->field, &c->mirror, &c->path_len, &c->path_off, &c->path_v, &c->flags, &c->counts, &c->scratch, &c->tab, &c->gsend, &c->grecv};
+                      &c->b_arc_mult, &c->label_all, &c->csr_scratch, &c->stat_buf, &c->field, &c->mirror, &c->path_len, &c->path_off, &c->path_v, &c->flags, &c->counts, &c->scratch, &c->tab, &c->gsend, &c->grecv};
     for (DevBuf *b : bufs) b->release();
     HostBuf *hb[] = {&c->h_fmax, &c->h_fsad, &c->h_maxima, &c->h_saddles, &c->h_sbeta, &c->h_arc_s, &c->h_arc_m, &c->h_arc_mult,
                      &c->h_raw_s, &c->h_raw_rep, &c->h_raw_m, &c->h_counts, &c->h_stage, &c->h_path_off,
                      &c->h_path_v};
     for (HostBuf *b : hb) b->release();
     for (auto &e : c->ev)
+        if (e) cudaEventDestroy(e);
+    for (auto &e : c->ev_s2)
         if (e) cudaEventDestroy(e);
     for (auto &e : c->ev_main)
         if (e) cudaEventDestroy(e);

@@ -92,12 +92,19 @@ struct LabelView {
 cudaError_t launch_classify_grid(const LinkTable &tab, int ndim, FieldView F, const Slab &s, int32_t *ptr,
                                  uint32_t *sad_bits, uint32_t *max_bits, uint8_t *beta_out, int *nan_flag,
                                  cudaStream_t st);
-// one warp per vertex, no degree cap: slow_u / slow_p are row_ptr-indexed
-// int32[nnz] scratch for vertices with more than 64 upper neighbours
-cudaError_t launch_classify_csr(const int64_t *row_ptr, const int32_t *col_idx, const float *f, int64_t v0,
-                                int64_t v1, int32_t *ptr, uint32_t *sad_bits, uint32_t *max_bits,
-                                uint8_t *beta_out, int *nan_flag, cudaStream_t st, int32_t *rep_buf,
-                                int32_t *slow_u, int32_t *slow_p);
+// CSR S1 + S3 in two warp-per-vertex passes, no degree cap (k_csr.cu).
+// S1 over [v0, v1): ptr[v - v0] = gradient, max_bits (nullable) = maxima of the
+// range, and the upper list of every v: upl[row_ptr[v] .. + nup[v]) (upl is
+// int32[nnz], nup int32[N], both indexed globally).  S3 over [v0, v1) needs
+// the upper lists of every neighbour of the range (run S1 over [0, N) first):
+// sad_bits, beta0+ (nullable), the saddles' reps in rep_buf[row_ptr[v] ..]
+// (nullable); par = int32[nnz] scratch for vertices with |U| > 64.
+cudaError_t launch_csr_upper(const int64_t *row_ptr, const int32_t *col_idx, const float *f, int64_t v0, int64_t v1,
+                             int32_t *ptr, uint32_t *max_bits, int32_t *upl, int32_t *nup, int *nan_flag,
+                             cudaStream_t st);
+cudaError_t launch_csr_link(const int64_t *row_ptr, const int32_t *col_idx, const float *f, int64_t v0, int64_t v1,
+                            const int32_t *upl, const int32_t *nup, uint32_t *sad_bits, uint8_t *beta_out,
+                            int32_t *rep_buf, int32_t *par, cudaStream_t st);
 // EG_CHECK_CSR: *bad |= a nonzero code if the CSR is not a sorted, symmetric,
 // loop-free adjacency with a valid row_ptr (k_csr.cu)
 cudaError_t launch_check_csr(const int64_t *row_ptr, const int32_t *col_idx, int64_t n, int64_t nnz, int *bad,
@@ -233,5 +240,5 @@ cudaError_t launch_bval_update(int32_t *bval, const int32_t *hval_lo, const int3
 // whose bit is set in `bits`) becomes final, via owned labels and the final
 // halo-plane values
 cudaError_t launch_finalize(int32_t *label, const uint32_t *bits, int64_t v0, int64_t v1, const int32_t *hval_lo,
-                            const int32_t *hval_hi, int64_t plane, cudaStream_t st);
+                            const int32_t *hval_hi, int64_t plane, cudaStream_t st, unsigned long long *hist = nullptr);
 }  // namespace eg

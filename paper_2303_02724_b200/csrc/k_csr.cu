@@ -15,42 +15,86 @@ __device__ __forceinline__ bool csr_higher(int32_t u, float fu, int32_t v, float
     return fu > fv || (fu == fv && u > v);     // simulated perturbation (L1)
 }
 
-// One warp per vertex (north_star (b): "warp-level shuffles and ballots for
-// link-component labelling"), a warp owns the 32 vertices of one bitmap word.
-//  S1  lanes take N(v) 32 at a time; U = ballot of the upper neighbours,
-//      compacted in order (ascending ids) into shared memory; the gradient is
-//      a shuffle argmax over (f, id) (ties by id, L1).
-//  S3  |U| <= 1: maximum / regular, no link edges needed.  Otherwise the link
-//      edges inside U (reading L14: the subgraph induced on N(v)) are found by
-//      flattening the rows N(a), a in U, over the lanes: every lane loads one
-//      x in N(a) (coalesced within a row), finds x in U by binary search, and
-//      sets bit q of a's adjacency word in shared memory.  Components
-//       by frontier expansion: each lane owns two link vertices, a
-//      step is one __reduce_or_sync of the owned adjacency words of the
-//      frontier; UpperLinkRep = shuffle argmax over the component.
-//  |U| > 64 (no degree cap): lane 0 runs a union-find over the merged sorted
-//      rows in ctx-owned global scratch (row_ptr-indexed), slow but exact.
+// Two warp-per-vertex passes (north_star (b): "warp-level shuffles and
+// ballots for link-component labelling"); a warp owns the 32 vertices of one
+// bitmap word.
+//  S1  (k_csr_upper) lanes take N(v) 32 at a time; U(v) = ballot of the upper
+//      neighbours, compacted in order (ascending ids) into the upper list
+//      upl[row_ptr[v] ..] (|U(v)| in nup[v]); the gradient is the (value, id)
+//      maximum over U by two warp max-reductions of order-preserving keys
+//      (ties by id, L1); maximum iff U is empty.
+//  S3  (k_csr_link) for |U(v)| >= 2: the link edges inside U(v) (reading L14:
+//      the subgraph induced on N(v)).  Every edge {a, b} of U(v) closes a
+//      triangle whose lowest vertex is v, and is found once from its lower end
+//      a: b in U(a) and b in U(v).  Lane p owns a = U(v)[p] (and p + 32), walks
+//      the upper list of a and looks each entry up in a per-warp hash set of
+//      U(v) -> a bit in its own adjacency word.  Components by
+//      frontier expansion: a step ORs the forward words of the frontier
+//      (__reduce_or_sync) and the ballot of the lanes whose word meets the
+//      frontier (the backward edges); UpperLinkRep = the component's
+//      (value, id) maximum.  |U| > 64 (no degree cap): lane 0 runs a
+//      union-find over merged sorted rows (row_ptr-indexed scratch), slow but
+//      exact.
 constexpr int kCsrWarps = 4;
 constexpr int kCsrFast = 64;                  // |U| handled by the warp path
+constexpr int kHash = 128;                    // per-warp open-addressing set of U
 
-struct CsrWarpSmem {
-    int32_t u[kCsrFast];
-    float fu[kCsrFast];
-    int32_t pre[kCsrFast + 1];                // prefix sums of deg(U[p])
-    int64_t rs[kCsrFast];                     // row start of U[p]
-    unsigned long long adj[kCsrFast];
-    int32_t rep[kCsrFast];
-};
+// order-preserving key of a non-NaN float with -0 == +0 (reading L2)
+__device__ __forceinline__ uint32_t fkey(float x) {
+    const uint32_t b = x == 0.0f ? 0u : __float_as_uint(x);
+    return b ^ ((b & 0x80000000u) ? 0xffffffffu : 0x80000000u);
+}
 
-__device__ __forceinline__ void argmax_fi(float &bf, int32_t &bv) {
-#pragma unroll
-    for (int o = 16; o; o >>= 1) {
-        const float of = __shfl_xor_sync(0xffffffffu, bf, o);
-        const int32_t ov = __shfl_xor_sync(0xffffffffu, bv, o);
-        if (ov >= 0 && (bv < 0 || of > bf || (of == bf && ov > bv))) {
-            bf = of;
-            bv = ov;
+__device__ __forceinline__ uint32_t hslot(int32_t x) { return (uint32_t(x) * 2654435761u) >> 25; }
+
+__global__ void __launch_bounds__(32 * kCsrWarps) k_csr_upper(
+    const int64_t *__restrict__ rp, const int32_t *__restrict__ ci, const float *__restrict__ f, int64_t v0,
+    int64_t v1, int32_t *ptr, uint32_t *max_bits, int32_t *upl, int32_t *nup, int *nan_flag) {
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const uint32_t lt = (1u << lane) - 1u;
+    const int64_t n = v1 - v0, words = (n + 31) / 32;
+    for (int64_t w = int64_t(blockIdx.x) * kCsrWarps + wib; w < words; w += int64_t(gridDim.x) * kCsrWarps) {
+        uint32_t mb = 0;
+        int32_t my_ptr = 0, my_nu = 0;
+        const int jn = n - w * 32 < 32 ? int(n - w * 32) : 32;
+        for (int j = 0; j < jn; ++j) {
+            const int32_t v = int32_t(v0 + w * 32 + j);
+            const int64_t b0 = rp[v], b1 = rp[v + 1];
+            const float fv = __ldg(f + v);
+            if (lane == 0 && fv != fv) atomicOr(nan_flag, 1);
+            int nu = 0;
+            uint32_t bk = 0u;          // lane-local best order key (0: none; every finite key is > 0)
+            int32_t bid = -1;
+            for (int64_t e0 = b0; e0 < b1; e0 += 32) {
+                const int64_t e = e0 + lane;
+                const int32_t u = e < b1 ? ci[e] : -1;
+                const float fu = u >= 0 ? __ldg(f + u) : 0.f;
+                const bool up = u >= 0 && csr_higher(u, fu, v, fv);
+                const uint32_t bal = __ballot_sync(0xffffffffu, up);
+                if (up) {
+                    upl[b0 + nu + __popc(bal & lt)] = u;
+                    const uint32_t k = fkey(fu);
+                    if (k > bk || (k == bk && u > bid)) {
+                        bk = k;
+                        bid = u;
+                    }
+                }
+                nu += __popc(bal);
+            }
+            const uint32_t km = __reduce_max_sync(0xffffffffu, bk);
+            const int32_t best = __reduce_max_sync(0xffffffffu, (bk == km && bid >= 0) ? bid : -1);
+            if (lane == j) {
+                my_ptr = nu == 0 ? v : best;
+                my_nu = nu;
+            }
+            mb |= uint32_t(nu == 0) << j;
         }
+        const int64_t i = w * 32 + lane;
+        if (lane < jn) {
+            ptr[i] = my_ptr;
+            nup[v0 + i] = my_nu;
+        }
+        if (lane == 0 && max_bits) max_bits[w] = mb;
     }
 }
 
@@ -62,12 +106,12 @@ __device__ __forceinline__ int uf_find_g(int32_t *par, int x) {
     return x;
 }
 
-// lane 0 only: union-find over U (already in gU, ascending, with values in
-// gF not needed: f is read again) for |U| > kCsrFast.  Returns beta0+; the
-// reps (ascending) go to reps_out when non-null.
-__device__ int csr_slow_components(const int64_t *__restrict__ rp, const int32_t *__restrict__ ci,
-                                   const float *__restrict__ f, const int32_t *gU, int32_t *par, int nu,
-                                   int32_t *reps_out) {
+// lane 0 only: union-find over U (ascending, in gU) for |U| > kCsrFast, link
+// edges by merging the sorted rows N(a) with U.  Returns beta0+; the reps
+// (ascending) go to reps_out when non-null.
+__device__ __noinline__ int csr_slow_components(const int64_t *__restrict__ rp, const int32_t *__restrict__ ci,
+                                                const float *__restrict__ f, const int32_t *gU, int32_t *par, int nu,
+                                                int32_t *reps_out) {
     for (int p = 0; p < nu; ++p) par[p] = p;
     for (int p = 0; p < nu; ++p) {
         const int32_t a = gU[p];
@@ -115,146 +159,194 @@ __device__ int csr_slow_components(const int64_t *__restrict__ rp, const int32_t
     return b;
 }
 
-__global__ void __launch_bounds__(32 * kCsrWarps) k_classify_csr(
-    const int64_t *__restrict__ rp, const int32_t *__restrict__ ci, const float *__restrict__ f, int64_t v0,
-    int64_t v1, int32_t *ptr, uint32_t *sad_bits, uint32_t *max_bits, uint8_t *beta_out, int *nan_flag,
-    int32_t *rep_buf, int32_t *slow_u, int32_t *slow_p) {
-    __shared__ CsrWarpSmem sm_all[kCsrWarps];
-    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-    CsrWarpSmem &sm = sm_all[wib];
-    const uint32_t lt = (1u << lane) - 1u;
-    const int64_t n = v1 - v0, words = (n + 31) / 32;
-    for (int64_t w = int64_t(blockIdx.x) * kCsrWarps + wib; w < words; w += int64_t(gridDim.x) * kCsrWarps) {
-        uint32_t sb = 0, mb = 0;
-        int32_t my_ptr = 0;
-        int my_beta = 0;
-        const int jn = n - w * 32 < 32 ? int(n - w * 32) : 32;
-        for (int j = 0; j < jn; ++j) {
-            const int32_t v = int32_t(v0 + w * 32 + j);
-            const int64_t b0 = rp[v], b1 = rp[v + 1];
-            const float fv = __ldg(f + v);
-            if (lane == 0 && fv != fv) atomicOr(nan_flag, 1);
-            // ---- S1: upper set U (ascending) and the gradient
-            int nu = 0;
-            float bf = fv;
-            int32_t bv = v;
-            for (int64_t e0 = b0; e0 < b1; e0 += 32) {
-                const int64_t e = e0 + lane;
-                const int32_t u = e < b1 ? ci[e] : -1;
-                const float fu = u >= 0 ? __ldg(f + u) : 0.f;
-                const bool up = u >= 0 && csr_higher(u, fu, v, fv);
-                const uint32_t bal = __ballot_sync(0xffffffffu, up);
-                const int pos = nu + __popc(bal & lt);
-                if (up) {
-                    if (pos < kCsrFast) {
-                        sm.u[pos] = u;
-                        sm.fu[pos] = fu;
-                    } else if (slow_u) {
-                        slow_u[b0 + pos] = u;
-                    }
-                    if (fu > bf || (fu == bf && u > bv)) {
-                        bf = fu;
-                        bv = u;
-                    }
-                }
-                nu += __popc(bal);
-            }
-            argmax_fi(bf, bv);
-            int beta = 0;
-            if (nu >= 2 && nu <= kCsrFast) {
-                __syncwarp();
-                // ---- S3: link edges inside U, flattened over the rows N(a)
-                const int pa = lane, pb = lane + 32;
-                int64_t ra = 0, rb = 0;
-                int da = 0, db = 0;
-                if (pa < nu) {
-                    const int32_t a = sm.u[pa];
-                    ra = rp[a];
-                    da = int(rp[a + 1] - ra);
-                }
-                if (pb < nu) {
-                    const int32_t a = sm.u[pb];
-                    rb = rp[a];
-                    db = int(rp[a + 1] - rb);
-                }
-                // inclusive scan of (da, db) over the lanes: positions pa and pb
-                int sa = da, sbb = db;
+struct __align__(16) CsrLinkSmem {
+    int32_t hkey[kHash];                      // first: 16-byte aligned for the int4 clear
+    int32_t hpos[kHash];
+    int32_t rep[kCsrFast];
+};
+
+__device__ __forceinline__ void hset_insert(CsrLinkSmem &sm, int32_t u, int pos) {
+    uint32_t h = hslot(u);
+    while (atomicCAS(&sm.hkey[h], -1, u) != -1) h = (h + 1) & (kHash - 1);
+    sm.hpos[h] = pos;
+}
+
+__device__ __forceinline__ int hset_find(const CsrLinkSmem &sm, int32_t x) {   // position of x in U, or -1
+    uint32_t h = hslot(x);
+    for (;;) {
+        const int32_t key = sm.hkey[h];
+        if (key == x) return sm.hpos[h];
+        if (key == -1) return -1;
+        h = (h + 1) & (kHash - 1);
+    }
+}
+
+// |U(v)| <= 32: lane p owns link vertex U[p]; 32-bit adjacency words.
+// Returns beta0+; with reps != null the ascending UpperLinkReps of a saddle
+// are stored there.
+__device__ __forceinline__ int csr_link32(CsrLinkSmem &sm, const int64_t *__restrict__ rp,
+                                          const float *__restrict__ f, const int32_t *__restrict__ upl,
+                                          const int32_t *__restrict__ nup, const int32_t *U, int nu, int lane,
+                                          int32_t *reps) {
+    reinterpret_cast<int4 *>(sm.hkey)[lane] = make_int4(-1, -1, -1, -1);
+    __syncwarp();
+    const int32_t uA = lane < nu ? U[lane] : -1;
+    int64_t sA = 0;
+    int lA = 0;
+    if (uA >= 0) {
+        hset_insert(sm, uA, lane);
+        sA = rp[uA];
+        lA = nup[uA];
+    }
+    const uint32_t kA = uA >= 0 ? fkey(__ldg(f + uA)) : 0u;
+    __syncwarp();
+    // forward link edges {a, b}, b in U(a) and b in U(v); four loads in flight
+    uint32_t adj = 0u;
+    for (int k = 0; k < lA; k += 4) {
+        int32_t x[4];
 #pragma unroll
-                for (int o = 1; o < 32; o <<= 1) {
-                    const int ya = __shfl_up_sync(0xffffffffu, sa, o);
-                    const int yb = __shfl_up_sync(0xffffffffu, sbb, o);
-                    if (lane >= o) {
-                        sa += ya;
-                        sbb += yb;
+        for (int i = 0; i < 4; ++i) x[i] = k + i < lA ? upl[sA + k + i] : -1;
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+            if (x[i] >= 0) {
+                const int q = hset_find(sm, x[i]);
+                if (q >= 0) adj |= 1u << q;
+            }
+    }
+    const uint32_t all = nu == 32 ? 0xffffffffu : ((1u << nu) - 1u);
+    uint32_t seen = 0u;
+    int beta = 0;
+    int32_t my_rep = -1;
+    while (seen != all) {
+        uint32_t comp = (all & ~seen) & (0u - (all & ~seen));     // lowest unseen link vertex
+        for (;;) {
+            const bool in = (comp >> lane) & 1u;
+            const uint32_t fw = __reduce_or_sync(0xffffffffu, in ? adj : 0u);        // forward edges
+            const uint32_t bw = __ballot_sync(0xffffffffu, (adj & comp) != 0u);       // backward edges
+            const uint32_t nc = (comp | fw | bw) & all;
+            if (nc == comp) break;
+            comp = nc;
+        }
+        // UpperLinkRep: the (value, id) maximum of the component
+        const bool in = (comp >> lane) & 1u;
+        const uint32_t kmax = __reduce_max_sync(0xffffffffu, in ? kA : 0u);
+        const int32_t rv = __reduce_max_sync(0xffffffffu, (in && kA == kmax) ? uA : -1);
+        if (lane == beta) my_rep = rv;
+        ++beta;
+        seen |= comp;
+    }
+    if (beta >= 2 && reps) {
+        int rank = 0;   // ascending reps: rank among the component reps
+        for (int j = 0; j < beta; ++j) rank += __shfl_sync(0xffffffffu, my_rep, j) < my_rep;
+        if (lane < beta) reps[rank] = my_rep;
+    }
+    return beta;
+}
+
+__global__ void __launch_bounds__(32 * kCsrWarps) k_csr_link(
+    const int64_t *__restrict__ rp, const int32_t *__restrict__ ci, const float *__restrict__ f, int64_t v0,
+    int64_t v1, const int32_t *__restrict__ upl, const int32_t *__restrict__ nup, uint32_t *sad_bits,
+    uint8_t *beta_out, int32_t *rep_buf, int32_t *slow_p) {
+    __shared__ CsrLinkSmem sm_all[kCsrWarps];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    CsrLinkSmem &sm = sm_all[wib];
+    const int64_t n = v1 - v0, words = (n + 31) / 32;
+    const int pa = lane, pb = lane + 32;
+    for (int64_t w = int64_t(blockIdx.x) * kCsrWarps + wib; w < words; w += int64_t(gridDim.x) * kCsrWarps) {
+        const int jn = n - w * 32 < 32 ? int(n - w * 32) : 32;
+        const int my_nu = lane < jn ? nup[v0 + w * 32 + lane] : 0;
+        int my_beta = my_nu < 2 ? my_nu : 0;            // 0: maximum, 1: regular
+        uint32_t todo = __ballot_sync(0xffffffffu, my_nu >= 2);
+        while (todo) {
+            const int j = __ffs(todo) - 1;
+            todo &= todo - 1;
+            const int32_t v = int32_t(v0 + w * 32 + j);
+            const int nu = __shfl_sync(0xffffffffu, my_nu, j);
+            const int64_t b0 = rp[v];
+            const int32_t *U = upl + b0;
+            int beta = 0;
+            if (nu <= 32) {
+                beta = csr_link32(sm, rp, f, upl, nup, U, nu, lane, rep_buf ? rep_buf + b0 : nullptr);
+                __syncwarp();
+            } else if (nu <= kCsrFast) {
+                reinterpret_cast<int4 *>(sm.hkey)[lane] = make_int4(-1, -1, -1, -1);
+                __syncwarp();
+                const int32_t uA = pa < nu ? U[pa] : -1, uB = pb < nu ? U[pb] : -1;
+                if (uA >= 0) {
+                    uint32_t h = hslot(uA);
+                    while (atomicCAS(&sm.hkey[h], -1, uA) != -1) h = (h + 1) & (kHash - 1);
+                    sm.hpos[h] = pa;
+                }
+                if (uB >= 0) {
+                    uint32_t h = hslot(uB);
+                    while (atomicCAS(&sm.hkey[h], -1, uB) != -1) h = (h + 1) & (kHash - 1);
+                    sm.hpos[h] = pb;
+                }
+                // the upper lists of a = U[pa] / U[pb]
+                int64_t sA = 0, sB = 0;
+                int lA = 0, lB = 0;
+                if (uA >= 0) {
+                    sA = rp[uA];
+                    lA = nup[uA];
+                }
+                if (uB >= 0) {
+                    sB = rp[uB];
+                    lB = nup[uB];
+                }
+                __syncwarp();
+                // forward link edges: b in U(a) and b in U(v)
+                unsigned long long adjA = 0ull, adjB = 0ull;
+                for (int k = 0; k < lA; ++k) {
+                    const int32_t x = upl[sA + k];
+                    uint32_t h = hslot(x);
+                    for (;;) {
+                        const int32_t key = sm.hkey[h];
+                        if (key == x) {
+                            adjA |= 1ull << sm.hpos[h];
+                            break;
+                        }
+                        if (key == -1) break;
+                        h = (h + 1) & (kHash - 1);
                     }
                 }
-                const int tot_a = __shfl_sync(0xffffffffu, sa, 31);
-                if (pa < nu) {
-                    sm.pre[pa + 1] = sa;
-                    sm.rs[pa] = ra;
-                }
-                if (pb < nu) {
-                    sm.pre[pb + 1] = tot_a + sbb;
-                    sm.rs[pb] = rb;
-                }
-                if (lane == 0) sm.pre[0] = 0;
-                sm.adj[pa] = 0ull;
-                sm.adj[pb] = 0ull;
-                __syncwarp();
-                const int T = sm.pre[nu];
-                for (int t0 = 0; t0 < T; t0 += 32) {
-                    const int t = t0 + lane;
-                    if (t < T) {
-                        // p = the row of element t: last p with pre[p] <= t
-                        int lo = 0, hi = nu - 1;
-                        while (lo < hi) {
-                            const int mid = (lo + hi + 1) >> 1;
-                            if (sm.pre[mid] <= t) lo = mid;
-                            else hi = mid - 1;
+                for (int k = 0; k < lB; ++k) {
+                    const int32_t x = upl[sB + k];
+                    uint32_t h = hslot(x);
+                    for (;;) {
+                        const int32_t key = sm.hkey[h];
+                        if (key == x) {
+                            adjB |= 1ull << sm.hpos[h];
+                            break;
                         }
-                        const int32_t x = ci[sm.rs[lo] + (t - sm.pre[lo])];
-                        // x in U?  (U ascending)
-                        int a = 0, b = nu - 1;
-                        while (a < b) {
-                            const int mid = (a + b) >> 1;
-                            if (sm.u[mid] < x) a = mid + 1;
-                            else b = mid;
-                        }
-                        if (sm.u[a] == x) {
-                            unsigned int *wd = reinterpret_cast<unsigned int *>(&sm.adj[lo]) + (a >> 5);
-                            atomicOr(wd, 1u << (a & 31));
-                        }
+                        if (key == -1) break;
+                        h = (h + 1) & (kHash - 1);
                     }
                 }
-                __syncwarp();
-                const unsigned long long adjA = sm.adj[pa], adjB = sm.adj[pb];
-                const float fA = pa < nu ? sm.fu[pa] : 0.f, fB = pb < nu ? sm.fu[pb] : 0.f;
-                const int32_t uA = pa < nu ? sm.u[pa] : -1, uB = pb < nu ? sm.u[pb] : -1;
+                const float fA = uA >= 0 ? __ldg(f + uA) : 0.f, fB = uB >= 0 ? __ldg(f + uB) : 0.f;
+                const uint32_t kA = uA >= 0 ? fkey(fA) : 0u, kB = uB >= 0 ? fkey(fB) : 0u;
                 const unsigned long long all = nu == 64 ? ~0ull : ((1ull << nu) - 1ull);
                 unsigned long long seen = 0ull;
                 while (seen != all) {
                     unsigned long long comp = 1ull << (__ffsll((long long)(all & ~seen)) - 1);
                     for (;;) {
-                        const unsigned long long c =
-                            (((comp >> pa) & 1ull) ? adjA : 0ull) | ((pb < 64 && ((comp >> pb) & 1ull)) ? adjB : 0ull);
+                        const bool inA = (comp >> pa) & 1ull, inB = (comp >> pb) & 1ull;
+                        const unsigned long long c = (inA ? adjA : 0ull) | (inB ? adjB : 0ull);
                         const unsigned lo32 = __reduce_or_sync(0xffffffffu, unsigned(c));
                         const unsigned hi32 = __reduce_or_sync(0xffffffffu, unsigned(c >> 32));
-                        const unsigned long long nc = (comp | (((unsigned long long)hi32 << 32) | lo32)) & all;
+                        // backward edges: lanes whose forward word meets the frontier
+                        const unsigned bA = __ballot_sync(0xffffffffu, (adjA & comp) != 0ull);
+                        const unsigned bBk = __ballot_sync(0xffffffffu, (adjB & comp) != 0ull);
+                        const unsigned long long nc =
+                            (comp | ((unsigned long long)(hi32 | bBk) << 32) | (lo32 | bA)) & all;
                         if (nc == comp) break;
                         comp = nc;
                     }
-                    // UpperLinkRep: the highest member
-                    float rf = 0.f;
-                    int32_t rv = -1;
-                    if ((comp >> pa) & 1ull) {
-                        rf = fA;
-                        rv = uA;
-                    }
-                    if (((comp >> pb) & 1ull) && (rv < 0 || fB > rf || (fB == rf && uB > rv))) {
-                        rf = fB;
-                        rv = uB;
-                    }
-                    argmax_fi(rf, rv);
+                    // UpperLinkRep: the (value, id) maximum of the component
+                    const bool inA = (comp >> pa) & 1ull, inB = (comp >> pb) & 1ull;
+                    const uint32_t kk = max(inA ? kA : 0u, inB ? kB : 0u);
+                    const uint32_t kmax = __reduce_max_sync(0xffffffffu, kk);
+                    const int32_t cand = max((inA && kA == kmax) ? uA : -1, (inB && kB == kmax) ? uB : -1);
+                    const int32_t rv = __reduce_max_sync(0xffffffffu, cand);
                     if (lane == 0) sm.rep[beta] = rv;
                     ++beta;
                     seen |= comp;
@@ -270,36 +362,17 @@ __global__ void __launch_bounds__(32 * kCsrWarps) k_classify_csr(
                     }
                 }
                 __syncwarp();
-            } else if (nu > kCsrFast) {
-                // no degree cap: the first kCsrFast entries of U are in shared
-                // memory, the rest in slow_u; lane 0 finishes serially
-                __syncwarp();
-                for (int k = lane; k < kCsrFast; k += 32) slow_u[b0 + k] = sm.u[k];
-                __syncwarp();
-                __threadfence_block();
-                if (lane == 0)
-                    beta = csr_slow_components(rp, ci, f, slow_u + b0, slow_p + b0, nu, rep_buf ? rep_buf + b0 : nullptr);
-                beta = __shfl_sync(0xffffffffu, beta, 0);
-                __syncwarp();
             } else {
-                beta = nu;   // 0: maximum, 1: regular
+                // no degree cap: lane 0 finishes serially over the merged full rows
+                if (lane == 0)
+                    beta = csr_slow_components(rp, ci, f, U, slow_p + b0, nu, rep_buf ? rep_buf + b0 : nullptr);
+                beta = __shfl_sync(0xffffffffu, beta, 0);
             }
-            if (lane == j) {
-                my_ptr = bv;
-                my_beta = beta;
-            }
-            sb |= uint32_t(beta >= 2) << j;
-            mb |= uint32_t(nu == 0) << j;
+            if (lane == j) my_beta = beta;
         }
-        const int64_t i = w * 32 + lane;
-        if (lane < jn) {
-            ptr[i] = my_ptr;
-            if (beta_out) beta_out[i] = uint8_t(my_beta > 255 ? 255 : my_beta);
-        }
-        if (lane == 0) {
-            sad_bits[w] = sb;
-            max_bits[w] = mb;
-        }
+        const uint32_t sb = __ballot_sync(0xffffffffu, my_beta >= 2);
+        if (lane < jn && beta_out) beta_out[w * 32 + lane] = uint8_t(my_beta > 255 ? 255 : my_beta);
+        if (lane == 0) sad_bits[w] = sb;
     }
 }
 
@@ -437,16 +510,26 @@ __global__ void __launch_bounds__(128) k_arc_paths_csr(const int64_t *__restrict
 
 static inline unsigned blocks_for(int64_t n, int bs) { return unsigned((n + bs - 1) / bs); }
 
-cudaError_t launch_classify_csr(const int64_t *row_ptr, const int32_t *col_idx, const float *f, int64_t v0,
-                                int64_t v1, int32_t *ptr, uint32_t *sad_bits, uint32_t *max_bits,
-                                uint8_t *beta_out, int *nan_flag, cudaStream_t st, int32_t *rep_buf,
-                                int32_t *slow_u, int32_t *slow_p) {
+static inline unsigned csr_blocks(int64_t n) {
+    const int64_t words = (n + 31) / 32;
+    return unsigned(std::min<int64_t>((words + kCsrWarps - 1) / kCsrWarps, 148 * 64));
+}
+
+cudaError_t launch_csr_upper(const int64_t *row_ptr, const int32_t *col_idx, const float *f, int64_t v0, int64_t v1,
+                             int32_t *ptr, uint32_t *max_bits, int32_t *upl, int32_t *nup, int *nan_flag,
+                             cudaStream_t st) {
     if (v1 <= v0) return cudaSuccess;
-    const int64_t words = (v1 - v0 + 31) / 32;
-    const int64_t blocks = std::min<int64_t>((words + kCsrWarps - 1) / kCsrWarps, 148 * 64);
-    k_classify_csr<<<unsigned(blocks), 32 * kCsrWarps, 0, st>>>(row_ptr, col_idx, f, v0, v1, ptr, sad_bits,
-                                                                 max_bits, beta_out, nan_flag, rep_buf, slow_u,
-                                                                 slow_p);
+    k_csr_upper<<<csr_blocks(v1 - v0), 32 * kCsrWarps, 0, st>>>(row_ptr, col_idx, f, v0, v1, ptr, max_bits, upl, nup,
+                                                                 nan_flag);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_csr_link(const int64_t *row_ptr, const int32_t *col_idx, const float *f, int64_t v0, int64_t v1,
+                            const int32_t *upl, const int32_t *nup, uint32_t *sad_bits, uint8_t *beta_out,
+                            int32_t *rep_buf, int32_t *par, cudaStream_t st) {
+    if (v1 <= v0) return cudaSuccess;
+    k_csr_link<<<csr_blocks(v1 - v0), 32 * kCsrWarps, 0, st>>>(row_ptr, col_idx, f, v0, v1, upl, nup, sad_bits,
+                                                                beta_out, rep_buf, par);
     return cudaGetLastError();
 }
 

@@ -139,6 +139,7 @@ struct TileArgs {
     int32_t rounds;                 // pointer-doubling rounds before the chase
     int32_t no_elist;               // one slab: no exit-target list (the finalize pass chases)
     int32_t tma;                    // field box by TMA (else plain row loads)
+    unsigned long long *exit_count; // EG_STATS: += vertices whose root is an exit (else null)
 };
 
 // ------------------------------------------------------------ TMA helpers
@@ -464,7 +465,7 @@ __global__ void __launch_bounds__(kThreads, 2)
 #pragma unroll
         for (int z = 0; z < TZ; ++z) {
             const int c = cfb + 2 * (z + 1) * PS;
-            P(c) = P(P(c));
+            P(c) = P(P(c));   // benign-race: a reader sees the old or the new pointer, both on the path
         }
         __syncthreads();
     }
@@ -476,6 +477,7 @@ __global__ void __launch_bounds__(kThreads, 2)
     // and this column's owned index at z = 0
     const int32_t g_box0 = ((z0 - 1) * D.ny + (y0 - 1)) * D.nx + (x0 - XO);
     const int32_t i_col = (z0 * D.ny + gy) * D.nx + gx - int32_t(A.v0);
+    int n_exit = 0;
 #pragma unroll kOutUnroll
     for (int zz = 0; zz < TZ; ++zz) {
         const int z = TZ - 1 - zz;   // top down: measured 1.5 % faster than bottom up on C3
@@ -483,14 +485,14 @@ __global__ void __launch_bounds__(kThreads, 2)
         const int c = cfb + 2 * (z + 1) * PS;
         // chase to the root (a cell that points to itself), two hops per
         // loop turn so that no register copies are needed
-        uint32_t r = ld16(pbase + c);
+        uint32_t r = ld16(pbase + c);   // benign-race (see above)
         for (;;) {
-            const uint32_t q = ld16(pbase + r);
+            const uint32_t q = ld16(pbase + r);   // benign-race
             if (q == r) break;
-            r = ld16(pbase + q);
+            r = ld16(pbase + q);   // benign-race
             if (r == q) break;
         }
-        P(c) = uint16_t(r);
+        P(c) = uint16_t(r);   // benign-race: the root is a later vertex of every path through c
         const int bz = r >> 11;
         const int32_t t = *reinterpret_cast<const int32_t *>(reinterpret_cast<const char *>(ptab) + ((r & (2 * PS - 2)) << 1));
         // exit: the root is in the halo shell of the box, or (last tile of a
@@ -501,7 +503,12 @@ __global__ void __launch_bounds__(kThreads, 2)
         if (kInterior || ok) {
             A.label[i_col + z * nxy] = exit ? int32_t(uint32_t(root) | kFlag) : root;
             if (exit && !A.no_elist) used[r] = 1;
+            n_exit += exit;
         }
+    }
+    if (A.exit_count) {
+        const unsigned sum = __reduce_add_sync(0xffffffffu, unsigned(n_exit));
+        if (tx == 0 && sum) atomicAdd(A.exit_count, (unsigned long long)sum);
     }
 
     // ---- maxima and saddles of this column, appended (unordered) to the
@@ -650,7 +657,7 @@ static cudaError_t upload(T **d, const std::vector<T> &h) {
 
 eg_status tiled3d_local(Tiled3D *t, int ndim, const int64_t *dims, const Slab &s, const FieldView &F, int32_t *labels,
                         int *flags, cudaStream_t st, eg_stats *stats, std::string *err, cudaEvent_t ev_main0,
-                        cudaEvent_t ev_main1) {
+                        cudaEvent_t ev_main1, unsigned long long *exit_count) {
     int64_t d3[3] = {1, 1, 1};
     for (int i = 0; i < ndim; ++i) d3[i] = dims[i];
     cudaError_t e;
@@ -811,6 +818,8 @@ eg_status tiled3d_local(Tiled3D *t, int ndim, const int64_t *dims, const Slab &s
         A.shell = t->d_shell;
         A.btiles = t->d_btiles;
         A.rounds = t->rounds;
+        A.exit_count = exit_count;
+        stats->tile_rounds = t->rounds;
         // One slab: no exit list, the finalize pass chases (C3: 0.6 ms faster;
         // with L1-cached chase loads also for L2-resident label arrays: C2
         // 2.95 vs 2.97 ms, F1-256 0.30 vs 0.34 ms).  EG_ELIST=1 / 0 forces
@@ -832,9 +841,10 @@ eg_status tiled3d_local(Tiled3D *t, int ndim, const int64_t *dims, const Slab &s
             A.mx = ((uint64_t(1) << 32) + uint64_t(A.tiles_x) - 1) / uint64_t(A.tiles_x);
             A.my = ((uint64_t(1) << 32) + uint64_t(A.tiles_y) - 1) / uint64_t(A.tiles_y);
             A.n_tiles = int32_t(nt);
-            // persistent CTAs (2 per SM) on the one-slab TMA path (EG_PERSIST=0: one CTA per tile)
+            // persistent CTAs (2 per SM) on the one-slab TMA path: measured slower
+            // on C3 (6.27 vs 5.65 ms), so only on request (EG_PERSIST=1)
             const char *pe = std::getenv("EG_PERSIST");
-            const bool persist = A.no_elist && A.tma && !(pe && pe[0] == '0') && nt > 2 * t->n_sm;
+            const bool persist = A.no_elist && A.tma && (pe && pe[0] == '1') && nt > 2 * t->n_sm;
             if (persist)
                 k_tile<true, true><<<unsigned(2 * t->n_sm), kThreads, kTileSmem, st>>>(tmap, A, D);
             else

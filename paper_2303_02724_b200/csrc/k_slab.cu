@@ -94,10 +94,14 @@ cudaError_t launch_bval_update(int32_t *bval, const int32_t *hval_lo, const int3
 // chase: C3 3.13 ms vs 3.27 at kW = 4 or 8, 3.75 at 12; the smooth F1-1024
 // field prefers 8, 4.59 vs 5.18 ms; 128-thread blocks retire a block held by
 // one long chain sooner: C3 3.09 vs 3.12 ms at 256 or 64)
+// kStats (EG_STATS): hist[k] += vertices whose chase followed k exit
+// pointers (k >= 15 in hist[15]), hist[16] = max over vertices.
 constexpr int kW = 6;
+template <bool kStats>
 __global__ void __launch_bounds__(128, 16) k_finalize(int32_t *label, const uint32_t *__restrict__ bits, int64_t v0,
                                                   int64_t v1, const int32_t *__restrict__ hlo,
-                                                  const int32_t *__restrict__ hhi, int64_t plane) {
+                                                  const int32_t *__restrict__ hhi, int64_t plane,
+                                                  unsigned long long *hist) {
     const int64_t n = v1 - v0;
     const int64_t words = (n + 31) / 32;
     const int64_t w0 = (int64_t(blockIdx.x) * (blockDim.x / 32) + (threadIdx.x >> 5)) * kW;
@@ -134,15 +138,28 @@ __global__ void __launch_bounds__(128, 16) k_finalize(int32_t *label, const uint
 #pragma unroll
         for (int k = 0; k < kW; ++k)
             if (need[k]) e[k] = label[(e[k] & 0x7fffffff) - v0];
+        int hops[kW];
 #pragma unroll
         for (int k = 0; k < kW; ++k) {
+            hops[k] = need[k] ? 1 : 0;
             if (need[k] && e[k] < 0) {
                 int32_t w = e[k];
                 do {
                     w = __ldca(label + ((w & 0x7fffffff) - v0));
+                    if (kStats) ++hops[k];
                 } while (w < 0);
                 e[k] = w;
             }
+        }
+        if (kStats) {
+            int mx = 0;
+#pragma unroll
+            for (int k = 0; k < kW; ++k) {
+                if (need[k]) atomicAdd(hist + min(hops[k], 15), 1ull);
+                mx = max(mx, hops[k]);
+            }
+            mx = __reduce_max_sync(0xffffffffu, unsigned(mx));
+            if (lane == 0 && mx) atomicMax(hist + 16, (unsigned long long)mx);
         }
 #pragma unroll
         for (int k = 0; k < kW; ++k)
@@ -154,7 +171,7 @@ __global__ void __launch_bounds__(128, 16) k_finalize(int32_t *label, const uint
         if (need[k]) {
             int64_t x = e[k] & 0x7fffffff;
             if (x >= v0 && x < v1) {
-                const int32_t w = __ldg(label + (x - v0));
+                const int32_t w = __ldca(label + (x - v0));   // written by this kernel: not the read-only path
                 if (w >= 0) {
                     e[k] = w;
                     continue;
@@ -170,10 +187,15 @@ __global__ void __launch_bounds__(128, 16) k_finalize(int32_t *label, const uint
 }
 
 cudaError_t launch_finalize(int32_t *label, const uint32_t *bits, int64_t v0, int64_t v1, const int32_t *hval_lo,
-                            const int32_t *hval_hi, int64_t plane, cudaStream_t st) {
+                            const int32_t *hval_hi, int64_t plane, cudaStream_t st, unsigned long long *hist) {
     const int64_t words = (v1 - v0 + 31) / 32;
     if (words <= 0) return cudaSuccess;
-    k_finalize<<<blocks_for(words, 4 * kW), 128, 0, st>>>(label, bits, v0, v1, hval_lo, hval_hi, plane);
+    if (hist)
+        k_finalize<true><<<blocks_for(words, 4 * kW), 128, 0, st>>>(label, bits, v0, v1, hval_lo, hval_hi, plane,
+                                                                     hist);
+    else
+        k_finalize<false><<<blocks_for(words, 4 * kW), 128, 0, st>>>(label, bits, v0, v1, hval_lo, hval_hi, plane,
+                                                                      nullptr);
     return cudaGetLastError();
 }
 

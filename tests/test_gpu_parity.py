@@ -559,6 +559,23 @@ def test_simplify(eg, ctx, dims, kind, minimum):
             assert first_diff(a, b) is None, f"{name} tau={tau}: {first_diff(a, b)}"
 
 
+@pytest.mark.parametrize("k", [2, 3, 5])
+def test_node_values_with_virtual_parts(eg, ctx, k):
+    """EG_NODE_VALUES (bit 8) and EG_VIRTUAL_PARTS(k) (bits 16-31) are
+    independent flag fields (odd k used to switch node values on)."""
+    import torch
+    f, dims = G.random_field([23, 19, 17], 70 + k, "normal")
+    o = O.grid(f, dims)
+    g = ctx.compute(torch.from_numpy(f).cuda(), dims=dims, flags=eg.EG_NODE_VALUES | eg.EG_VIRTUAL_PARTS(k))
+    assert_graph_equal(g, o, what=f"node values + {k} virtual parts")
+    s = ctx.simplify(0.25)
+    e = O.simplify(o, f, 0.25)
+    assert np.array_equal(s.maxima, e.maxima) and np.array_equal(s.arcs, e.arcs)
+    # a rank type without node values but with virtual parts of an even / odd count
+    g = ctx.compute(torch.from_numpy(f.astype(np.float64)).cuda(), dims=dims)
+    assert_graph_equal(g, o, what="float64 rank image")
+
+
 def test_simplify_csr_and_state(eg, ctx):
     import torch
     X, f = G.gmm_points(4000, seed=8)
