@@ -10,7 +10,7 @@
 //           S1  the gradient = SoS argmax of the closed star,
 //               separably: closed star = box(v) u box(v - 1), box(w) = w + {0,1}^3,
 //               so the argmax is 2x2 in-plane maxima combined across z;
-//           S3  the 14-bit upper mask -> "beta0+ >= 2" from a 2 KB bit LUT
+//           S3  the 14-bit upper mask -> a 2-bit class code (saddle: beta0+ >= 2, maximum: empty mask) from a 4 KB LUT
 //               (Table 1; maximum iff the mask is empty).
 //         The gradients are stored as 16-bit byte offsets into a pointer box and
 //         compressed in shared memory (S2 inside the tile): every vertex ends
@@ -48,7 +48,7 @@ constexpr int PS = 1024;                             // pointer-box plane stride
 constexpr int PBOX = BZ * PS;                        // 18432 cells; pointers are byte offsets 2 r < 65536 (16 bits)
 constexpr int kThreads = TX * TY;                    // one z-column per thread
 constexpr int kWarps = kThreads / 32;
-constexpr int kLutWords = (1 << 14) / 32;            // 1 bit per 14-bit upper mask: beta0+ >= 2
+constexpr int kLutWords = (1 << 14) / 16;            // 2 bits per 14-bit upper mask: beta0+ >= 2, beta0+ == 0
 constexpr uint32_t kFlag = 0x80000000u;              // label bit 31: exit (not yet final)
 #ifndef EG_S1_UNROLL
 #define EG_S1_UNROLL 4
@@ -235,7 +235,7 @@ __device__ __forceinline__ void load_plane(float *fbox, int bz, const float *src
 // (the shell is never written afterwards), and the next tile's field box is
 // requested by TMA as soon as S1 has consumed the current one, so the copy
 // runs behind S2 and the label stores.
-template <bool kInterior, bool kPersist>
+template <bool kInterior, bool kPersist, bool kStats = false>
 __global__ void __launch_bounds__(kThreads, 2)
     k_tile(const __grid_constant__ CUtensorMap tmap, TileArgs A, Dims3 D) {
     extern __shared__ __align__(128) unsigned char smem[];
@@ -390,7 +390,7 @@ __global__ void __launch_bounds__(kThreads, 2)
     star(1, p0);
     VK bm_prev = bminus(pm, -1);       // B-(z-1) for z = 0
     VK bp_cur = bplus(p0, 0);          // B+(z)   for z = 0
-    uint32_t sad_mask = 0, max_mask = 0;
+    uint32_t cls = 0;                  // 2-bit class codes of the column's 16 vertices
 #pragma unroll kS1Unroll
     for (int z = 0; z < TZ; ++z) {
         star(z + 2, pp);
@@ -426,15 +426,25 @@ __global__ void __launch_bounds__(kThreads, 2)
         d = mask ? d : 0;
         const int c = cfb + 2 * (z + 1) * PS;
         P(c) = uint16_t(kInterior || ok ? c + d : c);
-        const uint32_t sad = (lut[mask >> 5] >> (mask & 31)) & 1u;
-        sad_mask |= ((kInterior || ok) ? sad : 0u) << z;
-        max_mask |= ((kInterior || ok) && mask == 0) ? (1u << z) : 0u;
+        // 2-bit class code from the LUT: bit 0 saddle (beta0+ >= 2), bit 1
+        // maximum (empty mask); interleaved, vertex z at bits 2z, 2z + 1
+        const uint32_t code = (lut[mask >> 4] >> ((mask & 15) << 1)) & 3u;
+        cls |= ((kInterior || ok) ? code : 0u) << (2 * z);
 #pragma unroll
         for (int k = 0; k < 7; ++k) {
             pm[k] = p0[k];
             p0[k] = pp[k];
         }
     }
+    // deinterleave: even bits -> saddles, odd bits -> maxima
+    auto compact = [](uint32_t x) {        // bits 0, 2, 4, ... -> 0, 1, 2, ...
+        x &= 0x55555555u;
+        x = (x | (x >> 1)) & 0x33333333u;
+        x = (x | (x >> 2)) & 0x0f0f0f0fu;
+        x = (x | (x >> 4)) & 0x00ff00ffu;
+        return (x | (x >> 8)) & 0x0000ffffu;
+    };
+    const uint32_t sad_mask = compact(cls), max_mask = compact(cls >> 1);
     // NaN (reading L2): a NaN vertex compares false with everything, so its
     // upper mask is empty -- only the (rare) maxima need the test
     for (uint32_t m = max_mask; m; m &= m - 1) {
@@ -503,10 +513,10 @@ __global__ void __launch_bounds__(kThreads, 2)
         if (kInterior || ok) {
             A.label[i_col + z * nxy] = exit ? int32_t(uint32_t(root) | kFlag) : root;
             if (exit && !A.no_elist) used[r] = 1;
-            n_exit += exit;
+            if (kStats) n_exit += exit;
         }
     }
-    if (A.exit_count) {
+    if (kStats) {
         const unsigned sum = __reduce_add_sync(0xffffffffu, unsigned(n_exit));
         if (tx == 0 && sum) atomicAdd(A.exit_count, (unsigned long long)sum);
     }
@@ -662,14 +672,16 @@ eg_status tiled3d_local(Tiled3D *t, int ndim, const int64_t *dims, const Slab &s
     for (int i = 0; i < ndim; ++i) d3[i] = dims[i];
     cudaError_t e;
     if (!t->ready) {
-        // 1-bit LUT: is beta0+ >= 2 for every 14-bit upper mask of the 3-D link,
+        // 2-bit LUT: beta0+ >= 2 (bit 0) and empty mask (bit 1) for every 14-bit upper mask of the 3-D link,
         // in the ascending-index offset order (lexicographic in (dz, dy, dx))
         int64_t dl[3] = {4, 4, 4};
         LinkTable tab = make_link_table(3, dl);
         std::vector<uint8_t> beta = make_beta_lut3(tab);
         std::vector<uint32_t> bits(kLutWords, 0u);
-        for (int m = 0; m < (1 << 14); ++m)
-            if (beta[m] >= 2) bits[m >> 5] |= 1u << (m & 31);
+        for (int m = 0; m < (1 << 14); ++m) {
+            const uint32_t code = (beta[m] >= 2 ? 1u : 0u) | (m == 0 ? 2u : 0u);
+            bits[m >> 4] |= code << ((m & 15) * 2);
+        }
         if ((e = upload(&t->d_lut, bits)) != cudaSuccess) return fail(err, e, "lut upload");
         // pointer-box indices of the halo shell
         std::vector<uint16_t> sh;
@@ -690,6 +702,10 @@ eg_status tiled3d_local(Tiled3D *t, int ndim, const int64_t *dims, const Slab &s
             (e = cudaFuncSetAttribute(k_tile<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       int(kTileSmem))) != cudaSuccess ||
             (e = cudaFuncSetAttribute(k_tile<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      int(kTileSmem))) != cudaSuccess ||
+            (e = cudaFuncSetAttribute(k_tile<true, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      int(kTileSmem))) != cudaSuccess ||
+            (e = cudaFuncSetAttribute(k_tile<false, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       int(kTileSmem))) != cudaSuccess)
             return fail(err, e, "smem attr");
         int dev = 0;
@@ -829,7 +845,10 @@ eg_status tiled3d_local(Tiled3D *t, int ndim, const int64_t *dims, const Slab &s
         A.tma = tma ? 1 : 0;
         if (ev_main0) cudaEventRecord(ev_main0, st);
         if (t->n_btiles > 0) {
-            k_tile<false, false><<<unsigned(t->n_btiles), kThreads, kTileSmem, st>>>(tmap, A, D);
+            if (A.exit_count)
+                k_tile<false, false, true><<<unsigned(t->n_btiles), kThreads, kTileSmem, st>>>(tmap, A, D);
+            else
+                k_tile<false, false><<<unsigned(t->n_btiles), kThreads, kTileSmem, st>>>(tmap, A, D);
             stats->kernel_launches += 1;
             if ((e = cudaGetLastError()) != cudaSuccess) return fail(err, e, "k_tile<boundary>");
         }
@@ -847,6 +866,8 @@ eg_status tiled3d_local(Tiled3D *t, int ndim, const int64_t *dims, const Slab &s
             const bool persist = A.no_elist && A.tma && (pe && pe[0] == '1') && nt > 2 * t->n_sm;
             if (persist)
                 k_tile<true, true><<<unsigned(2 * t->n_sm), kThreads, kTileSmem, st>>>(tmap, A, D);
+            else if (A.exit_count)
+                k_tile<true, false, true><<<unsigned(nt), kThreads, kTileSmem, st>>>(tmap, A, D);
             else
                 k_tile<true, false><<<unsigned(nt), kThreads, kTileSmem, st>>>(tmap, A, D);
             stats->kernel_launches += 1;
