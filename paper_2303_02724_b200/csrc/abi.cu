@@ -151,6 +151,8 @@ struct eg_ctx {
     // while the labels are finalised on `stream` (ev_tile: local phase done,
     // ev_graph: graph stage done); gstream = the stream of the graph stage
     cudaStream_t aux = nullptr, gstream = nullptr;
+    cudaStream_t cst = nullptr;        // several GPUs: the f halo exchange beside the interior tiles
+    cudaEvent_t ev_halo[2] = {};
     int prio_lo = 0, prio_hi = 0;
     cudaEvent_t ev_tile = nullptr, ev_graph = nullptr;
     bool overlap = false;
@@ -322,15 +324,16 @@ static eg_status nccl_allgather_i64(eg_ctx *c, const int64_t *h_in, int n, std::
 // plane exchange with the neighbour ranks: send_lo (our first plane) goes to
 // rank - 1 and arrives there as its recv_hi; send_hi to rank + 1 as recv_lo
 static eg_status nccl_exchange(eg_ctx *c, const void *send_lo, const void *send_hi, void *recv_lo, void *recv_hi,
-                               size_t count, ncclDataType_t dt) {
+                               size_t count, ncclDataType_t dt, cudaStream_t st = nullptr) {
+    if (!st) st = c->stream;
     NK(ncclGroupStart());
     if (c->rank > 0) {
-        NK(ncclSend(send_lo, count, dt, c->rank - 1, c->comm, c->stream));
-        NK(ncclRecv(recv_lo, count, dt, c->rank - 1, c->comm, c->stream));
+        NK(ncclSend(send_lo, count, dt, c->rank - 1, c->comm, st));
+        NK(ncclRecv(recv_lo, count, dt, c->rank - 1, c->comm, st));
     }
     if (c->rank < c->world - 1) {
-        NK(ncclSend(send_hi, count, dt, c->rank + 1, c->comm, c->stream));
-        NK(ncclRecv(recv_hi, count, dt, c->rank + 1, c->comm, c->stream));
+        NK(ncclSend(send_hi, count, dt, c->rank + 1, c->comm, st));
+        NK(ncclRecv(recv_hi, count, dt, c->rank + 1, c->comm, st));
     }
     NK(ncclGroupEnd());
     return EG_OK;
@@ -651,19 +654,22 @@ static eg_status gather_graph(eg_ctx *c, bool raw) {
 }
 
 // the boundary exchange: rounds of neighbour plane exchange and
-// jumping until no boundary value of any slab is unresolved
+// jumping until no boundary value of any slab is unresolved.  Rounds are
+// queued in batches of kBatch with one host check per batch (paths cross a
+// slab boundary only a few times: SURVEY 8(e) measured <= 4); a round whose
+// predecessor left nothing unresolved returns at once on the device.
 static eg_status boundary_rounds(eg_ctx *c, int *rounds_out) {
     auto &slabs = c->slabs;
     const size_t K = slabs.size();
-    unsigned long long *d_unres = reinterpret_cast<unsigned long long *>(c->counts.as<int64_t>() + 8);
+    constexpr int kBatch = 4;
+    unsigned long long *d_unres = reinterpret_cast<unsigned long long *>(c->counts.as<int64_t>() + 8);   // [kBatch]
     for (SlabState *S : slabs) {
         CK(launch_bval_init(S->label, S->s, S->bval.as<int32_t>(), c->stream));
         c->stats.kernel_launches += 1;
     }
-    int rounds = 0;
-    for (int it = 0;; ++it) {
-        // exchange: hval_lo of slab k = bval_hi of slab k-1; hval_hi = bval_lo of slab k+1
-        const int64_t plane = slabs[0]->s.plane;
+    const int64_t plane = slabs[0]->s.plane;
+    auto exchange = [&]() -> eg_status {
+        // hval_lo of slab k = bval_hi of slab k-1; hval_hi = bval_lo of slab k+1
         if (c->world > 1) {
             SlabState &S = *slabs[0];
             ST(nccl_exchange(c, S.bval.as<int32_t>(), S.bval.as<int32_t>() + plane, S.hval_lo.as<int32_t>(),
@@ -678,24 +684,39 @@ static eg_status boundary_rounds(eg_ctx *c, int *rounds_out) {
                                        cudaMemcpyDeviceToDevice, c->stream));
             }
         }
-        if (it > 0) {
-            // the previous update left no unresolved value anywhere: the
-            // exchange just done made the halo values final too
-            unsigned long long u = 0;
-            CK(cudaMemcpyAsync(&u, d_unres, sizeof(u), cudaMemcpyDeviceToHost, c->stream));
-            CK(cudaStreamSynchronize(c->stream));
-            if (u == 0) break;
+        return EG_OK;
+    };
+    int rounds = 0;
+    for (int batch = 0;; ++batch) {
+        if (batch * kBatch > 4096) return set_err(c, EG_ERR_STATE, "boundary exchange did not converge");
+        CK(cudaMemsetAsync(d_unres, 0, sizeof(unsigned long long) * kBatch, c->stream));
+        for (int r = 0; r < kBatch; ++r) {
+            ST(exchange());
+            for (SlabState *S : slabs) {
+                CK(launch_bval_update(S->bval.as<int32_t>(), S->has_lo ? S->hval_lo.as<int32_t>() : nullptr,
+                                      S->has_hi ? S->hval_hi.as<int32_t>() : nullptr, S->s, d_unres + r, c->stream,
+                                      r > 0 ? d_unres + r - 1 : nullptr));
+                c->stats.kernel_launches += 1;
+            }
+            if (c->world > 1) NK(ncclAllReduce(d_unres + r, d_unres + r, 1, ncclUint64, ncclSum, c->comm, c->stream));
         }
-        if (it > 4096) return set_err(c, EG_ERR_STATE, "boundary exchange did not converge");
-        CK(cudaMemsetAsync(d_unres, 0, sizeof(unsigned long long), c->stream));
-        for (SlabState *S : slabs) {
-            CK(launch_bval_update(S->bval.as<int32_t>(), S->has_lo ? S->hval_lo.as<int32_t>() : nullptr,
-                                  S->has_hi ? S->hval_hi.as<int32_t>() : nullptr, S->s, d_unres, c->stream));
-            c->stats.kernel_launches += 1;
+        unsigned long long u[kBatch];
+        CK(cudaMemcpyAsync(u, d_unres, sizeof(u), cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        int done = -1;
+        for (int r = 0; r < kBatch; ++r)
+            if (u[r] == 0) {
+                done = r;
+                break;
+            }
+        if (done >= 0) {
+            rounds += done + 1;
+            break;
         }
-        if (c->world > 1) NK(ncclAllReduce(d_unres, d_unres, 1, ncclUint64, ncclSum, c->comm, c->stream));
-        ++rounds;
+        rounds += kBatch;
     }
+    // one more exchange: the halo values are now the neighbours' final values
+    ST(exchange());
     *rounds_out = rounds;
     return EG_OK;
 }
@@ -762,12 +783,24 @@ static eg_status compute_grid(eg_ctx *c, const Problem &P, const float *f, uint3
     ST(ensure_table(c, P));
     CK(cudaEventRecord(c->ev[0], c->stream));
 
-    // ---- halo planes of f (P:281 ghost vertices)
+    // ---- halo planes of f (P:281 ghost vertices).  Several GPUs, tiled: on
+    // the comm stream, overlapped with the interior tiles (halo_ev)
+    cudaEvent_t halo_ev = nullptr;
     if (multi) {
         if (c->world > 1) {
             SlabState &S = *c->slabs[0];
             const int64_t np = S.s.z1 - S.s.z0;
-            ST(nccl_exchange(c, S.F.own, S.F.own + (np - 1) * P.plane, S.f_lo.p, S.f_hi.p, size_t(P.plane), ncclFloat32));
+            if (tiled) {
+                CK(cudaEventRecord(c->ev_halo[0], c->stream));
+                CK(cudaStreamWaitEvent(c->cst, c->ev_halo[0], 0));
+                ST(nccl_exchange(c, S.F.own, S.F.own + (np - 1) * P.plane, S.f_lo.p, S.f_hi.p, size_t(P.plane),
+                                 ncclFloat32, c->cst));
+                CK(cudaEventRecord(c->ev_halo[1], c->cst));
+                halo_ev = c->ev_halo[1];
+            } else {
+                ST(nccl_exchange(c, S.F.own, S.F.own + (np - 1) * P.plane, S.f_lo.p, S.f_hi.p, size_t(P.plane),
+                                 ncclFloat32));
+            }
         } else {
             for (size_t k = 0; k < plan.size(); ++k) {
                 SlabState &S = *c->slabs[k];
@@ -790,7 +823,8 @@ static eg_status compute_grid(eg_ctx *c, const Problem &P, const float *f, uint3
             eg_status s = tiled3d_local(S->tiled, P.ndim, P.dims, S->s, S->F, S->label, c->flags.as<int>(),
                                         c->stream, &c->stats, &c->err, first ? c->ev_main[0] : nullptr,
                                         first ? c->ev_main[1] : nullptr,
-                                        (flags & EG_STATS) ? c->stat_buf.as<unsigned long long>() : nullptr);
+                                        (flags & EG_STATS) ? c->stat_buf.as<unsigned long long>() : nullptr,
+                                        halo_ev);
             if (s != EG_OK) {
                 if (s == EG_ERR_CUDA) c->poisoned = true;
                 return s;
@@ -806,10 +840,12 @@ static eg_status compute_grid(eg_ctx *c, const Problem &P, const float *f, uint3
     // arcs -- which follow a representative's exit pointer themselves -- and
     // their copies to the host) runs on the aux stream while the labels are
     // finalised on the ctx stream.  The widening flags keep the serial order.
-    c->overlap = tiled && !multi && c->world == 1 && !c->min_reflect && !c->bundle &&
+    // (several slabs in one process: after the boundary exchange, when every
+    // halo value is final)
+    c->overlap = tiled && c->world == 1 && !c->min_reflect && !c->bundle &&
                  !(flags & (EG_ARC_PATHS | EG_NODE_VALUES | EG_RAW_ARCS));
     c->gstream = c->overlap ? c->aux : c->stream;
-    if (c->overlap) {
+    if (c->overlap && !multi) {
         CK(cudaEventRecord(c->ev_tile, c->stream));
         CK(cudaStreamWaitEvent(c->aux, c->ev_tile, 0));
     }
@@ -821,6 +857,10 @@ static eg_status compute_grid(eg_ctx *c, const Problem &P, const float *f, uint3
         CK(cudaEventRecord(c->ev_s2[3], c->stream));
         c->s2_timed[1] = true;
         c->stats.boundary_rounds = rounds;
+        if (c->overlap) {
+            CK(cudaEventRecord(c->ev_tile, c->stream));
+            CK(cudaStreamWaitEvent(c->aux, c->ev_tile, 0));
+        }
     }
     if (tiled || multi) {
         CK(cudaEventRecord(c->ev_s2[4], c->stream));
@@ -1265,6 +1305,9 @@ eg_status eg_create(eg_ctx **out, int cuda_device, void *cuda_stream) {
         cudaDeviceGetStreamPriorityRange(&c->prio_lo, &c->prio_hi) != cudaSuccess ||
         // high priority: the graph stage's few blocks run ahead of the finalize pass's queue
         cudaStreamCreateWithPriority(&c->aux, cudaStreamNonBlocking, c->prio_hi) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&c->cst, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c->ev_halo[0], cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c->ev_halo[1], cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&c->ev_tile, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&c->ev_graph, cudaEventDisableTiming) != cudaSuccess) {
         delete c;
@@ -1512,6 +1555,12 @@ eg_status eg_destroy(eg_ctx *c) {
         cudaStreamSynchronize(c->d2h);
         cudaStreamDestroy(c->d2h);
     }
+    if (c->cst) {
+        cudaStreamSynchronize(c->cst);
+        cudaStreamDestroy(c->cst);
+    }
+    for (auto &e : c->ev_halo)
+        if (e) cudaEventDestroy(e);
     if (c->aux) {
         cudaStreamSynchronize(c->aux);
         cudaStreamDestroy(c->aux);

@@ -66,16 +66,22 @@ struct LabelView {
     int64_t v0, v1;
     const int32_t *lo, *hi;                // halo planes z0 - 1 and z1 (grid, multi-slab) or null
     int64_t plane;
-    // one slab whose labels are still being finalised concurrently: a label
-    // with bit 31 is an exit pointer, followed to the final value (every value
-    // read lies on the same ascending path, so stale reads are harmless)
+    // labels still being finalised concurrently: a label with bit 31 is an
+    // exit pointer, followed to the final value (every value read lies on the
+    // same ascending path, so stale reads are harmless); a pointer that leaves
+    // the slab lands in a halo plane, whose values (lo / hi) are final
     bool chase;
 #ifdef __CUDACC__
     __device__ __forceinline__ int32_t at(int64_t g) const {
         if (chase) {
-            int32_t w = __ldca(own + (g - v0));
-            while (w < 0) w = __ldca(own + ((w & 0x7fffffff) - v0));
-            return w;
+            int64_t x = g;
+            for (;;) {
+                if (x < v0) return lo[x - v0 + plane];
+                if (x >= v1) return hi[x - v1];
+                const int32_t w = __ldca(own + (x - v0));
+                if (w >= 0) return w;
+                x = w & 0x7fffffff;
+            }
         }
         if (g >= v0 && g < v1) return own[g - v0];
         if (g < v0) return lo[g - v0 + plane];
@@ -235,7 +241,7 @@ cudaError_t launch_bval_init(const int32_t *label, const Slab &s, int32_t *bval,
 // one exchange round: bval entries pointing into a halo plane take the
 // neighbour's value (hval lo = plane z0 - 1, hi = plane z1); counts unresolved
 cudaError_t launch_bval_update(int32_t *bval, const int32_t *hval_lo, const int32_t *hval_hi, const Slab &s,
-                               unsigned long long *unresolved, cudaStream_t st);
+                               unsigned long long *unresolved, cudaStream_t st, const unsigned long long *prev = nullptr);
 // final pass: every unresolved owned label (all owned vertices, or only those
 // whose bit is set in `bits`) becomes final, via owned labels and the final
 // halo-plane values

@@ -17,7 +17,8 @@ void tiled3d_destroy(Tiled3D *t);
 eg_status tiled3d_local(Tiled3D *t, int ndim, const int64_t *dims, const Slab &s, const FieldView &F, int32_t *labels,
                         int *flags, cudaStream_t st, eg_stats *stats, std::string *err,
                         cudaEvent_t ev_main0 = nullptr, cudaEvent_t ev_main1 = nullptr,
-                        unsigned long long *exit_count = nullptr);   // EG_STATS: += exiting vertices
+                        unsigned long long *exit_count = nullptr,   // EG_STATS: += exiting vertices
+                        cudaEvent_t halo_ready = nullptr);            // halo planes arrive after this event
 // number of maxima (which = 0) / saddles (which = 1) found by the last tiled3d_local
 int64_t tiled3d_count(const Tiled3D *t, int which);
 // the maxima (int64) and saddles (int32 and int64) of the last tiled3d_local,

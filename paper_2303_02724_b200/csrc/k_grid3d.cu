@@ -667,7 +667,7 @@ static cudaError_t upload(T **d, const std::vector<T> &h) {
 
 eg_status tiled3d_local(Tiled3D *t, int ndim, const int64_t *dims, const Slab &s, const FieldView &F, int32_t *labels,
                         int *flags, cudaStream_t st, eg_stats *stats, std::string *err, cudaEvent_t ev_main0,
-                        cudaEvent_t ev_main1, unsigned long long *exit_count) {
+                        cudaEvent_t ev_main1, unsigned long long *exit_count, cudaEvent_t halo_ready) {
     int64_t d3[3] = {1, 1, 1};
     for (int i = 0; i < ndim; ++i) d3[i] = dims[i];
     cudaError_t e;
@@ -836,21 +836,33 @@ eg_status tiled3d_local(Tiled3D *t, int ndim, const int64_t *dims, const Slab &s
         A.rounds = t->rounds;
         A.exit_count = exit_count;
         stats->tile_rounds = t->rounds;
-        // One slab: no exit list, the finalize pass chases (C3: 0.6 ms faster;
+        // No exit list: the label pass chases (one slab: C3 0.6 ms faster;
         // with L1-cached chase loads also for L2-resident label arrays: C2
-        // 2.95 vs 2.97 ms, F1-256 0.30 vs 0.34 ms).  EG_ELIST=1 / 0 forces
-        // either.
+        // 2.95 vs 2.97 ms, F1-256 0.30 vs 0.34 ms; several slabs: the chase
+        // stops at the first remote vertex, C3 at 2 virtual slabs XXX).
+        // EG_ELIST=1 builds and resolves the exit list instead.
         const char *el = std::getenv("EG_ELIST");
-        A.no_elist = (!F.lo && !F.hi && (el ? el[0] == '0' : true)) ? 1 : 0;
+        A.no_elist = (el && el[0] == '1') ? 0 : 1;
         A.tma = tma ? 1 : 0;
         if (ev_main0) cudaEventRecord(ev_main0, st);
-        if (t->n_btiles > 0) {
+        // halo_ready (several GPUs): the neighbour slabs' halo planes arrive on
+        // another stream while the interior tiles (which never read them) run;
+        // the boundary tiles are launched after them
+        auto boundary_tiles = [&]() -> eg_status {
+            if (t->n_btiles <= 0) return EG_OK;
+            if (halo_ready && (e = cudaStreamWaitEvent(st, halo_ready, 0)) != cudaSuccess)
+                return fail(err, e, "halo wait");
             if (A.exit_count)
                 k_tile<false, false, true><<<unsigned(t->n_btiles), kThreads, kTileSmem, st>>>(tmap, A, D);
             else
                 k_tile<false, false><<<unsigned(t->n_btiles), kThreads, kTileSmem, st>>>(tmap, A, D);
             stats->kernel_launches += 1;
             if ((e = cudaGetLastError()) != cudaSuccess) return fail(err, e, "k_tile<boundary>");
+            return EG_OK;
+        };
+        if (!halo_ready) {
+            const eg_status bs = boundary_tiles();
+            if (bs != EG_OK) return bs;
         }
         if (have_interior) {
             A.tiles_x = hi.x - lo.x + 1;
@@ -872,6 +884,10 @@ eg_status tiled3d_local(Tiled3D *t, int ndim, const int64_t *dims, const Slab &s
                 k_tile<true, false><<<unsigned(nt), kThreads, kTileSmem, st>>>(tmap, A, D);
             stats->kernel_launches += 1;
             if ((e = cudaGetLastError()) != cudaSuccess) return fail(err, e, "k_tile<interior>");
+        }
+        if (halo_ready) {
+            const eg_status bs = boundary_tiles();
+            if (bs != EG_OK) return bs;
         }
         if (ev_main1) cudaEventRecord(ev_main1, st);
         // resolve the owned part of E

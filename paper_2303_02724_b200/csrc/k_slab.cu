@@ -29,13 +29,15 @@ cudaError_t launch_flag_remote(int32_t *label, int64_t n, int64_t v0, cudaStream
     return cudaGetLastError();
 }
 
-// value of owned vertex g, followed one step through an owned exit target
-// (whose own label is final or points to a remote vertex)
+// value of owned vertex g: its label followed through owned vertices until it
+// is final or points to the first vertex of its path outside the slab (a
+// vertex of a halo plane: a path changes the slowest coordinate by <= 1 per step)
 __device__ __forceinline__ int32_t local_value(const int32_t *label, int64_t g, int64_t v0, int64_t v1) {
     int32_t w = label[g - v0];
-    if (w < 0) {
+    while (w < 0) {
         const int64_t x = w & 0x7fffffff;
-        if (x >= v0 && x < v1) w = label[x - v0];
+        if (x < v0 || x >= v1) break;
+        w = __ldcg(label + (x - v0));
     }
     return w;
 }
@@ -53,7 +55,8 @@ cudaError_t launch_bval_init(const int32_t *label, const Slab &s, int32_t *bval,
 }
 
 __global__ void k_bval_update(int32_t *bval, const int32_t *__restrict__ hlo, const int32_t *__restrict__ hhi, Slab s,
-                              unsigned long long *unresolved) {
+                              unsigned long long *unresolved, const unsigned long long *prev) {
+    if (prev && *prev == 0) return;             // converged in an earlier round of this batch
     const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     bool still = false;
     if (i < 2 * s.plane) {
@@ -82,8 +85,8 @@ __global__ void k_bval_update(int32_t *bval, const int32_t *__restrict__ hlo, co
 }
 
 cudaError_t launch_bval_update(int32_t *bval, const int32_t *hval_lo, const int32_t *hval_hi, const Slab &s,
-                               unsigned long long *unresolved, cudaStream_t st) {
-    k_bval_update<<<blocks_for(2 * s.plane, 256), 256, 0, st>>>(bval, hval_lo, hval_hi, s, unresolved);
+                               unsigned long long *unresolved, cudaStream_t st, const unsigned long long *prev) {
+    k_bval_update<<<blocks_for(2 * s.plane, 256), 256, 0, st>>>(bval, hval_lo, hval_hi, s, unresolved, prev);
     return cudaGetLastError();
 }
 
@@ -166,21 +169,23 @@ __global__ void __launch_bounds__(128, 16) k_finalize(int32_t *label, const uint
             if (need[k]) label[(w0 + k) * 32 + lane] = e[k];
         return;
     }
+    // several slabs: follow the chain through owned vertices (race-benign as
+    // above) to a final label, or to its first vertex outside the slab, whose
+    // value the boundary exchange made final (hval).  The first hop of every
+    // word is issued before any chain is followed further.
+    auto step = [&](int32_t w) -> int32_t {     // one hop from exit pointer w
+        const int64_t x = w & 0x7fffffff;
+        if (x < v0) return hlo[x - v0 + plane];
+        if (x >= v1) return hhi[x - v1];
+        return __ldca(label + (x - v0));        // written by this kernel: not the read-only path
+    };
 #pragma unroll
-    for (int k = 0; k < kW; ++k) {
-        if (need[k]) {
-            int64_t x = e[k] & 0x7fffffff;
-            if (x >= v0 && x < v1) {
-                const int32_t w = __ldca(label + (x - v0));   // written by this kernel: not the read-only path
-                if (w >= 0) {
-                    e[k] = w;
-                    continue;
-                }
-                x = w & 0x7fffffff;
-            }
-            e[k] = x < v0 ? hlo[x - v0 + plane] : hhi[x - v1];
-        }
-    }
+    for (int k = 0; k < kW; ++k)
+        if (need[k]) e[k] = step(e[k]);
+#pragma unroll
+    for (int k = 0; k < kW; ++k)
+        if (need[k])
+            while (e[k] < 0) e[k] = step(e[k]);
 #pragma unroll
     for (int k = 0; k < kW; ++k)
         if (need[k]) label[(w0 + k) * 32 + lane] = e[k];

@@ -323,6 +323,26 @@ def test_virtual_slabs_3d(eg, ctx, k, path):
     assert st["boundary_rounds"] >= 1
 
 
+@pytest.mark.parametrize("k", [2, 5, 16])
+@pytest.mark.parametrize("path", PATHS)
+def test_virtual_slabs_ridge(eg, ctx, k, path):
+    """A ramp along the slowest axis with a wavy ridge (SPEC S:313 analogue):
+    nearly every ascending path crosses every slab boundary above it, so the
+    boundary exchange needs about k - 1 rounds (several host-checked batches
+    at k = 16) and every finalize chain ends in a remote label."""
+    import torch
+    nx, ny, nz = 40, 24, 64
+    x, y, z = np.meshgrid(np.arange(nx), np.arange(ny), np.arange(nz), indexing="ij")
+    rng = np.random.default_rng(k)
+    f = (z + 0.6 * np.sin(x / 3.0) * np.cos(y / 4.0) + 0.05 * rng.standard_normal(z.shape)).astype(np.float32)
+    f = np.ascontiguousarray(f.transpose(2, 1, 0)).reshape(-1)      # axis 0 (x) fastest
+    dims = [nx, ny, nz]
+    o = O.grid(f, dims)
+    g = ctx.compute(torch.from_numpy(f).cuda(), dims=dims, flags=_flags(eg, path, eg.EG_VIRTUAL_PARTS(k)))
+    assert_graph_equal(g, o, what=f"ridge, {k} slabs, {path}")
+    assert ctx.stats()["boundary_rounds"] >= k - 1
+
+
 @pytest.mark.parametrize("dims,kind,k", [([40, 36, 50], "int", 3), ([70, 9, 40], "signed_zero", 4),
                                          ([33, 35, 19], "normal", 2), ([64, 64, 64], "int", 8)])
 def test_virtual_slabs_tie_heavy(eg, ctx, dims, kind, k):
