@@ -839,7 +839,7 @@ eg_status tiled3d_local(Tiled3D *t, int ndim, const int64_t *dims, const Slab &s
         // No exit list: the label pass chases (one slab: C3 0.6 ms faster;
         // with L1-cached chase loads also for L2-resident label arrays: C2
         // 2.95 vs 2.97 ms, F1-256 0.30 vs 0.34 ms; several slabs: the chase
-        // stops at the first remote vertex, C3 at 2 virtual slabs XXX).
+        // stops at the first remote vertex: C3 at 2 / 4 virtual slabs 11.8 / 12.5 -> 9.9 / 10.2 ms).
         // EG_ELIST=1 builds and resolves the exit list instead.
         const char *el = std::getenv("EG_ELIST");
         A.no_elist = (el && el[0] == '1') ? 0 : 1;
