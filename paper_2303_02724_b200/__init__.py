@@ -163,16 +163,20 @@ class Context:
         return self._graph(getattr(self, "_last_flags", 0))
 
     def compute_host(self, field: torch.Tensor, dims=None, csr=None, flags: int = 0, labels_out=None,
-                     slab=None, v_range=None) -> Graph:
+                     slab=None, v_range=None, materialize: bool = True) -> Optional[Graph]:
         """End to end from a host (ideally pinned) float32 tensor; optional
-        host int32 labels_out receives the owned labels."""
+        host int32 labels_out (pinned: the library's chunked pipeline copies
+        each chunk's labels while later chunks of the field arrive) receives
+        the owned labels.  The graph is in host memory owned by the library
+        when this returns; materialize=False skips the numpy copies (graph())."""
         if field.is_cuda or field.dtype != torch.float32 or not field.is_contiguous():
             raise TypeError("field must be a contiguous host float32 tensor")
         dom = self._domain(dims, csr, slab, v_range)
         lp = C.c_void_p(labels_out.data_ptr()) if labels_out is not None else C.c_void_p()
         st = _abi.lib().eg_compute_host(self._h, C.byref(dom), C.c_void_p(field.data_ptr()), lp, flags)
         self._check(st, "eg_compute_host")
-        return self._graph(flags)
+        self._last_flags = flags
+        return self._graph(flags) if materialize else None
 
     def gradient(self, field: torch.Tensor, dims=None, csr=None, slab=None, v_range=None):
         """S1 + S3 per owned vertex: (ptr int32 global ids, beta0+ uint8)."""

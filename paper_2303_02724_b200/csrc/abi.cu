@@ -107,6 +107,7 @@ struct eg_ctx {
     std::vector<SlabState *> slabs;
     DevBuf label_all;                  // labels of every slab of this process
     DevBuf csr_scratch;                // CSR: int32[2 nnz + N]: upper lists, union-find parents, |U| per vertex
+    DevBuf fix_dev;                    // eg_compute_host pipeline: labels patched on the host
     DevBuf field;                      // eg_compute_host staging target
     DevBuf mirror;                     // EG_MINIMUM: g[i] = -f[N-1-i]
     DevBuf typed;                      // eg_compute_typed: the field converted to float32
@@ -152,6 +153,8 @@ struct eg_ctx {
     // ev_graph: graph stage done); gstream = the stream of the graph stage
     cudaStream_t aux = nullptr, gstream = nullptr;
     cudaStream_t cst = nullptr;        // several GPUs: the f halo exchange beside the interior tiles
+    cudaStream_t h2d = nullptr, ld2h = nullptr, fst = nullptr;   // eg_compute_host pipeline streams
+    ChunkIO *io = nullptr;             // set by eg_compute_host for the duration of one call
     cudaEvent_t ev_halo[2] = {};
     int prio_lo = 0, prio_hi = 0;
     cudaEvent_t ev_tile = nullptr, ev_graph = nullptr;
@@ -824,7 +827,7 @@ static eg_status compute_grid(eg_ctx *c, const Problem &P, const float *f, uint3
                                         c->stream, &c->stats, &c->err, first ? c->ev_main[0] : nullptr,
                                         first ? c->ev_main[1] : nullptr,
                                         (flags & EG_STATS) ? c->stat_buf.as<unsigned long long>() : nullptr,
-                                        halo_ev);
+                                        halo_ev, !multi ? c->io : nullptr);
             if (s != EG_OK) {
                 if (s == EG_ERR_CUDA) c->poisoned = true;
                 return s;
@@ -866,8 +869,11 @@ static eg_status compute_grid(eg_ctx *c, const Problem &P, const float *f, uint3
         CK(cudaEventRecord(c->ev_s2[4], c->stream));
         c->s2_timed[2] = true;
     }
+    const bool piped = c->io && c->io->done;      // eg_compute_host pipeline: labels finished on c->io->fst
+    if (piped) CK(cudaStreamWaitEvent(c->stream, c->io->fin_done, 0));
     for (SlabState *S : c->slabs) {
         if (!tiled && !multi) continue;           // generic single slab: already final
+        if (piped) continue;
         CK(launch_finalize(S->label, nullptr, S->s.v0, S->s.v1,
                            S->has_lo ? S->hval_lo.as<int32_t>() : nullptr,
                            S->has_hi ? S->hval_hi.as<int32_t>() : nullptr, P.plane, c->stream,
@@ -1306,6 +1312,9 @@ eg_status eg_create(eg_ctx **out, int cuda_device, void *cuda_stream) {
         // high priority: the graph stage's few blocks run ahead of the finalize pass's queue
         cudaStreamCreateWithPriority(&c->aux, cudaStreamNonBlocking, c->prio_hi) != cudaSuccess ||
         cudaStreamCreateWithFlags(&c->cst, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&c->h2d, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&c->ld2h, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&c->fst, cudaStreamNonBlocking) != cudaSuccess ||
         cudaEventCreateWithFlags(&c->ev_halo[0], cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&c->ev_halo[1], cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&c->ev_tile, cudaEventDisableTiming) != cudaSuccess ||
@@ -1388,6 +1397,17 @@ eg_status eg_compute_typed(eg_ctx *c, const eg_domain *d, const void *d_field, i
     return compute_impl(c, d, c->typed.as<float>(), flags, true);
 }
 
+static void tiled3d_fin_list_of(eg_ctx *c, const int32_t **list, const unsigned long long **n, int64_t *cap) {
+    tiled3d_fin_list(c->slabs[0]->tiled, list, n, cap);
+}
+
+static bool is_pinned(const void *p) {
+    cudaPointerAttributes a;
+    const bool ok = p && cudaPointerGetAttributes(&a, p) == cudaSuccess && a.type == cudaMemoryTypeHost;
+    cudaGetLastError();
+    return ok;
+}
+
 eg_status eg_compute_host(eg_ctx *c, const eg_domain *d, const float *h_field, int32_t *h_labels, uint32_t flags) {
     if (!c) return EG_ERR_INVALID_ARG;
     if (c->poisoned) return set_err(c, EG_ERR_STATE, "context is poisoned: %s", c->err.c_str());
@@ -1397,10 +1417,30 @@ eg_status eg_compute_host(eg_ctx *c, const eg_domain *d, const float *h_field, i
     CK(cudaSetDevice(c->device));
     const int64_t nfield = P.grid ? (P.v1 - P.v0) : P.N;
     CK(c->field.ensure(sizeof(float) * std::max<int64_t>(nfield, 1)));
-    cudaPointerAttributes a;
-    const bool pinned = cudaPointerGetAttributes(&a, h_field) == cudaSuccess && a.type == cudaMemoryTypeHost;
-    cudaGetLastError();
-    if (pinned || nfield * 4 <= (int64_t(1) << 20)) {
+    const bool pinned = is_pinned(h_field);
+    // the pipeline (one 3-D slab of whole tiles on one GPU, pinned host
+    // buffers, the plain maximum graph): the field arrives in z-chunks, each
+    // chunk's labels leave while later chunks arrive (ChunkIO, k_grid3d.cu);
+    // EG_E2E_CHUNKS = chunk count (1 = off)
+    const char *ek = std::getenv("EG_E2E_CHUNKS");
+    const int K = ek ? std::atoi(ek) : 16;
+    const bool pipe = K >= 2 && pinned && (!h_labels || is_pinned(h_labels)) && c->world == 1 && P.grid &&
+                      P.ndim == 3 && P.dims[0] % 32 == 0 && P.dims[1] % 16 == 0 && P.dims[2] % 16 == 0 &&
+                      !(flags & (EG_FORCE_GENERIC | EG_MINIMUM | EG_RAW_ARCS | EG_ARC_PATHS | EG_BUNDLE |
+                                 EG_NODE_VALUES)) &&
+                      ((flags >> 16) & 0xffff) <= 1;
+    ChunkIO io;
+    if (pipe) {
+        CK(cudaStreamSynchronize(c->stream));       // the previous call's uses of c->field are done
+        io.K = K;
+        io.h2d = c->h2d;
+        io.d2h = c->ld2h;
+        io.fst = c->fst;
+        io.h_field = h_field;
+        io.d_field = c->field.as<float>();
+        io.h_labels = h_labels;
+        c->io = &io;
+    } else if (pinned || nfield * 4 <= (int64_t(1) << 20)) {
         CK(cudaMemcpyAsync(c->field.p, h_field, sizeof(float) * nfield, cudaMemcpyHostToDevice, c->stream));
     } else {
         // pageable source: stage through two pinned halves
@@ -1422,10 +1462,47 @@ eg_status eg_compute_host(eg_ctx *c, const eg_domain *d, const float *h_field, i
             used[k] = true;
         }
     }
-    ST(compute_impl(c, d, c->field.as<float>(), flags, true));
+    const eg_status st = compute_impl(c, d, c->field.as<float>(), flags, true);
+    c->io = nullptr;
+    if (st != EG_OK) {
+        if (pipe) {
+            cudaStreamSynchronize(c->h2d);
+            cudaStreamSynchronize(c->fst);
+            cudaStreamSynchronize(c->ld2h);
+        }
+        return st;
+    }
     if (h_labels) {
-        CK(cudaMemcpyAsync(h_labels, c->d_labels, sizeof(int32_t) * c->n_own, cudaMemcpyDeviceToHost, c->stream));
-        CK(cudaStreamSynchronize(c->stream));
+        if (pipe && io.done) {
+            // the label chunks are on their way; the vertices the chunked pass
+            // finished last (after their chunk was copied) are patched
+            CK(cudaEventSynchronize(io.d2h_done));
+            const int32_t *d_list = nullptr;
+            const unsigned long long *d_n = nullptr;
+            int64_t cap = 0;
+            tiled3d_fin_list_of(c, &d_list, &d_n, &cap);
+            unsigned long long n = 0;
+            CK(cudaMemcpy(&n, d_n, sizeof(n), cudaMemcpyDeviceToHost));
+            c->stats.n_exit_targets = int64_t(n);       // (reported: labels patched on the host)
+            if (int64_t(n) > cap) {
+                CK(cudaMemcpy(h_labels, c->d_labels, sizeof(int32_t) * c->n_own, cudaMemcpyDeviceToHost));
+            } else if (n > 0) {
+                CK(c->fix_dev.ensure(sizeof(int32_t) * 2 * n));
+                int32_t *dv = c->fix_dev.as<int32_t>();
+                CK(launch_gather_labels(c->d_labels, d_list, int64_t(n), dv, c->stream));
+                CK(cudaMemcpyAsync(dv + n, d_list, sizeof(int32_t) * n, cudaMemcpyDeviceToDevice, c->stream));
+                std::vector<int32_t> hv(2 * n);
+                CK(cudaMemcpyAsync(hv.data(), dv, sizeof(int32_t) * 2 * n, cudaMemcpyDeviceToHost, c->stream));
+                CK(cudaStreamSynchronize(c->stream));
+                for (unsigned long long j = 0; j < n; ++j) h_labels[hv[n + j]] = hv[j];
+            }
+        } else {
+            CK(cudaMemcpyAsync(h_labels, c->d_labels, sizeof(int32_t) * c->n_own, cudaMemcpyDeviceToHost,
+                               c->stream));
+            CK(cudaStreamSynchronize(c->stream));
+        }
+    } else if (pipe) {
+        CK(cudaStreamSynchronize(c->ld2h));
     }
     return EG_OK;
 }
@@ -1539,7 +1616,7 @@ eg_status eg_destroy(eg_ctx *c) {
     cudaStreamSynchronize(c->stream);
     set_slab_count(c, 0);
     DevBuf *bufs[] = {&c->typed, &c->rank_scratch, &c->d_fnode, &c->bund_scratch, &c->b_sad64, &c->b_sad32, &c->b_sbeta, &c->b_nu, &c->b_arc_s, &c->b_arc_m,
-                      &c->b_arc_mult, &c->label_all, &c->csr_scratch, &c->stat_buf, &c->field, &c->mirror, &c->path_len, &c->path_off, &c->path_v, &c->flags, &c->counts, &c->scratch, &c->tab, &c->gsend, &c->grecv};
+                      &c->b_arc_mult, &c->label_all, &c->csr_scratch, &c->fix_dev, &c->stat_buf, &c->field, &c->mirror, &c->path_len, &c->path_off, &c->path_v, &c->flags, &c->counts, &c->scratch, &c->tab, &c->gsend, &c->grecv};
     for (DevBuf *b : bufs) b->release();
     HostBuf *hb[] = {&c->h_fmax, &c->h_fsad, &c->h_maxima, &c->h_saddles, &c->h_sbeta, &c->h_arc_s, &c->h_arc_m, &c->h_arc_mult,
                      &c->h_raw_s, &c->h_raw_rep, &c->h_raw_m, &c->h_counts, &c->h_stage, &c->h_path_off,
@@ -1555,10 +1632,11 @@ eg_status eg_destroy(eg_ctx *c) {
         cudaStreamSynchronize(c->d2h);
         cudaStreamDestroy(c->d2h);
     }
-    if (c->cst) {
-        cudaStreamSynchronize(c->cst);
-        cudaStreamDestroy(c->cst);
-    }
+    for (cudaStream_t *sp : {&c->cst, &c->h2d, &c->ld2h, &c->fst})
+        if (*sp) {
+            cudaStreamSynchronize(*sp);
+            cudaStreamDestroy(*sp);
+        }
     for (auto &e : c->ev_halo)
         if (e) cudaEventDestroy(e);
     if (c->aux) {

@@ -245,6 +245,18 @@ cudaError_t launch_bval_update(int32_t *bval, const int32_t *hval_lo, const int3
 // final pass: every unresolved owned label (all owned vertices, or only those
 // whose bit is set in `bits`) becomes final, via owned labels and the final
 // halo-plane values
+// the one-slab label pass in z-chunks (eg_compute_host pipeline, k_slab.cu):
+// words [w_begin, w_end) of the owned labels, chains followed only through
+// local indices < lim; unfinished vertices are appended to list (capacity
+// list_cap, count *list_n) for launch_finalize_list, which finishes them once
+// every vertex is labelled (or every label if the list overflowed)
+cudaError_t launch_finalize_chunk(int32_t *label, int64_t w_begin, int64_t w_end, int64_t n, int64_t v0, int64_t lim,
+                                  int32_t *list, unsigned long long *list_n, int64_t list_cap, cudaStream_t st,
+                                  unsigned long long *hist = nullptr);
+cudaError_t launch_finalize_list(int32_t *label, const int32_t *list, const unsigned long long *list_n,
+                                 int64_t list_cap, int64_t v0, int64_t n_all, cudaStream_t st,
+                                 unsigned long long *hist = nullptr);
+cudaError_t launch_gather_labels(const int32_t *label, const int32_t *list, int64_t n, int32_t *out, cudaStream_t st);
 cudaError_t launch_finalize(int32_t *label, const uint32_t *bits, int64_t v0, int64_t v1, const int32_t *hval_lo,
                             const int32_t *hval_hi, int64_t plane, cudaStream_t st, unsigned long long *hist = nullptr);
 }  // namespace eg

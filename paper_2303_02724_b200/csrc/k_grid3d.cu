@@ -34,6 +34,8 @@
 #include <cstring>
 #include <vector>
 
+#include <algorithm>
+
 #include "eg_tiled.h"
 
 namespace eg {
@@ -50,6 +52,7 @@ constexpr int kThreads = TX * TY;                    // one z-column per thread
 constexpr int kWarps = kThreads / 32;
 constexpr int kLutWords = (1 << 14) / 16;            // 2 bits per 14-bit upper mask: beta0+ >= 2, beta0+ == 0
 constexpr uint32_t kFlag = 0x80000000u;              // label bit 31: exit (not yet final)
+constexpr int kMaxChunks = 32;                       // z-chunks of the eg_compute_host pipeline
 #ifndef EG_S1_UNROLL
 #define EG_S1_UNROLL 4
 #endif
@@ -83,7 +86,7 @@ struct Tiled3D {
     int64_t n_btiles = 0;
     int32_t *d_elist = nullptr;                      // exit targets E
     int64_t ecap = 0;
-    unsigned long long *d_ecount = nullptr;          // [0] |E|, [1] maxima, [2] saddles
+    unsigned long long *d_ecount = nullptr;          // [0] |E|, [1] maxima, [2] saddles, [3] unfinished labels
     int32_t *d_max = nullptr, *d_sad = nullptr;      // unordered maxima / saddles of the last call
     int64_t list_cap = 0;
     int64_t n_max = 0, n_sad = 0, v0 = 0, v1 = 0;
@@ -93,7 +96,18 @@ struct Tiled3D {
     int64_t alt_cap = 0;
     void *encode = nullptr;                          // cuTensorMapEncodeTiled
     int n_sm = 148;
+    // eg_compute_host pipeline: events per chunk (H2D, tile, label), the
+    // list of vertices a label chunk could not finish
+    cudaEvent_t ev_io[3 * kMaxChunks + 2] = {};
+    int32_t *d_fin_list = nullptr;
+    int64_t fin_cap = 0;
 };
+
+void tiled3d_fin_list(const Tiled3D *t, const int32_t **list, const unsigned long long **count, int64_t *cap) {
+    *list = t->d_fin_list;
+    *count = t->d_ecount + 3;
+    *cap = t->fin_cap;
+}
 
 Tiled3D *tiled3d_create() { return new Tiled3D(); }
 
@@ -109,6 +123,9 @@ void tiled3d_destroy(Tiled3D *t) {
     if (t->d_sad) cudaFree(t->d_sad);
     if (t->d_sort_tmp) cudaFree(t->d_sort_tmp);
     if (t->d_alt) cudaFree(t->d_alt);
+    if (t->d_fin_list) cudaFree(t->d_fin_list);
+    for (auto &e : t->ev_io)
+        if (e) cudaEventDestroy(e);
     delete t;
 }
 
@@ -665,9 +682,102 @@ static cudaError_t upload(T **d, const std::vector<T> &h) {
     return cudaMemcpy(*d, h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice);
 }
 
+// eg_compute_host pipeline (see ChunkIO): H2D chunk k on io->h2d; tile chunk k
+// on st after H2D chunk k + 1 (its top halo plane); label chunk k - 1 on
+// io->fst after tile chunk k, following chains only through labelled vertices
+// (those ending beyond go to the fix-up list); its labels to the host on
+// io->d2h.  After the last chunk the fix-up list is finished on the device;
+// the caller patches those labels on the host.
+static eg_status pipeline_chunks(Tiled3D *t, const TileArgs &A, const CUtensorMap &tmap, const Dims3 &D, int3 hi,
+                                 int3 lo, int32_t *labels, const Slab &s, int64_t nown, int64_t nxy, cudaStream_t st,
+                                 ChunkIO *io, eg_stats *stats, std::string *err) {
+    cudaError_t e;
+    const int layers = hi.z - lo.z + 1;
+    const int K = std::max(1, std::min({io->K, kMaxChunks, layers}));
+    const int64_t cap = std::max<int64_t>(nown / 16, 4096);
+    if (t->fin_cap < cap) {
+        if (t->d_fin_list) cudaFree(t->d_fin_list);
+        t->d_fin_list = nullptr;
+        t->fin_cap = 0;
+        if ((e = cudaMalloc(&t->d_fin_list, cap * 4)) != cudaSuccess) return fail(err, e, "cudaMalloc fix-up list");
+        t->fin_cap = cap;
+    }
+    auto first_layer = [&](int k) { return lo.z + int(int64_t(layers) * k / K); };
+    auto vend = [&](int k) -> int64_t {       // local index where chunk k ends
+        return k < 0 ? 0 : std::min<int64_t>(int64_t(first_layer(k + 1) - lo.z) * TZ * nxy, nown);
+    };
+    cudaEvent_t *evH = t->ev_io, *evT = t->ev_io + kMaxChunks, *evL = t->ev_io + 2 * kMaxChunks;
+    cudaEvent_t *evS = t->ev_io + 3 * kMaxChunks;
+    if ((e = cudaEventRecord(evS[0], st)) != cudaSuccess || (e = cudaStreamWaitEvent(io->h2d, evS[0], 0)) != cudaSuccess)
+        return fail(err, e, "pipeline start");
+    // H2D chunk k also carries the first plane of chunk k + 1 (tile chunk k's
+    // top halo), so tile chunk k waits for H2D chunk k only
+    const int64_t plane = nxy;
+    for (int k = 0; k < K; ++k) {
+        const int64_t a = k == 0 ? 0 : vend(k - 1) + plane, b = std::min(vend(k) + plane, nown);
+        if ((e = cudaMemcpyAsync(io->d_field + a, io->h_field + a, sizeof(float) * size_t(b - a),
+                                 cudaMemcpyHostToDevice, io->h2d)) != cudaSuccess ||
+            (e = cudaEventRecord(evH[k], io->h2d)) != cudaSuccess)
+            return fail(err, e, "H2D chunk");
+    }
+    auto label_chunk = [&](int k, int64_t lim) -> eg_status {
+        if ((e = launch_finalize_chunk(labels, vend(k - 1) / 32, (vend(k) + 31) / 32, nown, s.v0, lim,
+                                       t->d_fin_list, t->d_ecount + 3, t->fin_cap, io->fst)) != cudaSuccess)
+            return fail(err, e, "k_finalize_chunk");
+        stats->kernel_launches += 1;
+        return EG_OK;
+    };
+    auto labels_out = [&](int k) -> eg_status {
+        if (!io->h_labels) return EG_OK;
+        const int64_t a = vend(k - 1), b = vend(k);
+        if ((e = cudaStreamWaitEvent(io->d2h, evL[k], 0)) != cudaSuccess ||
+            (e = cudaMemcpyAsync(io->h_labels + a, labels + a, sizeof(int32_t) * size_t(b - a),
+                                 cudaMemcpyDeviceToHost, io->d2h)) != cudaSuccess)
+            return fail(err, e, "D2H labels chunk");
+        return EG_OK;
+    };
+    for (int k = 0; k < K; ++k) {
+        TileArgs Ak = A;
+        const int l0 = first_layer(k), l1 = first_layer(k + 1);
+        Ak.origin.z = l0;
+        Ak.n_tiles = int32_t(int64_t(A.tiles_x) * A.tiles_y * (l1 - l0));
+        if ((e = cudaStreamWaitEvent(st, evH[k], 0)) != cudaSuccess) return fail(err, e, "H2D wait");
+        k_tile<true, false><<<unsigned(Ak.n_tiles), kThreads, kTileSmem, st>>>(tmap, Ak, D);
+        stats->kernel_launches += 1;
+        if ((e = cudaGetLastError()) != cudaSuccess) return fail(err, e, "k_tile<interior> chunk");
+        if ((e = cudaEventRecord(evT[k], st)) != cudaSuccess) return fail(err, e, "tile chunk event");
+        if (k >= 1) {
+            // chunk k - 1: its chains may run through every chunk <= k
+            if ((e = cudaStreamWaitEvent(io->fst, evT[k], 0)) != cudaSuccess) return fail(err, e, "tile wait");
+            const eg_status ls = label_chunk(k - 1, k == K - 1 ? nown : vend(k));
+            if (ls != EG_OK) return ls;
+            if ((e = cudaEventRecord(evL[k - 1], io->fst)) != cudaSuccess) return fail(err, e, "label event");
+            const eg_status os = labels_out(k - 1);
+            if (os != EG_OK) return os;
+        }
+    }
+    if (K == 1 && (e = cudaStreamWaitEvent(io->fst, evT[0], 0)) != cudaSuccess) return fail(err, e, "tile wait");
+    const eg_status ls = label_chunk(K - 1, nown);
+    if (ls != EG_OK) return ls;
+    if ((e = launch_finalize_list(labels, t->d_fin_list, t->d_ecount + 3, t->fin_cap, s.v0, nown, io->fst)) !=
+            cudaSuccess ||
+        (e = cudaEventRecord(evL[K - 1], io->fst)) != cudaSuccess)
+        return fail(err, e, "k_finalize_list");
+    stats->kernel_launches += 1;
+    const eg_status os = labels_out(K - 1);
+    if (os != EG_OK) return os;
+    if ((e = cudaEventRecord(evS[1], io->d2h)) != cudaSuccess) return fail(err, e, "D2H event");
+    io->fin_done = evL[K - 1];
+    io->d2h_done = evS[1];
+    io->done = true;
+    return EG_OK;
+}
+
 eg_status tiled3d_local(Tiled3D *t, int ndim, const int64_t *dims, const Slab &s, const FieldView &F, int32_t *labels,
                         int *flags, cudaStream_t st, eg_stats *stats, std::string *err, cudaEvent_t ev_main0,
-                        cudaEvent_t ev_main1, unsigned long long *exit_count, cudaEvent_t halo_ready) {
+                        cudaEvent_t ev_main1, unsigned long long *exit_count, cudaEvent_t halo_ready,
+                        ChunkIO *io) {
+    if (io) io->done = false;
     int64_t d3[3] = {1, 1, 1};
     for (int i = 0; i < ndim; ++i) d3[i] = dims[i];
     cudaError_t e;
@@ -695,8 +805,11 @@ eg_status tiled3d_local(Tiled3D *t, int ndim, const int64_t *dims, const Slab &s
             return EG_ERR_STATE;
         }
         if ((e = upload(&t->d_shell, sh)) != cudaSuccess) return fail(err, e, "shell upload");
-        if ((e = cudaMalloc(&t->d_ecount, 3 * sizeof(unsigned long long))) != cudaSuccess)
+        if ((e = cudaMalloc(&t->d_ecount, 4 * sizeof(unsigned long long))) != cudaSuccess)
             return fail(err, e, "cudaMalloc ecount");
+        for (auto &ev : t->ev_io)
+            if ((e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming)) != cudaSuccess)
+                return fail(err, e, "pipeline events");
         if ((e = cudaFuncSetAttribute(k_tile<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       int(kTileSmem))) != cudaSuccess ||
             (e = cudaFuncSetAttribute(k_tile<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -812,7 +925,7 @@ eg_status tiled3d_local(Tiled3D *t, int ndim, const int64_t *dims, const Slab &s
     }
     stats->path = 1;
     for (int attempt = 0;; ++attempt) {
-        if ((e = cudaMemsetAsync(t->d_ecount, 0, 3 * sizeof(unsigned long long), st)) != cudaSuccess)
+        if ((e = cudaMemsetAsync(t->d_ecount, 0, 4 * sizeof(unsigned long long), st)) != cudaSuccess)
             return fail(err, e, "memset counts");
         TileArgs A{};
         A.f = F.own;
@@ -845,6 +958,17 @@ eg_status tiled3d_local(Tiled3D *t, int ndim, const int64_t *dims, const Slab &s
         A.no_elist = (el && el[0] == '1') ? 0 : 1;
         A.tma = tma ? 1 : 0;
         if (ev_main0) cudaEventRecord(ev_main0, st);
+        // eg_compute_host pipeline: every tile interior, no exit list, TMA
+        const char *pe = std::getenv("EG_PERSIST");
+        const bool persist_req = pe && pe[0] == '1';
+        const bool chunk = io && io->h_field && A.no_elist && A.tma && !persist_req && t->n_btiles == 0 &&
+                           have_interior && attempt == 0;
+        if (io && io->h_field && !chunk && attempt == 0) {
+            // not chunkable: the whole field first
+            if ((e = cudaMemcpyAsync(io->d_field, io->h_field, sizeof(float) * size_t(nown), cudaMemcpyHostToDevice,
+                                     st)) != cudaSuccess)
+                return fail(err, e, "H2D field");
+        }
         // halo_ready (several GPUs): the neighbour slabs' halo planes arrive on
         // another stream while the interior tiles (which never read them) run;
         // the boundary tiles are launched after them
@@ -874,9 +998,12 @@ eg_status tiled3d_local(Tiled3D *t, int ndim, const int64_t *dims, const Slab &s
             A.n_tiles = int32_t(nt);
             // persistent CTAs (2 per SM) on the one-slab TMA path: measured slower
             // on C3 (6.27 vs 5.65 ms), so only on request (EG_PERSIST=1)
-            const char *pe = std::getenv("EG_PERSIST");
-            const bool persist = A.no_elist && A.tma && (pe && pe[0] == '1') && nt > 2 * t->n_sm;
-            if (persist)
+            const bool persist = A.no_elist && A.tma && persist_req && nt > 2 * t->n_sm;
+            if (chunk) {
+                const eg_status cs = pipeline_chunks(t, A, tmap, D, hi, lo, labels, s, nown, int64_t(d3[0]) * d3[1],
+                                                     st, io, stats, err);
+                if (cs != EG_OK) return cs;
+            } else if (persist)
                 k_tile<true, true><<<unsigned(2 * t->n_sm), kThreads, kTileSmem, st>>>(tmap, A, D);
             else if (A.exit_count)
                 k_tile<true, false, true><<<unsigned(nt), kThreads, kTileSmem, st>>>(tmap, A, D);
@@ -904,6 +1031,14 @@ eg_status tiled3d_local(Tiled3D *t, int ndim, const int64_t *dims, const Slab &s
             // more critical points than the lists hold: grow them, run again
             const int64_t cap = std::max<int64_t>(int64_t(std::max(cnt[1], cnt[2])) * 5 / 4, t->list_cap);
             if ((e = grow_lists(t, cap)) != cudaSuccess) return fail(err, e, "cudaMalloc lists");
+            if (io && io->done) {
+                // the pipeline's label chunks ran on this pass's labels: let them
+                // finish; the rerun is unchunked (the field is on the device now)
+                if ((e = cudaStreamSynchronize(io->fst)) != cudaSuccess ||
+                    (e = cudaStreamSynchronize(io->d2h)) != cudaSuccess)
+                    return fail(err, e, "pipeline streams");
+                io->done = false;
+            }
             continue;
         }
         stats->n_exit_targets += int64_t(cnt[0]);

@@ -191,6 +191,152 @@ __global__ void __launch_bounds__(128, 16) k_finalize(int32_t *label, const uint
         if (need[k]) label[(w0 + k) * 32 + lane] = e[k];
 }
 
+// The one-slab label pass in z-chunks, for the end-to-end pipeline of
+// eg_compute_host (k_grid3d.cu, tiled3d_local): chunk k of the owned words
+// is finalised as soon as the tile kernel has labelled chunk k + 1, so its
+// labels can travel to the host while later chunks of the field are still
+// arriving.  A chain is followed only through vertices the tile kernel has
+// labelled (local index < lim); one that reaches beyond keeps its progress
+// (kFlag | the vertex it stopped at) and its index is appended to `list` for
+// k_finalize_list, which runs once every chunk is labelled.
+template <bool kStats>
+__global__ void __launch_bounds__(128, 16) k_finalize_chunk(int32_t *label, int64_t w_begin, int64_t w_end, int64_t n,
+                                                        int64_t v0, int64_t lim, int32_t *list,
+                                                        unsigned long long *list_n, int64_t list_cap,
+                                                        unsigned long long *hist) {
+    const int64_t w0 = w_begin + (int64_t(blockIdx.x) * (blockDim.x / 32) + (threadIdx.x >> 5)) * kW;
+    if (w0 >= w_end) return;
+    const int lane = threadIdx.x & 31;
+    bool need[kW];
+    int32_t e[kW];
+#pragma unroll
+    for (int k = 0; k < kW; ++k) {
+        const int64_t i = (w0 + k) * 32 + lane;
+        need[k] = w0 + k < w_end && i < n;
+    }
+#pragma unroll
+    for (int k = 0; k < kW; ++k) e[k] = need[k] ? label[(w0 + k) * 32 + lane] : 0;
+#pragma unroll
+    for (int k = 0; k < kW; ++k) need[k] = need[k] && e[k] < 0;
+    int hops[kW];
+    bool unres[kW];
+    // the first hop of every word's chains first (independent loads in flight)
+#pragma unroll
+    for (int k = 0; k < kW; ++k) {
+        hops[k] = 0;
+        unres[k] = false;
+        if (need[k]) {
+            const int64_t x = int64_t(e[k] & 0x7fffffff) - v0;
+            if (x >= lim) unres[k] = true;              // not labelled by the tile kernel yet
+            else {
+                e[k] = label[x];
+                hops[k] = 1;
+            }
+        }
+    }
+#pragma unroll
+    for (int k = 0; k < kW; ++k) {
+        if (need[k] && !unres[k] && e[k] < 0) {
+            int32_t w = e[k];
+            do {
+                const int64_t x = int64_t(w & 0x7fffffff) - v0;
+                if (x >= lim) {
+                    unres[k] = true;
+                    break;
+                }
+                w = __ldca(label + x);        // race-benign as in k_finalize
+                if (kStats) ++hops[k];
+            } while (w < 0);
+            e[k] = w;
+        }
+    }
+#pragma unroll
+    for (int k = 0; k < kW; ++k)
+        if (need[k]) label[(w0 + k) * 32 + lane] = e[k];
+#pragma unroll
+    for (int k = 0; k < kW; ++k) {
+        const uint32_t b = __ballot_sync(0xffffffffu, unres[k]);
+        if (b) {
+            unsigned long long base = 0;
+            if (lane == 0) base = atomicAdd(list_n, (unsigned long long)__popc(b));
+            base = __shfl_sync(0xffffffffu, base, 0);
+            const unsigned long long j = base + __popc(b & ((1u << lane) - 1u));
+            if (unres[k] && j < (unsigned long long)list_cap) list[j] = int32_t((w0 + k) * 32 + lane);
+        }
+    }
+    if (kStats) {
+        int mx = 0;
+#pragma unroll
+        for (int k = 0; k < kW; ++k) {
+            if (need[k] && !unres[k]) atomicAdd(hist + min(hops[k], 15), 1ull);
+            mx = max(mx, hops[k]);
+        }
+        mx = __reduce_max_sync(0xffffffffu, unsigned(mx));
+        if (lane == 0 && mx) atomicMax(hist + 16, (unsigned long long)mx);
+    }
+}
+
+// the vertices a chunk could not finish (every vertex is labelled by now); if
+// the list overflowed, every owned label is checked instead (exact, slower)
+template <bool kStats>
+__global__ void __launch_bounds__(128) k_finalize_list(int32_t *label, const int32_t *__restrict__ list,
+                                                       const unsigned long long *list_n, int64_t list_cap, int64_t v0,
+                                                       int64_t n_all, unsigned long long *hist) {
+    const int64_t nl = int64_t(*list_n);
+    const bool all = nl > list_cap;
+    const int64_t n = all ? n_all : nl;
+    for (int64_t j = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; j < n; j += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t i = all ? j : list[j];
+        int32_t w = label[i];
+        int h = 0;
+        while (w < 0) {
+            w = __ldca(label + (int64_t(w & 0x7fffffff) - v0));
+            ++h;
+        }
+        if (h) label[i] = w;
+        if (kStats && h) atomicAdd(hist + min(h, 15), 1ull);   // hops after the chunk stopped
+    }
+}
+
+__global__ void k_gather_labels(const int32_t *__restrict__ label, const int32_t *__restrict__ list, int64_t n,
+                                int32_t *out) {
+    const int64_t j = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (j < n) out[j] = label[list[j]];
+}
+
+cudaError_t launch_finalize_chunk(int32_t *label, int64_t w_begin, int64_t w_end, int64_t n, int64_t v0, int64_t lim,
+                                  int32_t *list, unsigned long long *list_n, int64_t list_cap, cudaStream_t st,
+                                  unsigned long long *hist) {
+    if (w_end <= w_begin) return cudaSuccess;
+    const unsigned blocks = blocks_for(w_end - w_begin, 4 * kW);
+    if (hist)
+        k_finalize_chunk<true><<<blocks, 128, 0, st>>>(label, w_begin, w_end, n, v0, lim, list, list_n, list_cap,
+                                                        hist);
+    else
+        k_finalize_chunk<false><<<blocks, 128, 0, st>>>(label, w_begin, w_end, n, v0, lim, list, list_n, list_cap,
+                                                         nullptr);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_finalize_list(int32_t *label, const int32_t *list, const unsigned long long *list_n,
+                                 int64_t list_cap, int64_t v0, int64_t n_all, cudaStream_t st,
+                                 unsigned long long *hist) {
+    if (n_all <= 0) return cudaSuccess;
+    const unsigned blocks = 148 * 16;
+    if (hist)
+        k_finalize_list<true><<<blocks, 128, 0, st>>>(label, list, list_n, list_cap, v0, n_all, hist);
+    else
+        k_finalize_list<false><<<blocks, 128, 0, st>>>(label, list, list_n, list_cap, v0, n_all, nullptr);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_gather_labels(const int32_t *label, const int32_t *list, int64_t n, int32_t *out,
+                                 cudaStream_t st) {
+    if (n <= 0) return cudaSuccess;
+    k_gather_labels<<<blocks_for(n, 256), 256, 0, st>>>(label, list, n, out);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_finalize(int32_t *label, const uint32_t *bits, int64_t v0, int64_t v1, const int32_t *hval_lo,
                             const int32_t *hval_hi, int64_t plane, cudaStream_t st, unsigned long long *hist) {
     const int64_t words = (v1 - v0 + 31) / 32;

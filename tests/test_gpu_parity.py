@@ -290,6 +290,32 @@ def test_compute_host_e2e(eg, ctx):
     assert_graph_equal(g2, o)
 
 
+@pytest.mark.parametrize("chunks", ["2", "5", "16", "32", "1"])
+def test_compute_host_pipeline(eg, ctx, chunks, monkeypatch):
+    """eg_compute_host's pipeline (field in z-chunks, each chunk's labels
+    copied while later chunks arrive, late-finished labels patched on the
+    host): a smooth field whose chains cross several chunks, any chunk count;
+    labels bit-exact, also with a pageable label buffer (no pipeline) and
+    after a device-resident compute."""
+    import torch
+    monkeypatch.setenv("EG_E2E_CHUNKS", chunks)
+    t, dims = G.turbulence(64, seed=5, device="cpu", kc_div=4)
+    f = np.ascontiguousarray(np.tile(t.numpy().reshape(64, 64, 64), (4, 1, 1)).reshape(-1))   # 64 x 64 x 256
+    dims = [64, 64, 256]
+    o = O.grid(f, dims)
+    host = torch.from_numpy(f).pin_memory()
+    for _ in range(2):
+        lab = torch.full((len(f),), -7, dtype=torch.int32).pin_memory()
+        g = ctx.compute_host(host, dims=dims, labels_out=lab, flags=eg.EG_CHECK_NAN)
+        assert_graph_equal(g, o, what=f"pipeline {chunks}")
+        assert first_diff(lab.numpy().astype(np.int64), o.label) is None
+    lab2 = torch.zeros(len(f), dtype=torch.int32)                 # pageable: plain path
+    ctx.compute_host(host, dims=dims, labels_out=lab2)
+    assert np.array_equal(lab2.numpy().astype(np.int64), o.label)
+    g3 = ctx.compute(host.cuda(), dims=dims)
+    assert_graph_equal(g3, o, what="device compute after the pipeline")
+
+
 @pytest.mark.parametrize("dims,kind", [([70, 9, 40], "signed_zero"), ([33, 35, 19], "int"), ([96, 64, 48], "int")])
 def test_tie_heavy_repeated(eg, ctx, dims, kind):
     # in-place races in the shared-memory chase / exit resolution must never
