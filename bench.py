@@ -244,7 +244,8 @@ def run_ours(args):
         scaling, parallelism = "weak", "replicas"        # too few planes to cut: independent replicas
     if world == 1:
         scaling, parallelism = "strong", "single"
-    flags = eg.EG_CHECK_NAN
+    # the graph crosses to the host with 32-bit ids (12 B per arc; every id < 2^31)
+    flags = eg.EG_CHECK_NAN | eg.EG_GRAPH32
     if os.environ.get("EG_BENCH_VPARTS"):          # experiments: k virtual slabs on one GPU
         flags |= eg.EG_VIRTUAL_PARTS(int(os.environ["EG_BENCH_VPARTS"]))
     fallback = None
@@ -324,7 +325,7 @@ def run_ours(args):
         ems = torch.tensor([e0.elapsed_time(e1)], device=dev)
         if world > 1:
             dist.all_reduce(ems, op=dist.ReduceOp.MAX)
-        graph_bytes = 8 * len(ge.maxima) + 12 * len(ge.saddles) + 20 * len(ge.arcs)
+        graph_bytes = 4 * len(ge.maxima) + 8 * len(ge.saddles) + 12 * len(ge.arcs)     # EG_GRAPH32
         e2e = {"value": round(units * e_steps / (float(ems.item()) / 1e3) / 1e6, 2), "unit": "Mvertices/s",
                "h2d_bytes_per_step": int(4 * hf.numel()), "d2h_bytes_per_step": int(4 * n_lab + graph_bytes),
                "steps": e_steps,

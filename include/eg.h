@@ -147,7 +147,13 @@ enum {
     EG_NODE_VALUES = 256u,
     /* collect the S2 statistics of eg_stats (exit counts, chase histogram);
      * costs a few instructions per vertex, so it is off in timed runs */
-    EG_STATS = 1024u
+    EG_STATS = 1024u,
+    /* copy the graph to the host as 32-bit ids (12 B per arc instead of 20;
+     * N < 2^31 always holds): read it with eg_get_graph32; eg_get_graph then
+     * widens it on the host on first use.  One process, plain maximum graph
+     * (with EG_BUNDLE / EG_MINIMUM / EG_NODE_VALUES or several ranks the graph
+     * is copied as 64-bit ids and eg_get_graph32 narrows it on the host). */
+    EG_GRAPH32 = 2048u
 };
 /* virtual partitions: process a grid as k slabs on one GPU, exchanging
  * boundaries by device copies exactly as k ranks would (partition test). */
@@ -201,6 +207,19 @@ eg_status eg_gradient(eg_ctx *ctx, const eg_domain *domain, const float *d_field
                       uint8_t *d_beta);
 
 eg_status eg_get_graph(eg_ctx *ctx, eg_graph *out);
+
+/* The same graph with 32-bit ids (see EG_GRAPH32); host pointers owned by the
+ * ctx, valid until the next compute / destroy. */
+typedef struct {
+    int64_t n_max, n_saddle, n_arc;
+    const int32_t *maxima;
+    const int32_t *saddles;
+    const int32_t *saddle_beta;
+    const int32_t *arc_saddle;
+    const int32_t *arc_max;
+    const int32_t *arc_mult;
+} eg_graph32;
+eg_status eg_get_graph32(eg_ctx *ctx, eg_graph32 *out);
 /* raw arcs (EG_RAW_ARCS): one (s, rep, m) per upper-link component, ordered by
  * (s, rep); host pointers owned by the ctx; this rank's saddles only. */
 eg_status eg_get_raw_arcs(eg_ctx *ctx, int64_t *n, const int64_t **s, const int64_t **rep, const int64_t **m);

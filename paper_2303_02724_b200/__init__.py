@@ -20,12 +20,12 @@ import torch
 
 from . import _abi
 from ._abi import (EG_ARC_PATHS, EG_BUNDLE, EG_NODE_VALUES, EG_CHECK_CSR, EG_CHECK_NAN, EG_FORCE_GENERIC, EG_MINIMUM, EG_NO_GRAPH_D2H,
-                   EG_RAW_ARCS, EG_STATS,  # noqa: F401
+                   EG_RAW_ARCS, EG_STATS, EG_GRAPH32,  # noqa: F401
                    EG_VIRTUAL_PARTS)
 
 __all__ = ["Context", "Graph", "EgError", "grid_domain", "csr_domain", "EG_CHECK_NAN", "EG_RAW_ARCS",
            "EG_CHECK_CSR", "EG_FORCE_GENERIC", "EG_NO_GRAPH_D2H", "EG_MINIMUM", "EG_ARC_PATHS", "EG_BUNDLE", "EG_NODE_VALUES",
-           "EG_STATS", "EG_VIRTUAL_PARTS"]
+           "EG_STATS", "EG_GRAPH32", "EG_VIRTUAL_PARTS"]
 
 
 class EgError(RuntimeError):
@@ -206,8 +206,12 @@ class Context:
         if flags & _abi.EG_NO_GRAPH_D2H:
             return Graph(np.zeros(0, np.int64), np.zeros(0, np.int64), np.zeros(0, np.int32),
                          np.zeros((0, 3), np.int64), self.labels().clone())
-        g = _abi.EgGraph()
-        self._check(_abi.lib().eg_get_graph(self._h, C.byref(g)), "eg_get_graph")
+        if flags & _abi.EG_GRAPH32:      # 32-bit ids on the host (widened here, outside the library)
+            g = _abi.EgGraph32()
+            self._check(_abi.lib().eg_get_graph32(self._h, C.byref(g)), "eg_get_graph32")
+        else:
+            g = _abi.EgGraph()
+            self._check(_abi.lib().eg_get_graph(self._h, C.byref(g)), "eg_get_graph")
         arcs = np.stack([_arr(g.arc_saddle, g.n_arc, np.int64), _arr(g.arc_max, g.n_arc, np.int64),
                          _arr(g.arc_mult, g.n_arc, np.int64)], axis=1) if g.n_arc else np.zeros((0, 3), np.int64)
         raw = None

@@ -19,7 +19,7 @@ EG_DOMAIN_GRID, EG_DOMAIN_CSR = 0, 1
 (EG_DTYPE_F32, EG_DTYPE_F16, EG_DTYPE_BF16, EG_DTYPE_U8, EG_DTYPE_I8, EG_DTYPE_U16, EG_DTYPE_I16, EG_DTYPE_F64,
  EG_DTYPE_I32, EG_DTYPE_U32, EG_DTYPE_I64, EG_DTYPE_U64) = range(12)
 (EG_CHECK_NAN, EG_RAW_ARCS, EG_CHECK_CSR, EG_FORCE_GENERIC, EG_NO_GRAPH_D2H, EG_MINIMUM, EG_ARC_PATHS,
- EG_BUNDLE, EG_NODE_VALUES, EG_STATS) = 1, 2, 4, 8, 16, 32, 64, 128, 256, 1024
+ EG_BUNDLE, EG_NODE_VALUES, EG_STATS, EG_GRAPH32) = 1, 2, 4, 8, 16, 32, 64, 128, 256, 1024, 2048
 
 
 def EG_VIRTUAL_PARTS(k: int) -> int:
@@ -31,7 +31,7 @@ def EG_VIRTUAL_PARTS(k: int) -> int:
 
 # every symbol include/eg.h declares (checked by tests/test_abi_exports.py)
 EXPORTS = ["eg_create", "eg_nccl_unique_id", "eg_create_dist", "eg_compute", "eg_compute_host", "eg_gradient",
-           "eg_compute_typed", "eg_get_graph", "eg_get_raw_arcs", "eg_get_arc_paths", "eg_simplify", "eg_get_labels", "eg_get_stats",
+           "eg_compute_typed", "eg_get_graph", "eg_get_graph32", "eg_get_raw_arcs", "eg_get_arc_paths", "eg_simplify", "eg_get_labels", "eg_get_stats",
            "eg_destroy", "eg_last_error"]
 
 
@@ -53,6 +53,13 @@ class EgGraph(C.Structure):
                 ("maxima", C.POINTER(C.c_int64)), ("saddles", C.POINTER(C.c_int64)),
                 ("saddle_beta", C.POINTER(C.c_int32)), ("arc_saddle", C.POINTER(C.c_int64)),
                 ("arc_max", C.POINTER(C.c_int64)), ("arc_mult", C.POINTER(C.c_int32))]
+
+
+class EgGraph32(C.Structure):
+    _fields_ = [("n_max", C.c_int64), ("n_saddle", C.c_int64), ("n_arc", C.c_int64),
+                ("maxima", C.POINTER(C.c_int32)), ("saddles", C.POINTER(C.c_int32)),
+                ("saddle_beta", C.POINTER(C.c_int32)), ("arc_saddle", C.POINTER(C.c_int32)),
+                ("arc_max", C.POINTER(C.c_int32)), ("arc_mult", C.POINTER(C.c_int32))]
 
 
 class EgStats(C.Structure):
@@ -86,6 +93,7 @@ def lib():
     L.eg_compute_typed.argtypes = [vp, C.POINTER(EgDomain), vp, C.c_int, u32]
     L.eg_gradient.argtypes = [vp, C.POINTER(EgDomain), vp, vp, vp]
     L.eg_get_graph.argtypes = [vp, C.POINTER(EgGraph)]
+    L.eg_get_graph32.argtypes = [vp, C.POINTER(EgGraph32)]
     P64 = C.POINTER(C.c_int64)
     L.eg_get_raw_arcs.argtypes = [vp, P64, C.POINTER(P64), C.POINTER(P64), C.POINTER(P64)]
     L.eg_get_labels.argtypes = [vp, C.POINTER(vp), P64]

@@ -84,11 +84,12 @@ struct SlabState {
     bool tiled_lists = false;          // maxima / saddles come from the tiled path's lists
     DevBuf maxima64, saddles32, saddles64, sbeta, slot_off, tmp_m, tmp_mult, n_unique, arc_off;
     DevBuf arc_s, arc_m, arc_mult, raw_s, raw_rep, raw_m;
+    DevBuf maxima32, arc_s32, arc_m32;  // EG_GRAPH32 device copies
     int64_t n_max = 0, n_sad = 0, n_arc = 0, n_raw = 0;
     ~SlabState() {
         DevBuf *b[] = {&f_lo, &f_hi, &sad_bits, &max_bits, &beta8, &rep_buf, &bval, &hval_lo, &hval_hi, &maxima64,
                        &saddles32, &saddles64, &sbeta, &slot_off, &tmp_m, &tmp_mult, &n_unique, &arc_off, &arc_s,
-                       &arc_m, &arc_mult, &raw_s, &raw_rep, &raw_m};
+                       &arc_m, &arc_mult, &raw_s, &raw_rep, &raw_m, &maxima32, &arc_s32, &arc_m32};
         for (DevBuf *x : b) x->release();
         tiled3d_destroy(tiled);
     }
@@ -126,6 +127,9 @@ struct eg_ctx {
     bool tab_valid = false;
 
     HostBuf h_maxima, h_saddles, h_sbeta, h_arc_s, h_arc_m, h_arc_mult, h_raw_s, h_raw_rep, h_raw_m, h_counts;
+    HostBuf h32_maxima, h32_saddles, h32_arc_s, h32_arc_m;   // EG_GRAPH32 (sbeta / mult are int32 anyway)
+    bool g32 = false;                  // the graph on the host is in the h32_* buffers (+ h_sbeta, h_arc_mult)
+    bool h64_valid = false, h32_valid = false;   // which id width of the host graph is materialised
     HostBuf h_stage;
     HostBuf h_path_off, h_path_v;      // EG_ARC_PATHS
     HostBuf h_fmax, h_fsad;            // EG_NODE_VALUES: f at the maxima / saddles
@@ -439,10 +443,25 @@ static eg_status grid_graph(eg_ctx *c, const Problem &P, SlabState &S, bool raw,
         CK(c->h_sbeta.ensure(sizeof(int32_t) * std::max<int64_t>(ns, 1)));
         CK(cudaEventRecord(c->ev_d2h[0], c->gstream));
         CK(cudaStreamWaitEvent(c->d2h, c->ev_d2h[0], 0));
-        if (S.n_max)
-            CK(cudaMemcpyAsync(c->h_maxima.p, S.maxima64.p, sizeof(int64_t) * S.n_max, cudaMemcpyDeviceToHost, c->d2h));
-        if (ns)
-            CK(cudaMemcpyAsync(c->h_saddles.p, S.saddles64.p, sizeof(int64_t) * ns, cudaMemcpyDeviceToHost, c->d2h));
+        if (c->g32) {
+            CK(c->h32_maxima.ensure(sizeof(int32_t) * std::max<int64_t>(S.n_max, 1)));
+            CK(c->h32_saddles.ensure(sizeof(int32_t) * std::max<int64_t>(ns, 1)));
+            CK(S.maxima32.ensure(sizeof(int32_t) * std::max<int64_t>(S.n_max, 1)));
+            CK(launch_narrow(S.maxima64.as<int64_t>(), S.maxima32.as<int32_t>(), S.n_max, c->d2h));
+            if (S.n_max)
+                CK(cudaMemcpyAsync(c->h32_maxima.p, S.maxima32.p, sizeof(int32_t) * S.n_max, cudaMemcpyDeviceToHost,
+                                   c->d2h));
+            if (ns)
+                CK(cudaMemcpyAsync(c->h32_saddles.p, S.saddles32.p, sizeof(int32_t) * ns, cudaMemcpyDeviceToHost,
+                                   c->d2h));
+        } else {
+            if (S.n_max)
+                CK(cudaMemcpyAsync(c->h_maxima.p, S.maxima64.p, sizeof(int64_t) * S.n_max, cudaMemcpyDeviceToHost,
+                                   c->d2h));
+            if (ns)
+                CK(cudaMemcpyAsync(c->h_saddles.p, S.saddles64.p, sizeof(int64_t) * ns, cudaMemcpyDeviceToHost,
+                                   c->d2h));
+        }
     }
 
     // beta0+ per saddle and slot offsets (sum beta0+ = raw arcs)
@@ -584,7 +603,44 @@ static eg_status gather_graph(eg_ctx *c, bool raw) {
     CK(c->h_arc_m.ensure(sizeof(int64_t) * std::max<int64_t>(na, 1)));
     CK(c->h_arc_mult.ensure(sizeof(int32_t) * std::max<int64_t>(na, 1)));
     cudaStream_t st = c->gstream;
-    if (c->world == 1) {
+    if (c->world == 1 && c->g32) {
+        // 32-bit ids: 4 B per maximum, 8 B per saddle, 12 B per arc
+        CK(c->h32_maxima.ensure(sizeof(int32_t) * std::max<int64_t>(nm, 1)));
+        CK(c->h32_saddles.ensure(sizeof(int32_t) * std::max<int64_t>(ns, 1)));
+        CK(c->h32_arc_s.ensure(sizeof(int32_t) * std::max<int64_t>(na, 1)));
+        CK(c->h32_arc_m.ensure(sizeof(int32_t) * std::max<int64_t>(na, 1)));
+        int64_t om = 0, os = 0, oa = 0;
+        for (SlabState *S : c->slabs) {
+            if (S->n_max && !c->early_d2h) {
+                CK(S->maxima32.ensure(sizeof(int32_t) * S->n_max));
+                CK(launch_narrow(S->maxima64.as<int64_t>(), S->maxima32.as<int32_t>(), S->n_max, st));
+                CK(cudaMemcpyAsync(c->h32_maxima.as<int32_t>() + om, S->maxima32.p, sizeof(int32_t) * S->n_max,
+                                   cudaMemcpyDeviceToHost, st));
+            }
+            if (S->n_sad && !c->early_d2h) {
+                CK(cudaMemcpyAsync(c->h32_saddles.as<int32_t>() + os, S->saddles32.p, sizeof(int32_t) * S->n_sad,
+                                   cudaMemcpyDeviceToHost, st));
+                CK(cudaMemcpyAsync(c->h_sbeta.as<int32_t>() + os, S->sbeta.p, sizeof(int32_t) * S->n_sad,
+                                   cudaMemcpyDeviceToHost, st));
+            }
+            if (S->n_arc) {
+                CK(S->arc_s32.ensure(sizeof(int32_t) * S->n_arc));
+                CK(S->arc_m32.ensure(sizeof(int32_t) * S->n_arc));
+                CK(launch_narrow(S->arc_s.as<int64_t>(), S->arc_s32.as<int32_t>(), S->n_arc, st));
+                CK(launch_narrow(S->arc_m.as<int64_t>(), S->arc_m32.as<int32_t>(), S->n_arc, st));
+                CK(cudaMemcpyAsync(c->h32_arc_s.as<int32_t>() + oa, S->arc_s32.p, sizeof(int32_t) * S->n_arc,
+                                   cudaMemcpyDeviceToHost, st));
+                CK(cudaMemcpyAsync(c->h32_arc_m.as<int32_t>() + oa, S->arc_m32.p, sizeof(int32_t) * S->n_arc,
+                                   cudaMemcpyDeviceToHost, st));
+                CK(cudaMemcpyAsync(c->h_arc_mult.as<int32_t>() + oa, S->arc_mult.p, sizeof(int32_t) * S->n_arc,
+                                   cudaMemcpyDeviceToHost, st));
+            }
+            om += S->n_max;
+            os += S->n_sad;
+            oa += S->n_arc;
+        }
+        if (c->early_d2h) CK(cudaStreamWaitEvent(st, c->ev_d2h[2], 0));   // the node lists' copies
+    } else if (c->world == 1) {
         int64_t om = 0, os = 0, oa = 0;
         for (SlabState *S : c->slabs) {
             if (S->n_max && !c->early_d2h)
@@ -1157,6 +1213,9 @@ static eg_status compute_impl(eg_ctx *c, const eg_domain *d, const float *f, uin
     }
     c->paths_valid = false;
     c->bundle = (flags & EG_BUNDLE) != 0;
+    c->g32 = (flags & EG_GRAPH32) && c->world == 1 && !c->bundle && !(flags & (EG_MINIMUM | EG_NODE_VALUES));
+    c->h64_valid = !c->g32;
+    c->h32_valid = c->g32;
     if (c->bundle && (c->world > 1 || ((flags >> 16) & 0xffff) > 1))
         return set_err(c, EG_ERR_UNSUPPORTED, "EG_BUNDLE: one GPU, one slab");
     if (flags & EG_ARC_PATHS) {
@@ -1541,10 +1600,60 @@ eg_status eg_gradient(eg_ctx *c, const eg_domain *d, const float *d_field, int32
     return fail_if_flags(c);
 }
 
+// the host graph in the other id width, on first use (EG_GRAPH32)
+static eg_status host_graph_width(eg_ctx *c, bool want64) {
+    const int64_t nm = c->n_max, ns = c->n_sad, na = c->n_arc;
+    if (want64 && !c->h64_valid) {
+        CK(c->h_maxima.ensure(sizeof(int64_t) * std::max<int64_t>(nm, 1)));
+        CK(c->h_saddles.ensure(sizeof(int64_t) * std::max<int64_t>(ns, 1)));
+        CK(c->h_arc_s.ensure(sizeof(int64_t) * std::max<int64_t>(na, 1)));
+        CK(c->h_arc_m.ensure(sizeof(int64_t) * std::max<int64_t>(na, 1)));
+        for (int64_t i = 0; i < nm; ++i) c->h_maxima.as<int64_t>()[i] = c->h32_maxima.as<int32_t>()[i];
+        for (int64_t i = 0; i < ns; ++i) c->h_saddles.as<int64_t>()[i] = c->h32_saddles.as<int32_t>()[i];
+        for (int64_t i = 0; i < na; ++i) {
+            c->h_arc_s.as<int64_t>()[i] = c->h32_arc_s.as<int32_t>()[i];
+            c->h_arc_m.as<int64_t>()[i] = c->h32_arc_m.as<int32_t>()[i];
+        }
+        c->h64_valid = true;
+    }
+    if (!want64 && !c->h32_valid) {
+        CK(c->h32_maxima.ensure(sizeof(int32_t) * std::max<int64_t>(nm, 1)));
+        CK(c->h32_saddles.ensure(sizeof(int32_t) * std::max<int64_t>(ns, 1)));
+        CK(c->h32_arc_s.ensure(sizeof(int32_t) * std::max<int64_t>(na, 1)));
+        CK(c->h32_arc_m.ensure(sizeof(int32_t) * std::max<int64_t>(na, 1)));
+        for (int64_t i = 0; i < nm; ++i) c->h32_maxima.as<int32_t>()[i] = int32_t(c->h_maxima.as<int64_t>()[i]);
+        for (int64_t i = 0; i < ns; ++i) c->h32_saddles.as<int32_t>()[i] = int32_t(c->h_saddles.as<int64_t>()[i]);
+        for (int64_t i = 0; i < na; ++i) {
+            c->h32_arc_s.as<int32_t>()[i] = int32_t(c->h_arc_s.as<int64_t>()[i]);
+            c->h32_arc_m.as<int32_t>()[i] = int32_t(c->h_arc_m.as<int64_t>()[i]);
+        }
+        c->h32_valid = true;
+    }
+    return EG_OK;
+}
+
+eg_status eg_get_graph32(eg_ctx *c, eg_graph32 *out) {
+    if (!c || !out) return EG_ERR_INVALID_ARG;
+    if (c->poisoned) return set_err(c, EG_ERR_STATE, "context is poisoned: %s", c->err.c_str());
+    if (!c->have_graph || !c->graph_on_host) return set_err(c, EG_ERR_STATE, "no graph on the host (call eg_compute)");
+    ST(host_graph_width(c, false));
+    out->n_max = c->n_max;
+    out->n_saddle = c->n_sad;
+    out->n_arc = c->n_arc;
+    out->maxima = c->h32_maxima.as<int32_t>();
+    out->saddles = c->h32_saddles.as<int32_t>();
+    out->saddle_beta = c->h_sbeta.as<int32_t>();
+    out->arc_saddle = c->h32_arc_s.as<int32_t>();
+    out->arc_max = c->h32_arc_m.as<int32_t>();
+    out->arc_mult = c->h_arc_mult.as<int32_t>();
+    return EG_OK;
+}
+
 eg_status eg_get_graph(eg_ctx *c, eg_graph *out) {
     if (!c || !out) return EG_ERR_INVALID_ARG;
     if (c->poisoned) return set_err(c, EG_ERR_STATE, "context is poisoned: %s", c->err.c_str());
     if (!c->have_graph || !c->graph_on_host) return set_err(c, EG_ERR_STATE, "no graph on the host (call eg_compute)");
+    ST(host_graph_width(c, true));
     out->n_max = c->n_max;
     out->n_saddle = c->n_sad;
     out->n_arc = c->n_arc;
@@ -1618,7 +1727,8 @@ eg_status eg_destroy(eg_ctx *c) {
     DevBuf *bufs[] = {&c->typed, &c->rank_scratch, &c->d_fnode, &c->bund_scratch, &c->b_sad64, &c->b_sad32, &c->b_sbeta, &c->b_nu, &c->b_arc_s, &c->b_arc_m,
                       &c->b_arc_mult, &c->label_all, &c->csr_scratch, &c->fix_dev, &c->stat_buf, &c->field, &c->mirror, &c->path_len, &c->path_off, &c->path_v, &c->flags, &c->counts, &c->scratch, &c->tab, &c->gsend, &c->grecv};
     for (DevBuf *b : bufs) b->release();
-    HostBuf *hb[] = {&c->h_fmax, &c->h_fsad, &c->h_maxima, &c->h_saddles, &c->h_sbeta, &c->h_arc_s, &c->h_arc_m, &c->h_arc_mult,
+    HostBuf *hb[] = {&c->h32_maxima, &c->h32_saddles, &c->h32_arc_s, &c->h32_arc_m,
+                     &c->h_fmax, &c->h_fsad, &c->h_maxima, &c->h_saddles, &c->h_sbeta, &c->h_arc_s, &c->h_arc_m, &c->h_arc_mult,
                      &c->h_raw_s, &c->h_raw_rep, &c->h_raw_m, &c->h_counts, &c->h_stage, &c->h_path_off,
                      &c->h_path_v};
     for (HostBuf *b : hb) b->release();

@@ -149,6 +149,8 @@ cudaError_t launch_arcs_csr_reps(const int64_t *row_ptr, const int32_t *rep_buf,
                                  const int32_t *sbeta, int64_t n_sad, const int64_t *slot_off, LabelView lv,
                                  int32_t *tmp_m, int32_t *tmp_mult, int32_t *n_unique, int64_t *raw_s,
                                  int64_t *raw_rep, int64_t *raw_m, cudaStream_t st);
+// int64 -> int32 ids (EG_GRAPH32 host copies; every id < 2^31)
+cudaError_t launch_narrow(const int64_t *in, int32_t *out, int64_t n, cudaStream_t st);
 cudaError_t launch_emit_arcs(const int32_t *saddles, int64_t n_sad, const int64_t *slot_off, const int64_t *arc_off,
                              const int32_t *tmp_m, const int32_t *tmp_mult, const int32_t *n_unique,
                              int64_t *arc_s, int64_t *arc_m, int32_t *arc_mult, cudaStream_t st,

@@ -242,6 +242,17 @@ cudaError_t launch_emit_arcs(const int32_t *saddles, int64_t n_sad, const int64_
     return cudaGetLastError();
 }
 
+__global__ void k_narrow(const int64_t *__restrict__ in, int32_t *out, int64_t n) {
+    const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i < n) out[i] = int32_t(in[i]);
+}
+
+cudaError_t launch_narrow(const int64_t *in, int32_t *out, int64_t n, cudaStream_t st) {
+    if (n <= 0) return cudaSuccess;
+    k_narrow<<<blocks_for(n, 256), 256, 0, st>>>(in, out, n);
+    return cudaGetLastError();
+}
+
 __global__ void k_gather_beta(const uint8_t *__restrict__ beta8, int64_t v0, const int32_t *__restrict__ saddles,
                               int64_t n, int32_t *out) {
     const int64_t j = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;

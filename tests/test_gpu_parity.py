@@ -290,6 +290,38 @@ def test_compute_host_e2e(eg, ctx):
     assert_graph_equal(g2, o)
 
 
+def test_graph32(eg, ctx):
+    """EG_GRAPH32: the graph crosses to the host with 32-bit ids (eg_get_graph32);
+    eg_get_graph widens it on demand, and a 64-bit graph narrows for
+    eg_get_graph32 -- every path gives the oracle's graph."""
+    import ctypes as C
+    import torch
+    from paper_2303_02724_b200 import _abi
+    f, dims = G.c2_gaussians_noise(n=64, seed=3, k=8)
+    o = O.grid(f, dims)
+    t = torch.from_numpy(f).cuda()
+    for extra in (0, eg.EG_FORCE_GENERIC, eg.EG_VIRTUAL_PARTS(3), eg.EG_BUNDLE, eg.EG_NODE_VALUES):
+        g = ctx.compute(t, dims=dims, flags=eg.EG_GRAPH32 | extra)
+        exp = O.bundle(o, f) if extra == eg.EG_BUNDLE else o
+        assert_graph_equal(g, exp, what=f"graph32 {extra}")
+        g64 = _abi.EgGraph()                      # the other width from the same compute
+        assert _abi.lib().eg_get_graph(ctx._h, C.byref(g64)) == 0
+        assert g64.n_arc == len(exp.arc_s) and [g64.arc_max[i] for i in range(min(5, g64.n_arc))] == \
+            exp.arc_m[:5].tolist()
+    g = ctx.compute(t, dims=dims)                 # 64-bit graph, read as 32-bit
+    g32 = _abi.EgGraph32()
+    assert _abi.lib().eg_get_graph32(ctx._h, C.byref(g32)) == 0
+    assert [g32.saddles[i] for i in range(g32.n_saddle)] == o.saddles.tolist()
+    X, fc = G.gmm_points(5000, seed=2)
+    rp, ci = G.knn_csr(X, 12)
+    csr = (torch.from_numpy(rp).cuda(), torch.from_numpy(ci).cuda())
+    assert_graph_equal(ctx.compute(torch.from_numpy(fc).cuda(), csr=csr, flags=eg.EG_GRAPH32), O.csr(fc, rp, ci),
+                       what="graph32 csr")
+    host = torch.from_numpy(f).pin_memory()
+    lab = torch.empty(len(f), dtype=torch.int32).pin_memory()
+    assert_graph_equal(ctx.compute_host(host, dims=dims, labels_out=lab, flags=eg.EG_GRAPH32), o, what="graph32 e2e")
+
+
 @pytest.mark.parametrize("chunks", ["2", "5", "16", "32", "1"])
 def test_compute_host_pipeline(eg, ctx, chunks, monkeypatch):
     """eg_compute_host's pipeline (field in z-chunks, each chunk's labels
