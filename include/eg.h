@@ -46,12 +46,13 @@ typedef enum {
     EG_ERR_CUDA = 4,          /* CUDA runtime error (sticky)                     */
     EG_ERR_NCCL = 5,          /* NCCL error (sticky)                             */
     EG_ERR_STATE = 6,         /* call out of order (e.g. get_graph before compute) */
-    EG_ERR_UNSUPPORTED = 7    /* e.g. N >= 2^31, ndim > 6, CSR degree > 128     */
+    EG_ERR_UNSUPPORTED = 7    /* e.g. N >= 2^31, a flag combination not built   */
 } eg_status;
 
 enum { EG_DOMAIN_GRID = 0, EG_DOMAIN_CSR = 1 };
 
-/* Regular grid.  dims[0] is the fastest axis; 1 <= ndim <= 6.
+/* Regular grid.  dims[0] is the fastest axis; 1 <= ndim <= 8
+ * (n <= 3: the tiled kernels; n = 4..8: the generic n-D kernels).
  * slab_begin/slab_end: the planes of the slowest axis owned by this rank
  * (multi-GPU slab partition, "blocks ... along the z-axis");
  * [0, dims[ndim-1]) on one GPU.  d_field then holds ONLY the owned planes,

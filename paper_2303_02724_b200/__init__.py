@@ -50,6 +50,8 @@ class Graph:
 
 
 def grid_domain(dims: Sequence[int], slab: Optional[Sequence[int]] = None) -> _abi.EgDomain:
+    if not 1 <= len(dims) <= 8:      # the eg_grid struct holds 8 extents (include/eg.h)
+        raise EgError(_abi.EG_ERR_INVALID_ARG, f"ndim {len(dims)} not in [1, 8]")
     d = _abi.EgDomain()
     d.kind = _abi.EG_DOMAIN_GRID
     d.grid.ndim = len(dims)

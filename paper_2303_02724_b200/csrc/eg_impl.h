@@ -11,8 +11,8 @@
 
 namespace eg {
 
-constexpr int kMaxDim = 6;                 // generic grid kernels: n <= 6
-constexpr int kMaxLink = 126;              // 2 (2^6 - 1)
+constexpr int kMaxDim = 8;                 // generic grid kernels: n <= 8
+constexpr int kMaxLink = 510;              // 2 (2^8 - 1)
 constexpr uint32_t kUnresolved = 0x80000000u;   // label bit 31: not final, low bits = a vertex further on the path
 
 // Freudenthal link of an interior vertex: the offsets d in
@@ -28,7 +28,7 @@ struct LinkTable {
     int64_t stride[8];
     int8_t d[kMaxLink][8];
     int64_t delta[kMaxLink];
-    uint64_t nbr[kMaxLink][2];
+    uint64_t nbr[kMaxLink][2];             // (filled for K <= 128, n <= 6: the 3-D LUT builder)
 };
 
 LinkTable make_link_table(int ndim, const int64_t *dims);

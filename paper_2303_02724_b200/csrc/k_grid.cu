@@ -1,4 +1,4 @@
-// Generic n-D grid kernels (n = 1..6): S1 steepest-ascent pointer, S3 upper-
+// Generic n-D grid kernels (n = 1..8): S1 steepest-ascent pointer, S3 upper-
 // link components, and the per-saddle part of S4.  One thread per vertex, the
 // way the paper's classification kernel is organised ("launching a CUDA
 // thread for each vertex"); n <= 3 grids normally take the tiled kernel in
@@ -27,7 +27,78 @@
 
 namespace eg {
 
-template <int NDIM>
+// A 2^n-bit word for n = 7, 8 (M = 128, 256): K 64-bit limbs, bit i in limb
+// i / 64.  Only what the lattice closure needs: bit ops, single-bit set,
+// lowest-bit / pop, and the subset shifts (see Lattice::up / down).
+template <int K>
+struct Bits {
+    uint64_t w[K];
+    __host__ __device__ constexpr Bits() : w{} {}
+    __host__ __device__ constexpr explicit Bits(uint64_t lo) : w{} { w[0] = lo; }
+    __host__ __device__ static constexpr Bits bit(int i) {
+        Bits r;
+        r.w[i >> 6] = 1ull << (i & 63);
+        return r;
+    }
+    __host__ __device__ constexpr Bits operator|(const Bits &o) const {
+        Bits r;
+        for (int k = 0; k < K; ++k) r.w[k] = w[k] | o.w[k];
+        return r;
+    }
+    __host__ __device__ constexpr Bits operator&(const Bits &o) const {
+        Bits r;
+        for (int k = 0; k < K; ++k) r.w[k] = w[k] & o.w[k];
+        return r;
+    }
+    __host__ __device__ constexpr Bits operator~() const {
+        Bits r;
+        for (int k = 0; k < K; ++k) r.w[k] = ~w[k];
+        return r;
+    }
+    __host__ __device__ constexpr Bits &operator|=(const Bits &o) {
+        for (int k = 0; k < K; ++k) w[k] |= o.w[k];
+        return *this;
+    }
+    __host__ __device__ constexpr Bits &operator&=(const Bits &o) {
+        for (int k = 0; k < K; ++k) w[k] &= o.w[k];
+        return *this;
+    }
+    __host__ __device__ constexpr bool operator==(const Bits &o) const {
+        for (int k = 0; k < K; ++k)
+            if (w[k] != o.w[k]) return false;
+        return true;
+    }
+    __host__ __device__ constexpr bool operator!=(const Bits &o) const { return !(*this == o); }
+    __host__ __device__ constexpr explicit operator bool() const {
+        for (int k = 0; k < K; ++k)
+            if (w[k]) return true;
+        return false;
+    }
+    __host__ __device__ constexpr bool test(int i) const { return (w[i >> 6] >> (i & 63)) & 1ull; }
+    // shift left / right by s bits, s a power of two (the subset shifts)
+    __host__ __device__ constexpr Bits shl(int s) const {
+        Bits r;
+        if (s >= 64) {
+            const int q = s >> 6;
+            for (int k = K - 1; k >= q; --k) r.w[k] = w[k - q];
+        } else {
+            for (int k = K - 1; k >= 0; --k) r.w[k] = (w[k] << s) | (k ? (w[k - 1] >> (64 - s)) : 0ull);
+        }
+        return r;
+    }
+    __host__ __device__ constexpr Bits shr(int s) const {
+        Bits r;
+        if (s >= 64) {
+            const int q = s >> 6;
+            for (int k = 0; k + q < K; ++k) r.w[k] = w[k + q];
+        } else {
+            for (int k = 0; k < K; ++k) r.w[k] = (w[k] >> s) | (k + 1 < K ? (w[k + 1] << (64 - s)) : 0ull);
+        }
+        return r;
+    }
+};
+
+template <int NDIM, bool kWide = (NDIM > 6)>
 struct Lattice {
     static constexpr int M = 1 << NDIM;  // subsets of the n axes
     using W = std::conditional_t<(M <= 32), uint32_t, uint64_t>;
@@ -62,6 +133,60 @@ struct Lattice {
         x &= x - 1;
         return b;
     }
+    __device__ __forceinline__ static W bit(int i) { return W(1) << i; }
+    __device__ __forceinline__ static bool test(W x, int i) { return (x >> i) & 1; }
+};
+
+// n = 7, 8: the same closure on multi-limb words
+template <int NDIM>
+struct Lattice<NDIM, true> {
+    static constexpr int M = 1 << NDIM;
+    using W = Bits<M / 64>;
+    __host__ __device__ static constexpr W full() { return ~W(); }
+    __host__ __device__ static constexpr W without(int a) {
+        W x;
+        for (int i = 0; i < M; ++i)
+            if (!((i >> a) & 1)) x |= W::bit(i);
+        return x;
+    }
+    __device__ __forceinline__ static W up(W x) {
+#pragma unroll
+        for (int a = 0; a < NDIM; ++a) x |= (x & without(a)).shl(1 << a);
+        return x;
+    }
+    __device__ __forceinline__ static W down(W x) {
+#pragma unroll
+        for (int a = 0; a < NDIM; ++a) x |= x.shr(1 << a) & without(a);
+        return x;
+    }
+    __device__ __forceinline__ static W rev(W x) {   // bit d -> bit M-1-d
+        W r;
+#pragma unroll
+        for (int k = 0; k < M / 64; ++k) r.w[M / 64 - 1 - k] = __brevll(x.w[k]);
+        return r;
+    }
+    __device__ __forceinline__ static W lowest(W x) {
+        W r;
+#pragma unroll
+        for (int k = 0; k < M / 64; ++k)
+            if (x.w[k]) {
+                r.w[k] = x.w[k] & (~x.w[k] + 1);
+                break;
+            }
+        return r;
+    }
+    __device__ __forceinline__ static int pop(W &x) {
+#pragma unroll
+        for (int k = 0; k < M / 64; ++k)
+            if (x.w[k]) {
+                const int b = __ffsll(x.w[k]) - 1;
+                x.w[k] &= x.w[k] - 1;
+                return 64 * k + b;
+            }
+        return -1;
+    }
+    __device__ __forceinline__ static W bit(int i) { return W::bit(i); }
+    __device__ __forceinline__ static bool test(const W &x, int i) { return x.test(i); }
 };
 
 // Per-grid constants, passed by value: every access with an unrolled (compile-
@@ -127,7 +252,7 @@ __device__ __forceinline__ void upper_link(const GridConst<NDIM> &S, const Field
     using L = Lattice<NDIM>;
     using W = typename L::W;
     constexpr int M = L::M;
-    W vp = L::full() & ~W(1), vn = vp;
+    W vp = L::full() & ~L::bit(0), vn = vp;
     uint32_t r = uint32_t(v);
 #pragma unroll
     for (int a = 0; a < NDIM; ++a) {
@@ -138,7 +263,7 @@ __device__ __forceinline__ void upper_link(const GridConst<NDIM> &S, const Field
         if (c == 0) vn &= L::without(a);
         if (c + 1 == D) vp &= L::without(a);
     }
-    W up = 0, un = 0;
+    W up{}, un{};
     float bf = -INFINITY;
     int bk = 0;  // -e or +d of the highest link vertex so far
     // kSafe: every offset's address is inside the array, so the loads are
@@ -147,7 +272,7 @@ __device__ __forceinline__ void upper_link(const GridConst<NDIM> &S, const Field
         constexpr bool kSafe = decltype(safe)::value;
 #pragma unroll
         for (int e = M - 1; e >= 1; --e) {  // lower indices: above v iff f > fv
-            const bool ok = (vn >> e) & 1;
+            const bool ok = L::test(vn, e);
             float fu;
             if constexpr (kSafe) {
                 fu = load(S.dneg[e]);
@@ -155,7 +280,7 @@ __device__ __forceinline__ void upper_link(const GridConst<NDIM> &S, const Field
             } else {
                 fu = ok ? load(S.dneg[e]) : nan_f();
             }
-            if (fu > fv) un |= W(1) << e;
+            if (fu > fv) un |= L::bit(e);
             if (fu >= bf) {
                 bf = fu;
                 bk = -e;
@@ -163,7 +288,7 @@ __device__ __forceinline__ void upper_link(const GridConst<NDIM> &S, const Field
         }
 #pragma unroll
         for (int d = 1; d < M; ++d) {  // higher indices: above v iff f >= fv
-            const bool ok = (vp >> d) & 1;
+            const bool ok = L::test(vp, d);
             float fu;
             if constexpr (kSafe) {
                 fu = load(S.dpos[d]);
@@ -171,7 +296,7 @@ __device__ __forceinline__ void upper_link(const GridConst<NDIM> &S, const Field
             } else {
                 fu = ok ? load(S.dpos[d]) : nan_f();
             }
-            if (fu >= fv) up |= W(1) << d;
+            if (fu >= fv) up |= L::bit(d);
             if (fu >= bf) {
                 bf = fu;
                 bk = d;
@@ -192,7 +317,7 @@ __device__ __forceinline__ void upper_link(const GridConst<NDIM> &S, const Field
     }
     Up = up;
     Un = un;
-    *best = (up | un) ? v + (bk < 0 ? -S.dpos[-bk] : S.dpos[bk]) : v;
+    *best = bool(up | un) ? v + (bk < 0 ? -S.dpos[-bk] : S.dpos[bk]) : v;
 }
 
 // beta0+  by lattice closure, see the file comment.  If reps !=
@@ -206,9 +331,9 @@ __device__ __forceinline__ int components(const GridConst<NDIM> &S, typename Lat
     using W = typename L::W;
     W P = Up, N = Un;  // not yet assigned to a component
     int beta = 0;
-    while (P | N) {
-        W cp = P ? L::lowest(P) : W(0);
-        W cn = P ? W(0) : L::lowest(N);
+    while (bool(P | N)) {
+        W cp = bool(P) ? L::lowest(P) : W{};
+        W cn = bool(P) ? W{} : L::lowest(N);
         for (;;) {
             const W np = Up & (L::up(cp) | L::down(cp | L::rev(cn)));
             const W nn = Un & (L::up(cn) | L::down(cn | L::rev(cp)));
@@ -221,7 +346,7 @@ __device__ __forceinline__ int components(const GridConst<NDIM> &S, typename Lat
         if (reps) {
             int64_t rep = -1;
             float rf = 0.f;
-            while (cn) {
+            while (bool(cn)) {
                 const int64_t u = v - S.dpos[L::pop(cn)];
                 const float fu = F.at(u);
                 if (rep < 0 || fu > rf || (fu == rf && u > rep)) {
@@ -229,7 +354,7 @@ __device__ __forceinline__ int components(const GridConst<NDIM> &S, typename Lat
                     rf = fu;
                 }
             }
-            while (cp) {
+            while (bool(cp)) {
                 const int64_t u = v + S.dpos[L::pop(cp)];
                 const float fu = F.at(u);
                 if (rep < 0 || fu > rf || (fu == rf && u > rep)) {
@@ -259,7 +384,7 @@ __global__ void __launch_bounds__(256) k_classify_grid(const __grid_constant__ G
         int64_t best;
         typename Lattice<NDIM>::W up, un;
         upper_link<NDIM, kPlain>(S, F, v, fv, up, un, &best);
-        is_max = (up | un) == 0;
+        is_max = !bool(up | un);
         const int beta = is_max ? 0 : components<NDIM>(S, up, un, F, v, nullptr);
         is_sad = beta >= 2;
         ptr[i] = int32_t(best);
@@ -382,7 +507,7 @@ __global__ void __launch_bounds__(128) k_arc_paths_grid(const __grid_constant__ 
         int64_t best;
         typename Lattice<NDIM>::W up, un;
         upper_link<NDIM, false>(S, F, v, F.at(v), up, un, &best);
-        if ((up | un) == 0) break;          // a maximum
+        if (!bool(up | un)) break;          // a maximum
         v = best;
     }
     if (!off) len_or_out[j] = k;
@@ -396,6 +521,8 @@ __global__ void __launch_bounds__(128) k_arc_paths_grid(const __grid_constant__ 
         case 4: CALL(4); break;                 \
         case 5: CALL(5); break;                 \
         case 6: CALL(6); break;                 \
+        case 7: CALL(7); break;                 \
+        case 8: CALL(8); break;                 \
         default: return cudaErrorInvalidValue;  \
     }
 

@@ -66,9 +66,10 @@ LinkTable make_link_table(int ndim, const int64_t *dims) {
         std::memcpy(t.d[k], offs[k].data(), 8);
         t.delta[k] = delta(offs[k]);
     }
-    for (int a = 0; a < t.K; ++a)
-        for (int b = 0; b < t.K; ++b)
-            if (a != b && alg1_offsets_adjacent(t.d[a], t.d[b], ndim)) t.nbr[a][b >> 6] |= 1ull << (b & 63);
+    if (t.K <= 128)   // explicit neighbour masks (the 3-D LUT builder); the kernels use the lattice closure
+        for (int a = 0; a < t.K; ++a)
+            for (int b = 0; b < t.K; ++b)
+                if (a != b && alg1_offsets_adjacent(t.d[a], t.d[b], ndim)) t.nbr[a][b >> 6] |= 1ull << (b & 63);
     return t;
 }
 

@@ -141,9 +141,9 @@ def test_invalid_args(eg, ctx):
     with pytest.raises(eg.EgError) as e:
         ctx.compute(t, dims=[2, 0, 4])
     assert "INVALID_ARG" in str(e.value)
-    with pytest.raises(eg.EgError) as e:
-        ctx.compute(t, dims=[2] * 7)
-    assert "UNSUPPORTED" in str(e.value)
+    with pytest.raises(eg.EgError) as e:         # 1 <= ndim <= 8
+        ctx.compute(t, dims=[2] * 9)
+    assert "INVALID_ARG" in str(e.value)
     with pytest.raises(eg.EgError) as e:      # N >= 2^31: rejected before touching memory
         ctx.compute(t, dims=[2048, 2048, 1024])
     assert "UNSUPPORTED" in str(e.value)
@@ -288,6 +288,24 @@ def test_compute_host_e2e(eg, ctx):
     assert np.array_equal(lab.numpy().astype(np.int64), o.label)
     g2 = ctx.compute_host(torch.from_numpy(f), dims=dims)      # pageable source
     assert_graph_equal(g2, o)
+
+
+@pytest.mark.parametrize("dims,kind", [([3, 4, 3, 3, 3, 3, 4], "int"), ([3, 4, 3, 3, 3, 3, 4], "normal"),
+                                       ([3, 2, 3, 2, 3, 2, 3, 4], "int"), ([4, 3, 3, 3, 3, 3, 3, 4], "normal")])
+def test_grid_7d_8d(eg, ctx, dims, kind):
+    """n = 7, 8 (1 <= ndim <= 8): the generic kernels on
+    multi-limb lattice words (254 / 510 link vertices), raw arcs, gradient,
+    and 2 virtual slabs."""
+    import torch
+    f, _ = G.random_field(dims, 40 + len(dims), kind, levels=3)
+    o = O.grid(f, dims)
+    t = torch.from_numpy(f).cuda()
+    assert_graph_equal(ctx.compute(t, dims=dims, flags=eg.EG_RAW_ARCS | eg.EG_CHECK_NAN), o, raw=True,
+                       what=f"{len(dims)}-D {kind}")
+    assert_graph_equal(ctx.compute(t, dims=dims, flags=eg.EG_VIRTUAL_PARTS(2)), o, what=f"{len(dims)}-D 2 slabs")
+    ptr, beta = ctx.gradient(t, dims=dims)
+    assert first_diff(ptr.cpu().numpy().astype(np.int64), o.ptr) is None
+    assert first_diff(beta.cpu().numpy().astype(np.int32), np.minimum(o.beta, 255)) is None
 
 
 def test_graph32(eg, ctx):

@@ -299,8 +299,26 @@ def _product_rule(profiles):
     return n_max, n_sad
 
 
+@pytest.mark.parametrize("n", [7, 8])
+def test_interior_link_size_high_dim(n):
+    # P:112's 2 x (2^n - 1) incident edges for n = 7, 8 (254, 510 link vertices);
+    # link-edge count = sum over link vertices of their link-link degree / 2,
+    # where +d ~ +d' iff one mask contains the other (likewise -e), and
+    # +d ~ -e iff the masks are disjoint (Alg. 1 on offsets):
+    # a closed form counted here independently of the oracle.
+    dims = [3] * n
+    v = (3 ** n - 1) // 2
+    nl, ne, _ = O.grid_link_stats(dims, v)
+    assert nl == 2 * (2 ** n - 1)
+    M = 1 << n
+    same = sum(1 for a in range(1, M) for b in range(1, M) if a != b and (a & b) in (a, b))   # ordered pairs
+    cross = sum(1 for a in range(1, M) for b in range(1, M) if (a & b) == 0)
+    assert ne == same + cross      # (2 * same / 2) over the +/- halves, + cross edges
+
+
 @pytest.mark.parametrize("dims,seed", [([40, 40], 0), ([40, 40], 1), ([24, 24, 24], 2), ([24, 24, 24], 3),
-                                       ([12, 12, 12, 12], 4), ([7, 7, 7, 7, 7], 5)])
+                                       ([12, 12, 12, 12], 4), ([7, 7, 7, 7, 7], 5),
+                                       ([3, 4, 3, 3, 4, 3, 3], 6), ([3, 2, 3, 2, 3, 2, 3, 2], 7)])
 def test_separable_product_rule(dims, seed):
     # tie-free separable f = sum_i h_i(x_i): #maxima = prod M_i and
     # #(n-1)-saddles = sum_i S_i prod_{j != i} M_j, all beta0+ = 2.
