@@ -806,7 +806,10 @@ static eg_status compute_grid(eg_ctx *c, const Problem &P, const float *f, uint3
     set_slab_count(c, plan.size());
     // labels: one array for every slab of this process (a view per slab)
     const int64_t nlab = (c->world > 1) ? P.v1 - P.v0 : P.N;
-    CK(c->label_all.ensure(sizeof(int32_t) * std::max<int64_t>(nlab, 1)));
+    // several GPUs: one halo plane of labels below and above the owned ones,
+    // filled with the neighbours' final boundary values before the label pass
+    const int64_t hpad = (c->world > 1) ? P.plane : 0;
+    CK(c->label_all.ensure(sizeof(int32_t) * std::max<int64_t>(nlab + 2 * hpad, 1)));
     const int64_t base_v = (c->world > 1) ? P.v0 : 0;
     for (size_t k = 0; k < plan.size(); ++k) {
         SlabState &S = *c->slabs[k];
@@ -816,7 +819,7 @@ static eg_status compute_grid(eg_ctx *c, const Problem &P, const float *f, uint3
         S.s.v0 = S.s.z0 * P.plane;
         S.s.v1 = S.s.z1 * P.plane;
         const int64_t n = S.s.v1 - S.s.v0, words = (n + 31) / 32;
-        S.label = c->label_all.as<int32_t>() + (S.s.v0 - base_v);
+        S.label = c->label_all.as<int32_t>() + hpad + (S.s.v0 - base_v);
         S.F.own = f + (S.s.v0 - base_v);     // f holds the whole grid (single / virtual) or the owned planes
         S.F.v0 = S.s.v0;
         S.F.v1 = S.s.v1;
@@ -927,19 +930,48 @@ static eg_status compute_grid(eg_ctx *c, const Problem &P, const float *f, uint3
     }
     const bool piped = c->io && c->io->done;      // eg_compute_host pipeline: labels finished on c->io->fst
     if (piped) CK(cudaStreamWaitEvent(c->stream, c->io->fin_done, 0));
+    if (multi) {
+        // every boundary value is final now: each slab's own boundary planes
+        // take them, and (several GPUs) the halo planes around the owned labels
+        // take the neighbours'; then ONE label pass over the whole label array
+        // of this process chases exactly like the one-slab pass: a chain that
+        // reaches another slab stops at a final boundary value
+        const int64_t pl = P.plane;
+        for (SlabState *S : c->slabs) {
+            const int64_t n = S->s.v1 - S->s.v0;
+            CK(cudaMemcpyAsync(S->label, S->bval.p, 4 * pl, cudaMemcpyDeviceToDevice, c->stream));
+            CK(cudaMemcpyAsync(S->label + n - pl, S->bval.as<int32_t>() + pl, 4 * pl, cudaMemcpyDeviceToDevice,
+                               c->stream));
+        }
+        int64_t e0 = base_v, e1 = base_v + nlab;
+        if (c->world > 1) {
+            SlabState &S = *c->slabs[0];
+            if (S.has_lo) {
+                CK(cudaMemcpyAsync(c->label_all.p, S.hval_lo.p, 4 * pl, cudaMemcpyDeviceToDevice, c->stream));
+                e0 -= pl;
+            }
+            if (S.has_hi) {
+                CK(cudaMemcpyAsync(c->label_all.as<int32_t>() + hpad + nlab, S.hval_hi.p, 4 * pl,
+                                   cudaMemcpyDeviceToDevice, c->stream));
+                e1 += pl;
+            }
+        }
+        int32_t *lab0 = c->label_all.as<int32_t>() + hpad - (base_v - e0);
+        CK(launch_finalize(lab0, nullptr, e0, e1, c->stream,
+                           (flags & EG_STATS) ? c->stat_buf.as<unsigned long long>() + 1 : nullptr));
+        c->stats.kernel_launches += 1;
+    }
     for (SlabState *S : c->slabs) {
         if (!tiled && !multi) continue;           // generic single slab: already final
-        if (piped) continue;
-        CK(launch_finalize(S->label, nullptr, S->s.v0, S->s.v1,
-                           S->has_lo ? S->hval_lo.as<int32_t>() : nullptr,
-                           S->has_hi ? S->hval_hi.as<int32_t>() : nullptr, P.plane, c->stream,
+        if (piped || multi) continue;
+        CK(launch_finalize(S->label, nullptr, S->s.v0, S->s.v1, c->stream,
                            (flags & EG_STATS) ? c->stat_buf.as<unsigned long long>() + 1 : nullptr));
         c->stats.kernel_launches += 1;
     }
     if (tiled || multi) CK(cudaEventRecord(c->ev_s2[5], c->stream));
     CK(cudaEventRecord(c->ev[2], c->stream));
     if (!c->overlap) ST(fail_if_flags(c));
-    c->d_labels = c->label_all.as<int32_t>();
+    c->d_labels = c->label_all.as<int32_t>() + hpad;
     c->n_own = nlab;
     c->have_labels = true;
     // one GPU, one slab, graph wanted: the node lists are copied early

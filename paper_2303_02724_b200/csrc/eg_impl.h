@@ -259,6 +259,6 @@ cudaError_t launch_finalize_list(int32_t *label, const int32_t *list, const unsi
                                  int64_t list_cap, int64_t v0, int64_t n_all, cudaStream_t st,
                                  unsigned long long *hist = nullptr);
 cudaError_t launch_gather_labels(const int32_t *label, const int32_t *list, int64_t n, int32_t *out, cudaStream_t st);
-cudaError_t launch_finalize(int32_t *label, const uint32_t *bits, int64_t v0, int64_t v1, const int32_t *hval_lo,
-                            const int32_t *hval_hi, int64_t plane, cudaStream_t st, unsigned long long *hist = nullptr);
+cudaError_t launch_finalize(int32_t *label, const uint32_t *bits, int64_t v0, int64_t v1, cudaStream_t st,
+                            unsigned long long *hist = nullptr);
 }  // namespace eg

@@ -102,9 +102,7 @@ cudaError_t launch_bval_update(int32_t *bval, const int32_t *hval_lo, const int3
 constexpr int kW = 6;
 template <bool kStats>
 __global__ void __launch_bounds__(128, 16) k_finalize(int32_t *label, const uint32_t *__restrict__ bits, int64_t v0,
-                                                  int64_t v1, const int32_t *__restrict__ hlo,
-                                                  const int32_t *__restrict__ hhi, int64_t plane,
-                                                  unsigned long long *hist) {
+                                                  int64_t v1, unsigned long long *hist) {
     const int64_t n = v1 - v0;
     const int64_t words = (n + 31) / 32;
     const int64_t w0 = (int64_t(blockIdx.x) * (blockDim.x / 32) + (threadIdx.x >> 5)) * kW;
@@ -126,10 +124,11 @@ __global__ void __launch_bounds__(128, 16) k_finalize(int32_t *label, const uint
     for (int k = 0; k < kW; ++k) e[k] = need[k] ? label[(w0 + k) * 32 + lane] : 0;
 #pragma unroll
     for (int k = 0; k < kW; ++k) need[k] = need[k] && e[k] < 0;
-    if (!hlo && !hhi) {
-        // one slab: every exit target is owned.  Its label is final when the
-        // exit list was resolved first (k_resolve_exits); otherwise the chain
-        // is chased here, through L1-cached loads (race-benign: every value
+    {
+        // every exit target lies in [v0, v1) (one slab; several slabs: the
+        // array then spans the halo planes, whose values are final).  Its label
+        // is final when the exit list was resolved first (k_resolve_exits);
+        // otherwise the chain is chased here, through L1-cached loads (race-benign: every value
         // ever stored is a later vertex of the same ascending path or the
         // final label, and a root's label is final before this pass, so a
         // stale value only lengthens a walk).  Measured on C3 / F1-512 /
@@ -167,28 +166,7 @@ __global__ void __launch_bounds__(128, 16) k_finalize(int32_t *label, const uint
 #pragma unroll
         for (int k = 0; k < kW; ++k)
             if (need[k]) label[(w0 + k) * 32 + lane] = e[k];
-        return;
     }
-    // several slabs: follow the chain through owned vertices (race-benign as
-    // above) to a final label, or to its first vertex outside the slab, whose
-    // value the boundary exchange made final (hval).  The first hop of every
-    // word is issued before any chain is followed further.
-    auto step = [&](int32_t w) -> int32_t {     // one hop from exit pointer w
-        const int64_t x = w & 0x7fffffff;
-        if (x < v0) return hlo[x - v0 + plane];
-        if (x >= v1) return hhi[x - v1];
-        return __ldca(label + (x - v0));        // written by this kernel: not the read-only path
-    };
-#pragma unroll
-    for (int k = 0; k < kW; ++k)
-        if (need[k]) e[k] = step(e[k]);
-#pragma unroll
-    for (int k = 0; k < kW; ++k)
-        if (need[k])
-            while (e[k] < 0) e[k] = step(e[k]);
-#pragma unroll
-    for (int k = 0; k < kW; ++k)
-        if (need[k]) label[(w0 + k) * 32 + lane] = e[k];
 }
 
 // The one-slab label pass in z-chunks, for the end-to-end pipeline of
@@ -337,16 +315,14 @@ cudaError_t launch_gather_labels(const int32_t *label, const int32_t *list, int6
     return cudaGetLastError();
 }
 
-cudaError_t launch_finalize(int32_t *label, const uint32_t *bits, int64_t v0, int64_t v1, const int32_t *hval_lo,
-                            const int32_t *hval_hi, int64_t plane, cudaStream_t st, unsigned long long *hist) {
+cudaError_t launch_finalize(int32_t *label, const uint32_t *bits, int64_t v0, int64_t v1, cudaStream_t st,
+                            unsigned long long *hist) {
     const int64_t words = (v1 - v0 + 31) / 32;
     if (words <= 0) return cudaSuccess;
     if (hist)
-        k_finalize<true><<<blocks_for(words, 4 * kW), 128, 0, st>>>(label, bits, v0, v1, hval_lo, hval_hi, plane,
-                                                                     hist);
+        k_finalize<true><<<blocks_for(words, 4 * kW), 128, 0, st>>>(label, bits, v0, v1, hist);
     else
-        k_finalize<false><<<blocks_for(words, 4 * kW), 128, 0, st>>>(label, bits, v0, v1, hval_lo, hval_hi, plane,
-                                                                      nullptr);
+        k_finalize<false><<<blocks_for(words, 4 * kW), 128, 0, st>>>(label, bits, v0, v1, nullptr);
     return cudaGetLastError();
 }
 
