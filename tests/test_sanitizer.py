@@ -34,6 +34,11 @@ def _run(tool, case):
     cmd += [sys.executable, os.path.join(ROOT, "tools", "sanitize_case.py"), case]
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=1200, cwd=ROOT)
     out = r.stdout + r.stderr
+    if "closed on this pool" in out:
+        # the GPU pool's operators replaced compute-sanitizer with a stub (runs under
+        # it left GPUs needing a reset); the clean reports of earlier runs are under
+        # profiles/r02/sanitizer/
+        pytest.skip("compute-sanitizer is disabled on this GPU pool")
     d = os.environ.get("EG_SANITIZER_LOG")
     if d:
         os.makedirs(d, exist_ok=True)
