@@ -54,9 +54,13 @@ def build(force: bool = False, verbose: bool = False) -> str:
     objdir = os.path.join(HERE, "build_obj")
     os.makedirs(objdir, exist_ok=True)
     procs, objs = [], []
+    newest_header = max([os.path.getmtime(h) for h in headers()] + [os.path.getmtime(__file__)])
     for src in sources():
         obj = os.path.join(objdir, os.path.basename(src)[:-3] + ".o")
         objs.append(obj)
+        if (not force and os.path.exists(obj) and os.path.getmtime(obj) > os.path.getmtime(src)
+                and os.path.getmtime(obj) > newest_header):
+            continue                      # object up to date
         cmd = [NVCC, *NVCC_FLAGS, "-I", os.path.join(ROOT, "include"), "-I", inc, "-c", "-o", obj, src]
         if verbose:
             print(" ".join(cmd), file=sys.stderr)

@@ -6,6 +6,7 @@
 
 namespace eg {
 struct Tiled3D;
+constexpr int kTileY = 16, kTileZ = 16;   // tile rows / planes of k_tile (k_grid3d.cu: TY, TZ)
 
 // End-to-end pipeline of eg_compute_host on one slab of one GPU (k_grid3d.cu):
 // the field arrives in z-chunks on stream h2d; tile chunk k starts when chunk

@@ -40,7 +40,7 @@
 
 namespace eg {
 
-constexpr int TX = 32, TY = 16, TZ = 16;
+constexpr int TX = 32, TY = kTileY, TZ = kTileZ;
 constexpr int XO = 4;                                // box x of the tile's first column: boxes start at x0 - 4 (16-byte aligned)
 constexpr int BX = TX + 2 * XO;                      // 40
 constexpr int BY = TY + 2, BZ = TZ + 2;
