@@ -125,7 +125,8 @@ enum {
     EG_RAW_ARCS = 2u,         /* also keep raw (s, rep, m) per component     */
     EG_CHECK_CSR = 4u,        /* validate CSR sortedness / symmetry           */
     EG_FORCE_GENERIC = 8u,    /* grid: use the generic n-D kernels even for n <= 3 */
-    EG_NO_GRAPH_D2H = 16u,    /* leave the graph on the device (eg_get_graph then fails) */
+    EG_NO_GRAPH_D2H = 16u,    /* leave the graph in HBM: one process -> eg_get_graph* copy it on the
+                                 first request; several ranks -> eg_get_graph* fail (EG_ERR_STATE) */
     /* The MINIMUM graph instead ("computes both maximum and
      * minimum graph"; reading L11): minima, 1-saddles (beta0 of the lower link
      * >= 2) and the descending arcs / labels -- the maximum graph under the
@@ -174,7 +175,9 @@ eg_status eg_create_dist(eg_ctx **out, int cuda_device, void *cuda_stream, const
 
 /* Compute S1..S4 for a device-resident field.  Stream-ordered on the ctx
  * stream; returns after one final synchronisation with the graph copied to
- * host memory owned by the ctx (unless EG_NO_GRAPH_D2H). */
+ * host memory owned by the ctx (unless EG_NO_GRAPH_D2H: then it stays in
+ * ctx-owned device memory until the next compute and, on one process, the
+ * first eg_get_graph / eg_get_graph32 / eg_get_raw_arcs copies it). */
 eg_status eg_compute(eg_ctx *ctx, const eg_domain *domain, const float *d_field, uint32_t flags);
 
 /* Other input types (readings L21/L22 in DESIGN.md).

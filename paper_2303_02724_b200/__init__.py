@@ -161,8 +161,14 @@ class Context:
         return self._graph(flags) if materialize else None
 
     def graph(self) -> Graph:
-        """The graph of the last compute as numpy arrays (copies)."""
-        return self._graph(getattr(self, "_last_flags", 0))
+        """The graph of the last compute as numpy arrays (copies).  After a
+        compute with EG_NO_GRAPH_D2H (graph left in HBM) the library copies
+        it to the host here (one process)."""
+        self._fetch = True
+        try:
+            return self._graph(getattr(self, "_last_flags", 0))
+        finally:
+            self._fetch = False
 
     def compute_host(self, field: torch.Tensor, dims=None, csr=None, flags: int = 0, labels_out=None,
                      slab=None, v_range=None, materialize: bool = True) -> Optional[Graph]:
@@ -205,7 +211,7 @@ class Context:
         return torch.as_tensor(_DevView(p.value, n.value, "<i4"), device=f"cuda:{self.device}")
 
     def _graph(self, flags: int) -> Graph:
-        if flags & _abi.EG_NO_GRAPH_D2H:
+        if flags & _abi.EG_NO_GRAPH_D2H and not getattr(self, "_fetch", False):
             return Graph(np.zeros(0, np.int64), np.zeros(0, np.int64), np.zeros(0, np.int32),
                          np.zeros((0, 3), np.int64), self.labels().clone())
         if flags & _abi.EG_GRAPH32:      # 32-bit ids on the host (widened here, outside the library)

@@ -141,6 +141,7 @@ struct eg_ctx {
     bool paths_valid = false;
     int64_t n_max = 0, n_sad = 0, n_arc = 0, n_raw = 0, n_own = 0;
     bool have_graph = false, have_labels = false, graph_on_host = false, raw_valid = false;
+    bool graph_deferred = false, deferred_raw = false;   // EG_NO_GRAPH_D2H on one process: copied on request
     const int32_t *d_labels = nullptr;
     eg_stats stats{};
     cudaEvent_t ev[8] = {};
@@ -1212,6 +1213,7 @@ static eg_status compute_impl(eg_ctx *c, const eg_domain *d, const float *f, uin
     if (c->poisoned)
         return set_err(c, EG_ERR_STATE, "context is poisoned by an earlier CUDA/NCCL error: %s", c->err.c_str());
     c->have_graph = c->have_labels = c->graph_on_host = false;
+    c->graph_deferred = false;
     if (c->d2h) CK(cudaStreamSynchronize(c->d2h));   // no copy of an earlier call still in flight
     Problem P;
     ST(validate(c, d, f, device_field, &P));
@@ -1319,6 +1321,11 @@ static eg_status compute_impl(eg_ctx *c, const eg_domain *d, const float *f, uin
     if (!(flags & EG_NO_GRAPH_D2H)) {
         ST(gather_graph(c, (flags & EG_RAW_ARCS) != 0));
         c->graph_on_host = true;
+    } else if (c->world == 1) {
+        // the graph stays in HBM (ctx-owned device arrays, valid until the next
+        // compute); eg_get_graph* copies it to the host on the first request
+        c->graph_deferred = true;
+        c->deferred_raw = (flags & EG_RAW_ARCS) != 0;
     }
     if (c->gstream != c->stream) {             // join the graph stage (aux) into the ctx stream
         CK(cudaEventRecord(c->ev_graph, c->gstream));
@@ -1677,9 +1684,20 @@ static eg_status host_graph_width(eg_ctx *c, bool want64) {
     return EG_OK;
 }
 
+// EG_NO_GRAPH_D2H on one process: the first host request copies the graph
+static eg_status fetch_deferred_graph(eg_ctx *c) {
+    if (!c->have_graph || c->graph_on_host || !c->graph_deferred) return EG_OK;
+    ST(gather_graph(c, c->deferred_raw));
+    CK(cudaStreamSynchronize(c->gstream));
+    CK(cudaStreamSynchronize(c->stream));
+    c->graph_on_host = true;
+    return EG_OK;
+}
+
 eg_status eg_get_graph32(eg_ctx *c, eg_graph32 *out) {
     if (!c || !out) return EG_ERR_INVALID_ARG;
     if (c->poisoned) return set_err(c, EG_ERR_STATE, "context is poisoned: %s", c->err.c_str());
+    ST(fetch_deferred_graph(c));
     if (!c->have_graph || !c->graph_on_host) return set_err(c, EG_ERR_STATE, "no graph on the host (call eg_compute)");
     ST(host_graph_width(c, false));
     out->n_max = c->n_max;
@@ -1697,6 +1715,7 @@ eg_status eg_get_graph32(eg_ctx *c, eg_graph32 *out) {
 eg_status eg_get_graph(eg_ctx *c, eg_graph *out) {
     if (!c || !out) return EG_ERR_INVALID_ARG;
     if (c->poisoned) return set_err(c, EG_ERR_STATE, "context is poisoned: %s", c->err.c_str());
+    ST(fetch_deferred_graph(c));
     if (!c->have_graph || !c->graph_on_host) return set_err(c, EG_ERR_STATE, "no graph on the host (call eg_compute)");
     ST(host_graph_width(c, true));
     out->n_max = c->n_max;
@@ -1713,6 +1732,7 @@ eg_status eg_get_graph(eg_ctx *c, eg_graph *out) {
 
 eg_status eg_get_raw_arcs(eg_ctx *c, int64_t *n, const int64_t **s, const int64_t **rep, const int64_t **m) {
     if (!c || !n || !s || !rep || !m) return EG_ERR_INVALID_ARG;
+    ST(fetch_deferred_graph(c));
     if (!c->have_graph || !c->raw_valid || !c->graph_on_host)
         return set_err(c, EG_ERR_STATE, "raw arcs need eg_compute with EG_RAW_ARCS");
     *n = c->n_raw;

@@ -796,3 +796,39 @@ def test_rank_dtype_beyond_2p24(eg, ctx):
         b = ctx.compute(t.cuda(), dims=dims)
         assert_graph_equal(b, a, labels=False, what=f"rank image {t.dtype}")
         assert np.array_equal(b.labels.cpu().numpy(), la)
+
+
+def test_deferred_graph(eg, ctx):
+    """EG_NO_GRAPH_D2H: the graph stays in HBM after eg_compute and the first
+    eg_get_graph / eg_get_graph32 / eg_get_raw_arcs copies it (one process) --
+    the same graph as an eager compute, on the tiled, generic and CSR paths."""
+    import torch
+    f, dims = G.c2_gaussians_noise(n=48, seed=5, k=6)
+    o = O.grid(f, dims)
+    t = torch.from_numpy(f).cuda()
+    for extra in (0, eg.EG_GRAPH32, eg.EG_FORCE_GENERIC, eg.EG_RAW_ARCS, eg.EG_VIRTUAL_PARTS(2)):
+        g0 = ctx.compute(t, dims=dims, flags=eg.EG_NO_GRAPH_D2H | extra)
+        assert len(g0.arcs) == 0                  # nothing copied by compute itself
+        g = ctx.graph()
+        assert_graph_equal(g, o, raw=bool(extra & eg.EG_RAW_ARCS), what=f"deferred {extra}")
+        assert_graph_equal(ctx.graph(), o, what=f"deferred {extra} (second request)")
+    X, fc = G.gmm_points(4000, seed=4)
+    rp, ci = G.knn_csr(X, 10)
+    csr = (torch.from_numpy(rp).cuda(), torch.from_numpy(ci).cuda())
+    ctx.compute(torch.from_numpy(fc).cuda(), csr=csr, flags=eg.EG_NO_GRAPH_D2H | eg.EG_GRAPH32)
+    assert_graph_equal(ctx.graph(), O.csr(fc, rp, ci), what="deferred csr")
+
+
+@pytest.mark.parametrize("split", ["0", "2", "3"])
+@pytest.mark.parametrize("dims", [[64, 48, 80], [40, 37, 70], [33, 17, 33]])
+def test_face_split_label_pass(eg, ctx, split, dims, monkeypatch):
+    """The one-slab label pass split by tile faces (EG_FIN_SPLIT: one pass /
+    z-face planes then the rest / z faces, y faces, rest): several tile layers
+    in z and y, ragged last tiles, a turbulence field whose paths cross many
+    tiles -- identical to the oracle either way."""
+    import torch
+    monkeypatch.setenv("EG_FIN_SPLIT", split)
+    t3, d3 = G.turbulence(max(dims), seed=11, device="cpu", kc_div=8)
+    f = t3.numpy().reshape(max(dims), max(dims), max(dims))[:dims[2], :dims[1], :dims[0]].ravel().copy()
+    o = O.grid(f, dims)
+    assert_graph_equal(ctx.compute(torch.from_numpy(f).cuda(), dims=dims), o, what=f"split {split} {dims}")
