@@ -6,6 +6,7 @@
 // row range of a row_ptr-indexed buffer), so S4 only gathers their labels.
 // One warp per vertex (k_classify_csr); no degree cap.
 #include <algorithm>
+#include <cstdlib>
 
 #include "eg_impl.h"
 
@@ -376,6 +377,322 @@ __global__ void __launch_bounds__(32 * kCsrWarps) k_csr_link(
     }
 }
 
+// k_csr_link_flat: the same S3 with the link-edge search flattened over the
+// warp.  The hash-set walk above gives lane p the whole list U(a_p) (about 11
+// entries on C5) while lanes p >= |U| idle and every probe loop diverges: 820
+// warp instructions per vertex at 15.7 active lanes (ncu, round 2).  Here the
+// |U(a_p)| entries of all positions p are numbered t = 0 .. T-1 (warp prefix
+// sum of the lengths), lane l takes t = l, l + 32, ...: the owner p of t is a
+// branch-free binary search over the prefix sums, b = U(a_p)[t - off_p] one
+// load, and b's position in the ascending U(v) a second binary search (5-6
+// fixed steps, no divergence); a hit sets bit q of adj[p] by a shared-memory
+// atomicOr.  Components, UpperLinkReps and the outputs are those of
+// k_csr_link.
+constexpr int kFlatMax = 64;
+constexpr int kFlatHash = 256;          // direct-mapped id -> position table (|U| <= 32)
+struct __align__(16) CsrFlatSmem {
+    int32_t hkey[kFlatHash];        // U(v) member with this slot, -1 = empty
+    uint32_t adj32[32];
+    int32_t owner[32];              // rank among the nonempty positions -> position
+    unsigned long long adj[kFlatMax];
+    int64_t sa[kFlatMax];          // upl offset of U(a_p)
+    int32_t su[kFlatMax];          // U(v), ascending ids
+    int32_t off[kFlatMax];         // exclusive prefix sums of |U(a_p)|
+    int32_t rep[kFlatMax];
+};
+
+// largest i < n with a[i] <= x, given a[0] <= x or returning 0 (a ascending, n <= 64)
+__device__ __forceinline__ int bsearch_le(const int32_t *a, int n, int32_t x) {
+    int lo = 0;
+#pragma unroll
+    for (int step = 32; step >= 1; step >>= 1) {
+        const int m = lo + step;
+        if (m < n && a[m] <= x) lo = m;
+    }
+    return lo;
+}
+
+__global__ void __launch_bounds__(32 * kCsrWarps) k_csr_link_flat(
+    const int64_t *__restrict__ rp, const int32_t *__restrict__ ci, const float *__restrict__ f, int64_t v0,
+    int64_t v1, const int32_t *__restrict__ upl, const int32_t *__restrict__ nup, uint32_t *sad_bits,
+    uint8_t *beta_out, int32_t *rep_buf, int32_t *slow_p) {
+    __shared__ CsrFlatSmem sm_all[kCsrWarps];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    CsrFlatSmem &sm = sm_all[wib];
+    const int64_t n = v1 - v0, words = (n + 31) / 32;
+    const uint32_t lt = (1u << lane) - 1u;
+    for (int64_t w = int64_t(blockIdx.x) * kCsrWarps + wib; w < words; w += int64_t(gridDim.x) * kCsrWarps) {
+        const int jn = n - w * 32 < 32 ? int(n - w * 32) : 32;
+        const int my_nu = lane < jn ? nup[v0 + w * 32 + lane] : 0;
+        int my_beta = my_nu < 2 ? my_nu : 0;            // 0: maximum, 1: regular
+        const int64_t my_b0 = lane < jn ? rp[v0 + w * 32 + lane] : 0;
+        uint32_t todo = __ballot_sync(0xffffffffu, my_nu >= 2);
+        // software pipeline over the word's vertices: the next vertex's U(v)
+        // entries are loaded when the current one starts, their rows / values
+        // while its link edges are searched (three dependent gathers per vertex
+        // otherwise serialise with its compute)
+        int32_t nx_u = -1;
+        int64_t nx_s = 0;
+        int nx_l = 0;
+        float nx_f = 0.f;
+        auto fetch_u = [&](uint32_t td) {
+            nx_u = -1;
+            if (!td) return;
+            const int jj = __ffs(td) - 1;
+            const int nn = __shfl_sync(0xffffffffu, my_nu, jj);
+            const int64_t bb = __shfl_sync(0xffffffffu, my_b0, jj);
+            if (lane < nn) nx_u = upl[bb + lane];
+        };
+        auto fetch_rows = [&]() {
+            if (nx_u >= 0) {
+                nx_s = rp[nx_u];
+                nx_l = nup[nx_u];
+                nx_f = __ldg(f + nx_u);
+            }
+        };
+        fetch_u(todo);
+        fetch_rows();
+        while (todo) {
+            const int j = __ffs(todo) - 1;
+            todo &= todo - 1;
+            const int nu = __shfl_sync(0xffffffffu, my_nu, j);
+            const int64_t b0 = __shfl_sync(0xffffffffu, my_b0, j);
+            const int32_t *U = upl + b0;
+            const int32_t cu = nx_u;
+            const int64_t cs = nx_s;
+            const int cl = nx_l;
+            const float cf = nx_f;
+            fetch_u(todo);
+            int beta = 0;
+            if (nu <= 32) {
+                // |U| <= 32 (almost every vertex of a kNN graph): position p = lane.
+                // U(v) goes into a direct-mapped table (slot = id hash, 8 bits);
+                // when two members share a slot the vertex takes the binary
+                // searches of the general path below instead.
+                const bool mine = lane < nu;
+                const int32_t uA = cu;
+                const int lA = mine ? cl : 0;
+                const int64_t sA = mine ? cs : 0;
+                const uint32_t kA = mine ? fkey(cf) : 0u;
+                const uint32_t slot = (uint32_t(uA) * 2654435761u) >> 24;
+                reinterpret_cast<int4 *>(sm.hkey)[lane] = make_int4(-1, -1, -1, -1);
+                reinterpret_cast<int4 *>(sm.hkey)[lane + 32] = make_int4(-1, -1, -1, -1);
+                const uint32_t same = __match_any_sync(0xffffffffu, mine ? slot : 0x100u + lane);
+                const bool clash = __any_sync(0xffffffffu, mine && __popc(same) > 1);
+                int iA = lA;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const int y = __shfl_up_sync(0xffffffffu, iA, o);
+                    if (lane >= o) iA += y;
+                }
+                const int T = __shfl_sync(0xffffffffu, iA, 31);
+                const int offA = iA - lA;
+                const uint32_t ne = __ballot_sync(0xffffffffu, lA > 0);
+                __syncwarp();
+                if (mine) {
+                    sm.su[lane] = uA;
+                    sm.off[lane] = offA;
+                    sm.sa[lane] = sA;
+                    if (!clash) sm.hkey[slot] = lane;    // the member's position (its id is sm.su[pos])
+                }
+                if (lA > 0) sm.owner[__popc(ne & lt)] = lane;
+                sm.adj32[lane] = 0u;
+                __syncwarp();
+                // windows of 32 entries: the owner of entry t0 + l is the last
+                // nonempty position starting at or before it (starts are distinct)
+                // up to four windows per batch: every gather of the batch is in
+                // flight before the first lookup
+                for (int t00 = 0; t00 < T; t00 += 128) {
+                    int32_t bb[4];
+                    int pp[4];
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        const int t0 = t00 + 32 * k;
+                        const bool st = lA > 0 && offA >= t0 && offA < t0 + 32;
+                        const uint32_t S = __reduce_or_sync(0xffffffffu, st ? 1u << (offA - t0) : 0u);
+                        const int base = __popc(__ballot_sync(0xffffffffu, lA > 0 && offA < t0));
+                        const int t = t0 + lane;
+                        pp[k] = -1;
+                        bb[k] = -1;
+                        if (t < T) {
+                            const int p = sm.owner[base - 1 + __popc(S & (0xffffffffu >> (31 - lane)))];
+                            pp[k] = p;
+                            bb[k] = upl[sm.sa[p] + (t - sm.off[p])];
+                        }
+                    }
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        if (pp[k] < 0) continue;
+                        const int32_t b = bb[k];
+                        int q;
+                        bool hit;
+                        if (!clash) {
+                            q = sm.hkey[(uint32_t(b) * 2654435761u) >> 24];
+                            hit = q >= 0 && sm.su[q] == b;
+                        } else {
+                            q = bsearch_le(sm.su, nu, b);
+                            hit = sm.su[q] == b;
+                        }
+                        if (hit) atomicOr(&sm.adj32[pp[k]], 1u << q);
+                    }
+                }
+                fetch_rows();
+                __syncwarp();
+                const uint32_t adj = sm.adj32[lane];
+                const uint32_t all = nu == 32 ? 0xffffffffu : ((1u << nu) - 1u);
+                uint32_t seen = 0u;
+                int32_t my_rep = -1;
+                while (seen != all) {
+                    uint32_t comp = (all & ~seen) & (0u - (all & ~seen));
+                    for (;;) {
+                        const bool in = (comp >> lane) & 1u;
+                        const uint32_t fw = __reduce_or_sync(0xffffffffu, in ? adj : 0u);
+                        const uint32_t bw = __ballot_sync(0xffffffffu, (adj & comp) != 0u);
+                        const uint32_t nc = (comp | fw | bw) & all;
+                        if (nc == comp) break;
+                        comp = nc;
+                    }
+                    const bool in = (comp >> lane) & 1u;
+                    const uint32_t kmax = __reduce_max_sync(0xffffffffu, in ? kA : 0u);
+                    const int32_t rv = __reduce_max_sync(0xffffffffu, (in && kA == kmax) ? uA : -1);
+                    if (lane == beta) my_rep = rv;
+                    ++beta;
+                    seen |= comp;
+                }
+                if (beta >= 2 && rep_buf) {
+                    int rank = 0;
+                    for (int k = 0; k < beta; ++k) rank += __shfl_sync(0xffffffffu, my_rep, k) < my_rep;
+                    if (lane < beta) rep_buf[b0 + rank] = my_rep;
+                }
+                __syncwarp();
+            } else if (nu <= kFlatMax) {
+                // positions lane and lane + 32: a, its upper list, its key
+                const int pb = lane + 32;
+                const int32_t uA = lane < nu ? U[lane] : -1, uB = pb < nu ? U[pb] : -1;
+                int lA = 0, lB = 0;
+                int64_t sA = 0, sB = 0;
+                if (uA >= 0) {
+                    sA = rp[uA];
+                    lA = nup[uA];
+                }
+                if (uB >= 0) {
+                    sB = rp[uB];
+                    lB = nup[uB];
+                }
+                const uint32_t kA = uA >= 0 ? fkey(__ldg(f + uA)) : 0u, kB = uB >= 0 ? fkey(__ldg(f + uB)) : 0u;
+                // exclusive prefix sums of the lengths over positions 0 .. nu-1
+                int iA = lA, iB = lB;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const int yA = __shfl_up_sync(0xffffffffu, iA, o), yB = __shfl_up_sync(0xffffffffu, iB, o);
+                    if (lane >= o) {
+                        iA += yA;
+                        iB += yB;
+                    }
+                }
+                const int totA = __shfl_sync(0xffffffffu, iA, 31), totB = __shfl_sync(0xffffffffu, iB, 31);
+                const int T = totA + totB;
+                if (lane < nu) {
+                    sm.su[lane] = uA;
+                    sm.off[lane] = iA - lA;
+                    sm.sa[lane] = sA;
+                }
+                if (pb < nu) {
+                    sm.su[pb] = uB;
+                    sm.off[pb] = totA + iB - lB;
+                    sm.sa[pb] = sB;
+                }
+                sm.adj[lane] = 0ull;
+                sm.adj[pb] = 0ull;
+                __syncwarp();
+                // link edges {a_p, b}: b in U(a_p) and b in U(v), one entry per lane
+                for (int t = lane; t < T; t += 32) {
+                    const int p = bsearch_le(sm.off, nu, t);
+                    const int32_t b = upl[sm.sa[p] + (t - sm.off[p])];
+                    const int q = bsearch_le(sm.su, nu, b);
+                    if (sm.su[q] == b) atomicOr(&sm.adj[p], 1ull << q);
+                }
+                __syncwarp();
+                if (nu <= 32) {
+                    const uint32_t adj = uint32_t(sm.adj[lane]);
+                    const uint32_t all = nu == 32 ? 0xffffffffu : ((1u << nu) - 1u);
+                    uint32_t seen = 0u;
+                    int32_t my_rep = -1;
+                    while (seen != all) {
+                        uint32_t comp = (all & ~seen) & (0u - (all & ~seen));
+                        for (;;) {
+                            const bool in = (comp >> lane) & 1u;
+                            const uint32_t fw = __reduce_or_sync(0xffffffffu, in ? adj : 0u);
+                            const uint32_t bw = __ballot_sync(0xffffffffu, (adj & comp) != 0u);
+                            const uint32_t nc = (comp | fw | bw) & all;
+                            if (nc == comp) break;
+                            comp = nc;
+                        }
+                        const bool in = (comp >> lane) & 1u;
+                        const uint32_t kmax = __reduce_max_sync(0xffffffffu, in ? kA : 0u);
+                        const int32_t rv = __reduce_max_sync(0xffffffffu, (in && kA == kmax) ? uA : -1);
+                        if (lane == beta) my_rep = rv;
+                        ++beta;
+                        seen |= comp;
+                    }
+                    if (beta >= 2 && rep_buf) {
+                        int rank = 0;
+                        for (int k = 0; k < beta; ++k) rank += __shfl_sync(0xffffffffu, my_rep, k) < my_rep;
+                        if (lane < beta) rep_buf[b0 + rank] = my_rep;
+                    }
+                } else {
+                    const unsigned long long adjA = sm.adj[lane], adjB = sm.adj[pb];
+                    const unsigned long long all = nu == 64 ? ~0ull : ((1ull << nu) - 1ull);
+                    unsigned long long seen = 0ull;
+                    while (seen != all) {
+                        unsigned long long comp = 1ull << (__ffsll((long long)(all & ~seen)) - 1);
+                        for (;;) {
+                            const bool inA = (comp >> lane) & 1ull, inB = (comp >> pb) & 1ull;
+                            const unsigned long long c = (inA ? adjA : 0ull) | (inB ? adjB : 0ull);
+                            const unsigned lo32 = __reduce_or_sync(0xffffffffu, unsigned(c));
+                            const unsigned hi32 = __reduce_or_sync(0xffffffffu, unsigned(c >> 32));
+                            const unsigned bA = __ballot_sync(0xffffffffu, (adjA & comp) != 0ull);
+                            const unsigned bBk = __ballot_sync(0xffffffffu, (adjB & comp) != 0ull);
+                            const unsigned long long nc =
+                                (comp | ((unsigned long long)(hi32 | bBk) << 32) | (lo32 | bA)) & all;
+                            if (nc == comp) break;
+                            comp = nc;
+                        }
+                        const bool inA = (comp >> lane) & 1ull, inB = (comp >> pb) & 1ull;
+                        const uint32_t kk = max(inA ? kA : 0u, inB ? kB : 0u);
+                        const uint32_t kmax = __reduce_max_sync(0xffffffffu, kk);
+                        const int32_t cand = max((inA && kA == kmax) ? uA : -1, (inB && kB == kmax) ? uB : -1);
+                        const int32_t rv = __reduce_max_sync(0xffffffffu, cand);
+                        if (lane == 0) sm.rep[beta] = rv;
+                        ++beta;
+                        seen |= comp;
+                    }
+                    __syncwarp();
+                    if (beta >= 2 && rep_buf) {
+                        for (int k = lane; k < beta; k += 32) {
+                            const int32_t r = sm.rep[k];
+                            int rank = 0;
+                            for (int j2 = 0; j2 < beta; ++j2) rank += sm.rep[j2] < r;
+                            rep_buf[b0 + rank] = r;
+                        }
+                    }
+                }
+                __syncwarp();
+            } else {
+                // no degree cap: lane 0 finishes serially over the merged full rows
+                if (lane == 0)
+                    beta = csr_slow_components(rp, ci, f, U, slow_p + b0, nu, rep_buf ? rep_buf + b0 : nullptr);
+                beta = __shfl_sync(0xffffffffu, beta, 0);
+            }
+            if (nu > 32) fetch_rows();
+            if (lane == j) my_beta = beta;
+        }
+        const uint32_t sb = __ballot_sync(0xffffffffu, my_beta >= 2);
+        if (lane < jn && beta_out) beta_out[w * 32 + lane] = uint8_t(my_beta > 255 ? 255 : my_beta);
+        if (lane == 0) sad_bits[w] = sb;
+    }
+}
+
 // EG_CHECK_CSR: row_ptr[0] = 0, monotone, row_ptr[N] = nnz;
 // 0 <= col_idx < N; every row strictly ascending (sorted, no duplicates); no
 // self loops; symmetric (u in N(v) => v in N(u), by binary search).  Reading
@@ -528,8 +845,13 @@ cudaError_t launch_csr_link(const int64_t *row_ptr, const int32_t *col_idx, cons
                             const int32_t *upl, const int32_t *nup, uint32_t *sad_bits, uint8_t *beta_out,
                             int32_t *rep_buf, int32_t *par, cudaStream_t st) {
     if (v1 <= v0) return cudaSuccess;
-    k_csr_link<<<csr_blocks(v1 - v0), 32 * kCsrWarps, 0, st>>>(row_ptr, col_idx, f, v0, v1, upl, nup, sad_bits,
-                                                                beta_out, rep_buf, par);
+    const char *ev = std::getenv("EG_CSR_LINK");   // tuning knob: 1 = the hash-set walk (k_csr_link)
+    if (ev && std::atoi(ev) == 1)
+        k_csr_link<<<csr_blocks(v1 - v0), 32 * kCsrWarps, 0, st>>>(row_ptr, col_idx, f, v0, v1, upl, nup, sad_bits,
+                                                                    beta_out, rep_buf, par);
+    else
+        k_csr_link_flat<<<csr_blocks(v1 - v0), 32 * kCsrWarps, 0, st>>>(row_ptr, col_idx, f, v0, v1, upl, nup,
+                                                                         sad_bits, beta_out, rep_buf, par);
     return cudaGetLastError();
 }
 
