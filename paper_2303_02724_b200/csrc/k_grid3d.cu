@@ -252,9 +252,12 @@ __device__ __forceinline__ void load_plane(float *fbox, int bz, const float *src
 // (the shell is never written afterwards), and the next tile's field box is
 // requested by TMA as soon as S1 has consumed the current one, so the copy
 // runs behind S2 and the label stores.
-template <bool kInterior, bool kPersist, bool kStats = false>
+// kNoE: the launch has no exit list (A.no_elist known at compile time: the
+// exit-mark stores and their flag test leave the output loop)
+template <bool kInterior, bool kPersist, bool kStats = false, bool kNoE = false>
 __global__ void __launch_bounds__(kThreads, 2)
     k_tile(const __grid_constant__ CUtensorMap tmap, TileArgs A, Dims3 D) {
+    const bool no_elist = kNoE || A.no_elist;
     extern __shared__ __align__(128) unsigned char smem[];
     float *fbox = reinterpret_cast<float *>(smem);
     unsigned char *pb = smem + kOffP;
@@ -485,7 +488,7 @@ __global__ void __launch_bounds__(kThreads, 2)
     // so nothing needs settling, and chains that run into a finished cell end
     // one hop later.
     uint8_t *used = reinterpret_cast<uint8_t *>(fbox);
-    if (!A.no_elist)   // exit marks are only read back when the tile appends to E
+    if (!no_elist)   // exit marks are only read back when the tile appends to E
         for (int i = tid; i < 2 * PBOX / 16; i += kThreads) reinterpret_cast<uint4 *>(used)[i] = make_uint4(0, 0, 0, 0);
 #pragma unroll 1
     for (int round = 0; round < A.rounds; ++round) {
@@ -529,7 +532,7 @@ __global__ void __launch_bounds__(kThreads, 2)
         const int32_t root = g_box0 + bz * nxy + (t & 0x7fffffff);
         if (kInterior || ok) {
             A.label[i_col + z * nxy] = exit ? int32_t(uint32_t(root) | kFlag) : root;
-            if (exit && !A.no_elist) used[r] = 1;
+            if (exit && !no_elist) used[r] = 1;
             if (kStats) n_exit += exit;
         }
     }
@@ -565,7 +568,7 @@ __global__ void __launch_bounds__(kThreads, 2)
                 if (js < (unsigned long long)A.list_cap) A.sad_list[js] = g0 + (__ffs(m) - 1) * nxy;
         }
     }
-    if (A.no_elist) {
+    if (no_elist) {
         if (kPersist) __syncthreads();   // the next tile's S1 rewrites the pointer box
         continue;
     }
@@ -742,7 +745,7 @@ static eg_status pipeline_chunks(Tiled3D *t, const TileArgs &A, const CUtensorMa
         Ak.origin.z = l0;
         Ak.n_tiles = int32_t(int64_t(A.tiles_x) * A.tiles_y * (l1 - l0));
         if ((e = cudaStreamWaitEvent(st, evH[k], 0)) != cudaSuccess) return fail(err, e, "H2D wait");
-        k_tile<true, false><<<unsigned(Ak.n_tiles), kThreads, kTileSmem, st>>>(tmap, Ak, D);
+        k_tile<true, false, false, true><<<unsigned(Ak.n_tiles), kThreads, kTileSmem, st>>>(tmap, Ak, D);
         stats->kernel_launches += 1;
         if ((e = cudaGetLastError()) != cudaSuccess) return fail(err, e, "k_tile<interior> chunk");
         if ((e = cudaEventRecord(evT[k], st)) != cudaSuccess) return fail(err, e, "tile chunk event");
@@ -815,6 +818,8 @@ eg_status tiled3d_local(Tiled3D *t, int ndim, const int64_t *dims, const Slab &s
             (e = cudaFuncSetAttribute(k_tile<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       int(kTileSmem))) != cudaSuccess ||
             (e = cudaFuncSetAttribute(k_tile<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      int(kTileSmem))) != cudaSuccess ||
+            (e = cudaFuncSetAttribute(k_tile<true, false, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       int(kTileSmem))) != cudaSuccess ||
             (e = cudaFuncSetAttribute(k_tile<true, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       int(kTileSmem))) != cudaSuccess ||
@@ -1008,7 +1013,10 @@ eg_status tiled3d_local(Tiled3D *t, int ndim, const int64_t *dims, const Slab &s
             else if (A.exit_count)
                 k_tile<true, false, true><<<unsigned(nt), kThreads, kTileSmem, st>>>(tmap, A, D);
             else
-                k_tile<true, false><<<unsigned(nt), kThreads, kTileSmem, st>>>(tmap, A, D);
+                if (A.no_elist)
+                    k_tile<true, false, false, true><<<unsigned(nt), kThreads, kTileSmem, st>>>(tmap, A, D);
+                else
+                    k_tile<true, false><<<unsigned(nt), kThreads, kTileSmem, st>>>(tmap, A, D);
             stats->kernel_launches += 1;
             if ((e = cudaGetLastError()) != cudaSuccess) return fail(err, e, "k_tile<interior>");
         }
