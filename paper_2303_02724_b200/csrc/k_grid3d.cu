@@ -75,6 +75,7 @@ static_assert(TZ == 16, "saddle / maximum column masks pack into one 32-bit word
 
 struct Tiled3D {
     uint32_t *d_lut = nullptr;
+    unsigned char *d_tmpl = nullptr;                 // pointer-box image (shell cells self-pointing) + LUT, smem layout
     uint16_t *d_shell = nullptr;                     // pointer-box index of every shell cell
     bool ready = false;
     int64_t bdims[3] = {0, 0, 0};
@@ -114,6 +115,7 @@ Tiled3D *tiled3d_create() { return new Tiled3D(); }
 void tiled3d_destroy(Tiled3D *t) {
     if (!t) return;
     if (t->d_lut) cudaFree(t->d_lut);
+    if (t->d_tmpl) cudaFree(t->d_tmpl);
     if (t->d_shell) cudaFree(t->d_shell);
     if (t->d_btiles) cudaFree(t->d_btiles);
     if (t->d_ptab) cudaFree(t->d_ptab);
@@ -146,6 +148,7 @@ struct TileArgs {
     unsigned long long *ecount;     // [0] exit targets, [1] maxima, [2] saddles
     int64_t ecap;
     const uint32_t *lut;
+    const unsigned char *tmpl;      // TMA launches: pointer-box template + LUT, bulk-copied at the tile start
     const int32_t *ptab;            // per box-plane cell: by * nx + bx, bit 31 = in-plane shell
     const uint16_t *shell;          // kShell pointer-box byte offsets
     const int32_t *btiles;          // boundary variant: packed tile ids
@@ -193,6 +196,14 @@ __device__ __forceinline__ void tma_load_3d(void *dst, const CUtensorMap *map, u
         "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];"
         ::"r"(smem_u32(dst)), "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar))
         : "memory");
+}
+
+// one bulk copy global -> shared (16-byte aligned, size a multiple of 16),
+// completing on the mbarrier like the tensor copy
+__device__ __forceinline__ void bulk_load(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(smem_u32(dst)), "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
 }
 
 // ------------------------------------------------------------ the tile kernel
@@ -292,11 +303,20 @@ __global__ void __launch_bounds__(kThreads, 2)
             bzo = packed >> 20;
         }
     };
-    auto issue_tma = [&](int t) {      // thread 0: request tile t's field box
+    // thread 0: request tile t's field box; with `tables` also the pointer-box
+    // template (shell cells point to themselves, P:296 partial-path ends), the
+    // LUT and the plane table -- three bulk copies instead of per-thread loops
+    constexpr uint32_t kTmplBytes = uint32_t(kOffM - kOffP), kPtabBytes = uint32_t(PL * 4);
+    static_assert(kTmplBytes % 16 == 0 && kPtabBytes % 16 == 0 && kOffP % 16 == 0 && kOffT % 16 == 0, "bulk copy");
+    auto issue_tma = [&](int t, bool tables) {
         int bx, by, bz;
         coords(t, bx, by, bz);
-        mbar_expect_tx(bar, uint32_t(BOX * 4));
+        mbar_expect_tx(bar, uint32_t(BOX * 4) + (tables ? kTmplBytes + kPtabBytes : 0u));
         tma_load_3d(fbox, &tmap, bar, bx * TX - XO, by * TY - 1, A.z_lo + bz * TZ - 1 - A.z_lo);
+        if (tables) {
+            bulk_load(pb, A.tmpl, kTmplBytes, bar);
+            bulk_load(ptab, A.ptab, kPtabBytes, bar);
+        }
     };
     if (A.tma) {
         if (tid == 0) {
@@ -304,15 +324,16 @@ __global__ void __launch_bounds__(kThreads, 2)
             asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         }
         __syncthreads();
-        if (tid == 0) issue_tma(blockIdx.x);
+        if (tid == 0) issue_tma(blockIdx.x, true);
+    } else {
+        // shell cells of the pointer box are terminal (point to themselves)
+        for (int s = tid; s < kShell; s += kThreads) {
+            const int i = __ldg(A.shell + s);
+            P(i) = uint16_t(i);
+        }
+        for (int i = tid; i < kLutWords; i += kThreads) lut[i] = __ldg(A.lut + i);
+        for (int i = tid; i < PL; i += kThreads) ptab[i] = __ldg(A.ptab + i);
     }
-    // shell cells of the pointer box are terminal (point to themselves)
-    for (int s = tid; s < kShell; s += kThreads) {
-        const int i = __ldg(A.shell + s);
-        P(i) = uint16_t(i);
-    }
-    for (int i = tid; i < kLutWords; i += kThreads) lut[i] = __ldg(A.lut + i);
-    for (int i = tid; i < PL; i += kThreads) ptab[i] = __ldg(A.ptab + i);
     const int t_end = kPersist ? A.n_tiles : int(blockIdx.x) + 1;
 #pragma unroll 1
     for (int t = blockIdx.x, it = 0; t < t_end; t += gridDim.x, ++it) {
@@ -476,7 +497,7 @@ __global__ void __launch_bounds__(kThreads, 2)
         // the field box is dead (no exit marks on the one-slab path): the
         // next tile's copy overlaps the rest of this one
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        issue_tma(t + int(gridDim.x));
+        issue_tma(t + int(gridDim.x), false);
     }
 
     // ---- S2 inside the tile.  The field box is dead: it now holds one
@@ -808,6 +829,13 @@ eg_status tiled3d_local(Tiled3D *t, int ndim, const int64_t *dims, const Slab &s
             return EG_ERR_STATE;
         }
         if ((e = upload(&t->d_shell, sh)) != cudaSuccess) return fail(err, e, "shell upload");
+        {
+            // smem image [kOffP, kOffM): pointer box with self-pointing shell cells, then the LUT
+            std::vector<unsigned char> img(kOffM - kOffP, 0);
+            for (uint16_t b : sh) std::memcpy(img.data() + b, &b, 2);
+            std::memcpy(img.data() + (kOffL - kOffP), bits.data(), size_t(kLutWords) * 4);
+            if ((e = upload(&t->d_tmpl, img)) != cudaSuccess) return fail(err, e, "template upload");
+        }
         if ((e = cudaMalloc(&t->d_ecount, 4 * sizeof(unsigned long long))) != cudaSuccess)
             return fail(err, e, "cudaMalloc ecount");
         for (auto &ev : t->ev_io)
@@ -948,6 +976,7 @@ eg_status tiled3d_local(Tiled3D *t, int ndim, const int64_t *dims, const Slab &s
         A.ecount = t->d_ecount;
         A.ecap = t->ecap;
         A.lut = t->d_lut;
+        A.tmpl = t->d_tmpl;
         A.ptab = t->d_ptab;
         A.shell = t->d_shell;
         A.btiles = t->d_btiles;
