@@ -4,8 +4,10 @@
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config C3] [--impl ours|reference]
 
 A step is one eg_compute over the resident field: steepest-ascent pointers,
-pointer-jumping labels, saddles, deduplicated arcs, and the graph copied to
-the host (SURVEY 8(d) timed region).  The default workload is C3 (3D 1024^3
+pointer-jumping labels, saddles and deduplicated arcs, with the labels and the
+graph left in HBM (SURVEY 8(d) timed region; graph() copies the graph
+afterwards).  The e2e number runs eg_compute_host from pinned host memory and
+copies the labels and the graph back inside its timing.  The default workload is C3 (3D 1024^3
 turbulence-like float32 field); the other BASELINE configs are parity cases.
 For N > 1 the grid is cut into slabs of the slowest axis, one per rank (CSR:
 vertex ranges), with the halo / boundary-label exchanges over NCCL inside the
