@@ -10,6 +10,9 @@
 // is unresolved; a final pass rewrites every unresolved owned label.  Paths
 // cross a slab boundary only through its two planes, so the exchange is a
 // fixed 2 planes per neighbour per round.
+#include <cstdlib>
+#include <type_traits>
+
 #include "eg_impl.h"
 
 namespace eg {
@@ -194,7 +197,7 @@ __device__ __forceinline__ bool face_pair(int32_t z, int32_t n) {   // z in a pa
     return (r == kFaceT - 1 && z + 1 < n) || (r == 0 && z > 0);
 }
 
-template <bool kStats>
+template <bool kStats, int kW>
 __global__ void __launch_bounds__(128, 16) k_finalize_faces(int32_t *label, int64_t v0, FaceSplit F, int pass,
                                                             unsigned long long *hist) {
     const int64_t plane = int64_t(F.nx) * F.ny;
@@ -274,16 +277,24 @@ cudaError_t launch_finalize_faces(int32_t *label, int64_t v0, int64_t nx, int64_
     const FaceSplit F{int32_t(nx), int32_t(ny), int32_t(planes), ysplit, div_magic(nx), div_magic(2 * nx)};
     const int64_t plane = nx * ny;
     const int64_t zpairs = (planes - 1) / tz, ypair_words = ((ny - 1) / ty) * 2 * nx / 32 + 1;
-    const unsigned per_blk = 4 * kW;
+    const char *kv = std::getenv("EG_FIN_KW");       // tuning knob: words per warp (4, 6, 8, 12)
+    const int kw = kv ? std::atoi(kv) : 6;
     for (int pass = 0; pass < 3; ++pass) {
         const int64_t gy = pass == 0 ? zpairs : planes;
         const int64_t words = pass == 0 ? (2 * plane + 31) / 32 : pass == 1 ? ypair_words : (plane + 31) / 32;
         if (gy <= 0 || (pass == 1 && (ny <= ty || !ysplit))) continue;
-        const dim3 grid(unsigned((words + per_blk - 1) / per_blk), unsigned(gy));
-        if (hist)
-            k_finalize_faces<true><<<grid, 128, 0, st>>>(label, v0, F, pass, hist);
-        else
-            k_finalize_faces<false><<<grid, 128, 0, st>>>(label, v0, F, pass, nullptr);
+        auto go = [&](auto kwc) {
+            constexpr int K = decltype(kwc)::value;
+            const dim3 grid(unsigned((words + 4 * K - 1) / (4 * K)), unsigned(gy));
+            if (hist)
+                k_finalize_faces<true, K><<<grid, 128, 0, st>>>(label, v0, F, pass, hist);
+            else
+                k_finalize_faces<false, K><<<grid, 128, 0, st>>>(label, v0, F, pass, nullptr);
+        };
+        if (kw == 4) go(std::integral_constant<int, 4>{});
+        else if (kw == 8) go(std::integral_constant<int, 8>{});
+        else if (kw == 12) go(std::integral_constant<int, 12>{});
+        else go(std::integral_constant<int, 6>{});
         cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) return e;
     }
