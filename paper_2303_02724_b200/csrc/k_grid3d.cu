@@ -54,10 +54,10 @@ constexpr int kLutWords = (1 << 14) / 16;            // 2 bits per 14-bit upper 
 constexpr uint32_t kFlag = 0x80000000u;              // label bit 31: exit (not yet final)
 constexpr int kMaxChunks = 32;                       // z-chunks of the eg_compute_host pipeline
 #ifndef EG_S1_UNROLL
-#define EG_S1_UNROLL 4
+#define EG_S1_UNROLL 16
 #endif
 #ifndef EG_OUT_UNROLL
-#define EG_OUT_UNROLL 4
+#define EG_OUT_UNROLL 16
 #endif
 constexpr int kS1Unroll = EG_S1_UNROLL, kOutUnroll = EG_OUT_UNROLL;   // z-loop unrolling (tuned on C3)
 // the halo shell of a box (the cells a path can exit to): both z faces, and
@@ -444,6 +444,10 @@ __global__ void __launch_bounds__(kThreads, 2)
     };
 
     float pm[7], p0[7], pp[7];
+    // the column's own pointer-box cells are written only by this thread, so
+    // their values are also kept in registers (the z loops are fully unrolled):
+    // the doubling rounds and the chase start skip the own-cell loads
+    uint32_t own[TZ];
     star(0, pm);
     star(1, p0);
     VK bm_prev = bminus(pm, -1);       // B-(z-1) for z = 0
@@ -483,7 +487,8 @@ __global__ void __launch_bounds__(kThreads, 2)
         // (every compare false) terminal, so no pointer cycle can form
         d = mask ? d : 0;
         const int c = cfb + 2 * (z + 1) * PS;
-        P(c) = uint16_t(kInterior || ok ? c + d : c);
+        own[z] = uint32_t(kInterior || ok ? c + d : c);
+        P(c) = uint16_t(own[z]);
         // 2-bit class code from the LUT: bit 0 saddle (beta0+ >= 2), bit 1
         // maximum (empty mask); interleaved, vertex z at bits 2z, 2z + 1
         const uint32_t code = (lut[mask >> 4] >> ((mask & 15) << 1)) & 3u;
@@ -533,7 +538,8 @@ __global__ void __launch_bounds__(kThreads, 2)
 #pragma unroll
         for (int z = 0; z < TZ; ++z) {
             const int c = cfb + 2 * (z + 1) * PS;
-            P(c) = P(P(c));   // benign-race: a reader sees the old or the new pointer, both on the path
+            own[z] = ld16(pbase + own[z]);   // benign-race: a reader sees the old or the new pointer, both on the path
+            P(c) = uint16_t(own[z]);
         }
         __syncthreads();
     }
@@ -553,7 +559,7 @@ __global__ void __launch_bounds__(kThreads, 2)
         const int c = cfb + 2 * (z + 1) * PS;
         // chase to the root (a cell that points to itself), two hops per
         // loop turn so that no register copies are needed
-        uint32_t r = ld16(pbase + c);   // benign-race (see above)
+        uint32_t r = own[z];
         for (;;) {
             const uint32_t q = ld16(pbase + r);   // benign-race
             if (q == r) break;
