@@ -958,9 +958,26 @@ static eg_status compute_grid(eg_ctx *c, const Problem &P, const float *f, uint3
             }
         }
         int32_t *lab0 = c->label_all.as<int32_t>() + hpad - (base_v - e0);
-        CK(launch_finalize(lab0, nullptr, e0, e1, c->stream,
-                           (flags & EG_STATS) ? c->stat_buf.as<unsigned long long>() + 1 : nullptr));
-        c->stats.kernel_launches += 1;
+        unsigned long long *hist = (flags & EG_STATS) ? c->stat_buf.as<unsigned long long>() + 1 : nullptr;
+        const char *sv = std::getenv("EG_FIN_SPLIT");
+        const int split = sv ? std::atoi(sv) : 2;
+        bool faces = P.ndim == 3 && split && tiled;
+        for (SlabState *S : c->slabs) faces = faces && S->s.z1 - S->s.z0 > kTileZ;
+        if (faces) {
+            // per slab (tiles start at every slab's first plane): first the z-face
+            // plane pairs of every slab, then the rest of every slab; a chain that
+            // reaches another slab stops at a final boundary value (or, with several
+            // GPUs, at a final halo plane)
+            for (int pm : {1 | (split >= 3 ? 2 : 0), 4})
+                for (SlabState *S : c->slabs) {
+                    CK(launch_finalize_faces(S->label, S->s.v0, P.dims[0], P.dims[1], S->s.z1 - S->s.z0, kTileZ,
+                                             kTileY, split >= 3, pm, c->stream, hist));
+                    c->stats.kernel_launches += pm == 4 ? 1 : (split >= 3 ? 2 : 1);
+                }
+        } else {
+            CK(launch_finalize(lab0, nullptr, e0, e1, c->stream, hist));
+            c->stats.kernel_launches += 1;
+        }
     }
     for (SlabState *S : c->slabs) {
         if (!tiled && !multi) continue;           // generic single slab: already final
@@ -975,7 +992,7 @@ static eg_status compute_grid(eg_ctx *c, const Problem &P, const float *f, uint3
             // a chain of the later pass that leaves its tile through a z face ends
             // one load later, at a label the first pass already finished (k_slab.cu)
             CK(launch_finalize_faces(S->label, S->s.v0, P.dims[0], P.dims[1], S->s.z1 - S->s.z0, kTileZ, kTileY,
-                                     split >= 3, c->stream, hist));
+                                     split >= 3, 7, c->stream, hist));
             c->stats.kernel_launches += split >= 3 ? 3 : 2;
         } else {
             CK(launch_finalize(S->label, nullptr, S->s.v0, S->s.v1, c->stream, hist));

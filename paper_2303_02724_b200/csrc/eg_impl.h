@@ -261,8 +261,11 @@ cudaError_t launch_finalize_list(int32_t *label, const int32_t *list, const unsi
 cudaError_t launch_gather_labels(const int32_t *label, const int32_t *list, int64_t n, int32_t *out, cudaStream_t st);
 cudaError_t launch_finalize(int32_t *label, const uint32_t *bits, int64_t v0, int64_t v1, cudaStream_t st,
                             unsigned long long *hist = nullptr);
-// the one-slab label pass of a 3-D grid in three launches (z-face plane pairs,
-// y-face row pairs, the rest; tiles of tz planes x ty rows from local plane 0)
+// the label pass of one 3-D slab in up to three launches (z-face plane pairs,
+// y-face row pairs, the rest; tiles of tz planes x ty rows from the slab's
+// first plane).  passes: bit p runs pass p.  label / v0: the slab's labels and
+// its first global id; chase targets may lie outside the slab (other slabs
+// of the same label array, or halo planes holding final values)
 cudaError_t launch_finalize_faces(int32_t *label, int64_t v0, int64_t nx, int64_t ny, int64_t planes, int tz, int ty,
-                                  int ysplit, cudaStream_t st, unsigned long long *hist = nullptr);
+                                  int ysplit, int passes, cudaStream_t st, unsigned long long *hist = nullptr);
 }  // namespace eg

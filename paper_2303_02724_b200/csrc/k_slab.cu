@@ -271,7 +271,7 @@ static uint64_t div_magic(int64_t d) {
 }
 
 cudaError_t launch_finalize_faces(int32_t *label, int64_t v0, int64_t nx, int64_t ny, int64_t planes, int tz, int ty,
-                                  int ysplit, cudaStream_t st, unsigned long long *hist) {
+                                  int ysplit, int passes, cudaStream_t st, unsigned long long *hist) {
     if (nx * ny * planes <= 0) return cudaSuccess;
     if (tz != kFaceT || ty != kFaceT) return cudaErrorInvalidValue;
     const FaceSplit F{int32_t(nx), int32_t(ny), int32_t(planes), ysplit, div_magic(nx), div_magic(2 * nx)};
@@ -282,7 +282,7 @@ cudaError_t launch_finalize_faces(int32_t *label, int64_t v0, int64_t nx, int64_
     for (int pass = 0; pass < 3; ++pass) {
         const int64_t gy = pass == 0 ? zpairs : planes;
         const int64_t words = pass == 0 ? (2 * plane + 31) / 32 : pass == 1 ? ypair_words : (plane + 31) / 32;
-        if (gy <= 0 || (pass == 1 && (ny <= ty || !ysplit))) continue;
+        if (!((passes >> pass) & 1) || gy <= 0 || (pass == 1 && (ny <= ty || !ysplit))) continue;
         auto go = [&](auto kwc) {
             constexpr int K = decltype(kwc)::value;
             const dim3 grid(unsigned((words + 4 * K - 1) / (4 * K)), unsigned(gy));
