@@ -1206,7 +1206,7 @@ static eg_status bundle_arcs(eg_ctx *c) {
     B.o_arc_m = c->b_arc_m.as<int64_t>();
     B.o_arc_mult = c->b_arc_mult.as<int32_t>();
     CK(launch_bundle(B, c->stream));
-    c->stats.kernel_launches += 9;
+    c->stats.kernel_launches += 11;
     int64_t cnt[2];
     CK(cudaMemcpyAsync(&cnt[0], B.s_pos + ns, sizeof(int64_t), cudaMemcpyDeviceToHost, c->stream));
     CK(cudaMemcpyAsync(&cnt[1], B.a_pos + ns, sizeof(int64_t), cudaMemcpyDeviceToHost, c->stream));
@@ -1513,6 +1513,20 @@ eg_status eg_compute_typed(eg_ctx *c, const eg_domain *d, const void *d_field, i
     if (n <= 0) return set_err(c, EG_ERR_INVALID_ARG, "empty field");
     CK(cudaSetDevice(c->device));
     CK(c->typed.ensure(sizeof(float) * size_t(n)));
+    if (rank) {
+        // every value exactly a float32 (f32 data stored wider, integers below
+        // 2^24, ...): the cast is an order isomorphism, no rank sort needed
+        CK(c->flags.ensure(sizeof(int) * 128));
+        CK(cudaMemsetAsync(c->flags.p, 0, sizeof(int), c->stream));
+        CK(launch_exact_f32(d_field, dtype, c->typed.as<float>(), n, c->flags.as<int>(), c->stream));
+        int inexact = 1;
+        CK(cudaMemcpyAsync(&inexact, c->flags.p, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        if (!inexact) {
+            c->stats.kernel_launches += 1;
+            return compute_impl(c, d, c->typed.as<float>(), flags, true);
+        }
+    }
     if (rank) {
         if (n > kRankMaxN) return set_err(c, EG_ERR_UNSUPPORTED, "rank image: N = %lld too large", (long long)n);
         size_t bytes = 0;

@@ -158,6 +158,8 @@ cudaError_t launch_emit_arcs(const int32_t *saddles, int64_t n_sad, const int64_
 
 // exact conversion of an EG_DTYPE_* field to float32 (reading L21)
 cudaError_t launch_to_f32(const void *in, int dtype, float *out, int64_t n, cudaStream_t st);
+// float64 / (u)int32 / (u)int64 -> float32 cast; *inexact |= 1 if a value is not exactly a float32
+cudaError_t launch_exact_f32(const void *in, int dtype, float *out, int64_t n, int *inexact, cudaStream_t st);
 // SoS-rank image of a field (reading L22; F32 too): out[v] = the float with bit
 // pattern rank(v) + 2^23 (reverse: N-1-rank(v), the reversed order of L11).
 // scratch == null: *bytes = the scratch size.

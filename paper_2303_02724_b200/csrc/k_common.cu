@@ -298,28 +298,35 @@ __global__ void k_bundle_keys(const int32_t *__restrict__ n_unique, const int64_
     keep[j] = 1;
 }
 
+// order key of a saddle's value (order-preserving, -0 == +0: reading L2)
+__global__ void k_bundle_vkeys(const int32_t *__restrict__ saddles, const float *__restrict__ f, int64_t f_base,
+                               int64_t ns, uint32_t *vkey) {
+    const int64_t j = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (j >= ns) return;
+    const float x = __ldg(f + (saddles[j] - f_base));
+    const uint32_t b = x == 0.0f ? 0u : __float_as_uint(x);
+    vkey[j] = b ^ ((b & 0x80000000u) ? 0xffffffffu : 0x80000000u);
+}
+
+__global__ void k_bundle_gather_keys(const uint64_t *__restrict__ keys, const int32_t *__restrict__ idx, int64_t ns,
+                                     uint64_t *out) {
+    const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i < ns) out[i] = keys[idx[i]];
+}
+
+// After the stable sorts (value key, then pair key) every pair's run lists its
+// saddles in ascending (value, index) order: the last one is the highest
+// (SoS) and survives; the others of a run of two or more are dropped.  O(1)
+// per saddle (a serial scan of every run by its first thread took 9 ms on C5,
+// whose 187 maxima give runs of thousands of saddles).
 __global__ void k_bundle_pick(const uint64_t *__restrict__ keys, const int32_t *__restrict__ idx, int64_t ns,
-                              const int32_t *__restrict__ saddles, const float *__restrict__ f, int64_t f_base,
                               int32_t *keep) {
     const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i >= ns) return;
     const uint64_t k = keys[i];
-    if (k == ~0ull || (i > 0 && keys[i - 1] == k)) return;     // not the first of a pair's run
-    int64_t e = i + 1;
-    while (e < ns && keys[e] == k) ++e;
-    if (e == i + 1) return;                                     // a single saddle for this pair
-    int32_t best = idx[i];
-    float bf = __ldg(f + (saddles[best] - f_base));
-    for (int64_t q = i + 1; q < e; ++q) {
-        const int32_t j = idx[q];
-        const float fj = __ldg(f + (saddles[j] - f_base));
-        if (fj > bf || (fj == bf && saddles[j] > saddles[best])) {
-            best = j;
-            bf = fj;
-        }
-    }
-    for (int64_t q = i; q < e; ++q)
-        if (idx[q] != best) keep[idx[q]] = 0;
+    if (k == ~0ull) return;
+    const bool last = i + 1 == ns || keys[i + 1] != k;
+    if (!last) keep[idx[i]] = 0;
 }
 
 // kept counts: saddles (keep) and arcs (keep * n_unique), for the scans
@@ -352,10 +359,12 @@ __global__ void k_bundle_emit(const int32_t *__restrict__ keep, const int64_t *_
 }
 
 size_t bundle_sort_bytes(int64_t ns) {
-    size_t b = 0;
+    size_t b = 0, b32 = 0;
     cub::DeviceRadixSort::SortPairs(nullptr, b, (const uint64_t *)nullptr, (uint64_t *)nullptr,
                                     (const int32_t *)nullptr, (int32_t *)nullptr, int(std::max<int64_t>(ns, 1)));
-    return b;
+    cub::DeviceRadixSort::SortPairs(nullptr, b32, (const uint32_t *)nullptr, (uint32_t *)nullptr,
+                                    (const int32_t *)nullptr, (int32_t *)nullptr, int(std::max<int64_t>(ns, 1)));
+    return std::max(b, b32);
 }
 
 cudaError_t launch_bundle(const BundleArgs &B, cudaStream_t st) {
@@ -363,11 +372,18 @@ cudaError_t launch_bundle(const BundleArgs &B, cudaStream_t st) {
     if (ns <= 0) return cudaSuccess;
     const unsigned nb = blocks_for(ns, 256);
     k_bundle_keys<<<nb, 256, 0, st>>>(B.n_unique, B.arc_off, B.arc_m, ns, B.keys, B.idx, B.keep);
+    // saddle order (value, then index: idx starts ascending and the sorts are
+    // stable), then the pair key: keys2 holds the two value-key arrays first
+    uint32_t *vkey = reinterpret_cast<uint32_t *>(B.keys2), *vkey2 = vkey + ns;
+    k_bundle_vkeys<<<nb, 256, 0, st>>>(B.sad32, B.f, B.f_base, ns, vkey);
     size_t bytes = B.sort_bytes;
-    cudaError_t e = cub::DeviceRadixSort::SortPairs(B.sort_tmp, bytes, B.keys, B.keys2, B.idx, B.idx2, int(ns), 0,
-                                                    64, st);
+    cudaError_t e = cub::DeviceRadixSort::SortPairs(B.sort_tmp, bytes, vkey, vkey2, B.idx, B.idx2, int(ns), 0, 32, st);
     if (e != cudaSuccess) return e;
-    k_bundle_pick<<<nb, 256, 0, st>>>(B.keys2, B.idx2, ns, B.sad32, B.f, B.f_base, B.keep);
+    k_bundle_gather_keys<<<nb, 256, 0, st>>>(B.keys, B.idx2, ns, B.keys2);
+    bytes = B.sort_bytes;
+    e = cub::DeviceRadixSort::SortPairs(B.sort_tmp, bytes, B.keys2, B.keys, B.idx2, B.idx, int(ns), 0, 64, st);
+    if (e != cudaSuccess) return e;
+    k_bundle_pick<<<nb, 256, 0, st>>>(B.keys, B.idx, ns, B.keep);
     k_bundle_counts<<<nb, 256, 0, st>>>(B.keep, B.n_unique, ns, B.arc_cnt);
     if ((e = launch_scan_i32(B.keep, B.s_pos, ns, B.scan_tmp, B.scan_bytes, st)) != cudaSuccess) return e;
     if ((e = launch_scan_i32(B.arc_cnt, B.a_pos, ns, B.scan_tmp, B.scan_bytes, st)) != cudaSuccess) return e;
@@ -403,6 +419,48 @@ cudaError_t launch_to_f32(const void *in, int dtype, float *out, int64_t n, cuda
         case EG_DTYPE_I8: k_to_f32<int8_t><<<nb, 256, 0, st>>>(static_cast<const int8_t *>(in), out, n); break;
         case EG_DTYPE_U16: k_to_f32<uint16_t><<<nb, 256, 0, st>>>(static_cast<const uint16_t *>(in), out, n); break;
         case EG_DTYPE_I16: k_to_f32<int16_t><<<nb, 256, 0, st>>>(static_cast<const int16_t *>(in), out, n); break;
+        default: return cudaErrorInvalidValue;
+    }
+    return cudaGetLastError();
+}
+
+// ------------------ exact float32 image of a wider type, when there is one
+// float64 / (u)int32 / (u)int64 fields whose every value is exactly a float32
+// (f32 data stored as f64, integers below 2^24, ...): the cast is then an
+// order isomorphism of the values, so the graph on it is the type's own
+// graph (reading L22) without the rank sort.  *inexact |= 1 if any value is
+// not exactly representable (NaN included: the rank path rejects it).
+__device__ __forceinline__ bool exact_back(double x, float f) { return double(f) == x; }
+__device__ __forceinline__ bool exact_back(int32_t x, float f) {
+    return f >= -2147483648.0f && f < 2147483648.0f && int32_t(f) == x;
+}
+__device__ __forceinline__ bool exact_back(uint32_t x, float f) { return f < 4294967296.0f && uint32_t(f) == x; }
+__device__ __forceinline__ bool exact_back(int64_t x, float f) {
+    return f >= -9.2233720e18f && f < 9.2233720e18f && int64_t(f) == x;
+}
+__device__ __forceinline__ bool exact_back(uint64_t x, float f) { return f < 1.8446744e19f && uint64_t(f) == x; }
+
+template <typename T>
+__global__ void k_exact_f32(const T *__restrict__ in, float *__restrict__ out, int64_t n, int *inexact) {
+    bool bad = false;
+    for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
+        const T x = in[i];
+        const float f = float(x);
+        out[i] = f;
+        bad = bad || !exact_back(x, f);
+    }
+    if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(inexact, 1);
+}
+
+cudaError_t launch_exact_f32(const void *in, int dtype, float *out, int64_t n, int *inexact, cudaStream_t st) {
+    if (n <= 0) return cudaSuccess;
+    const unsigned nb = unsigned(std::min<int64_t>((n + 255) / 256, 148 * 16));
+    switch (dtype) {
+        case EG_DTYPE_F64: k_exact_f32<double><<<nb, 256, 0, st>>>(static_cast<const double *>(in), out, n, inexact); break;
+        case EG_DTYPE_I32: k_exact_f32<int32_t><<<nb, 256, 0, st>>>(static_cast<const int32_t *>(in), out, n, inexact); break;
+        case EG_DTYPE_U32: k_exact_f32<uint32_t><<<nb, 256, 0, st>>>(static_cast<const uint32_t *>(in), out, n, inexact); break;
+        case EG_DTYPE_I64: k_exact_f32<int64_t><<<nb, 256, 0, st>>>(static_cast<const int64_t *>(in), out, n, inexact); break;
+        case EG_DTYPE_U64: k_exact_f32<uint64_t><<<nb, 256, 0, st>>>(static_cast<const uint64_t *>(in), out, n, inexact); break;
         default: return cudaErrorInvalidValue;
     }
     return cudaGetLastError();

@@ -832,3 +832,34 @@ def test_face_split_label_pass(eg, ctx, split, dims, monkeypatch):
     f = t3.numpy().reshape(max(dims), max(dims), max(dims))[:dims[2], :dims[1], :dims[0]].ravel().copy()
     o = O.grid(f, dims)
     assert_graph_equal(ctx.compute(torch.from_numpy(f).cuda(), dims=dims), o, what=f"split {split} {dims}")
+
+
+@pytest.mark.parametrize("tdtype", ["float64", "int32", "uint32", "int64", "uint64"])
+@pytest.mark.parametrize("dims,path", [([64, 48], 0), ([40, 33, 29], 0), ([9, 8, 7, 6], "generic")])
+def test_exact_image_dtypes(eg, ctx, tdtype, dims, path):
+    """eg_compute_typed on wide types whose every value is exactly a float32
+    (float32 data stored as float64, integers below 2^24, with ties): the
+    library takes the plain cast instead of the rank sort; the graph is still
+    the type's own -- equal to the oracle on the rank image, and on the values."""
+    import torch
+    if not hasattr(torch, tdtype):
+        pytest.skip(f"torch has no {tdtype}")
+    rng = np.random.default_rng(len(dims) * 7 + len(tdtype))
+    N = int(np.prod(dims))
+    if tdtype == "float64":
+        x = rng.standard_normal(N).astype(np.float32).astype(np.float64)
+        x[::5] = x[1::5][: len(x[::5])]              # ties
+    else:
+        x = rng.integers(0, 1 << 20, N).astype(tdtype)
+        x[::3] = 7                                    # ties
+    try:
+        t = torch.from_numpy(x).cuda()
+    except (TypeError, RuntimeError) as e:
+        pytest.skip(f"torch cannot move {tdtype} to the device: {e}")
+    fr = _rank_image(x)
+    for minimum in (False, True):
+        o = O.grid(fr, dims, minimum=minimum)
+        o2 = O.grid(x.astype(np.float32), dims, minimum=minimum)
+        assert np.array_equal(o.arcs, o2.arcs) and np.array_equal(o.label, o2.label)
+        g = ctx.compute(t, dims=dims, flags=_flags(eg, path, eg.EG_CHECK_NAN | (eg.EG_MINIMUM if minimum else 0)))
+        assert_graph_equal(g, o, what=f"{tdtype} {dims} {path} minimum={minimum}")

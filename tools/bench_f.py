@@ -75,8 +75,14 @@ def main():
             rows.append(row)
             print(json.dumps(row), flush=True)
         # f3: other input types through eg_compute_typed
-        for tdt, label in ((torch.float64, "f3 float64 (SoS-rank image)"), (torch.float16, "f3 float16 (exact image)")):
-            ft = f.to(tdt)
+        for tdt, label in ((torch.float64, "f3 float64, every value a float32 (exact cast, no rank sort)"),
+                           ("f64-wide", "f3 float64 with 52-bit mantissas (SoS-rank image: radix sort)"),
+                           (torch.float16, "f3 float16 (exact image)")):
+            if tdt == "f64-wide":
+                g64 = torch.Generator(device=f.device).manual_seed(64)
+                ft = f.double() * (1.0 + 1e-12 * torch.rand(f.shape, generator=g64, device=f.device, dtype=torch.float64))
+            else:
+                ft = f.to(tdt)
             row = timed(ft, kw, base, steps=5, label=label)
             row["config"] = cfg
             rows.append(row)
