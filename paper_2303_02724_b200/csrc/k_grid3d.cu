@@ -48,6 +48,17 @@ constexpr int PL = BX * BY;                          // 720 cells per plane of t
 constexpr int BOX = PL * BZ;                         // 12960 field-box cells = one TMA box
 constexpr int PS = 1024;                             // pointer-box plane stride: cell r = bz * PS + by * BX + bx
 constexpr int PBOX = BZ * PS;                        // 18432 cells; pointers are byte offsets 2 r < 65536 (16 bits)
+// plane bz of the pointer box starts at byte bz * (2 PS + SKEW): the skew turns
+// the plane stride from a multiple of 128 B (cells of three planes at one
+// (x, y) in one bank: 2-way conflicts in the pointer gathers) into one that
+// shifts the banks by 8 per plane; bz = offset >> 11 still holds, since
+// 17 * SKEW + 2 * (PL - 1) < 2 PS
+#ifndef EG_PB_SKEW
+#define EG_PB_SKEW 32
+#endif
+constexpr int SKEW = EG_PB_SKEW;
+constexpr int PSB = 2 * PS + SKEW;                   // plane stride in bytes
+static_assert((BY * BX * 18 > 0) && 17 * SKEW + 2 * (18 * 40 - 1) < 2 * 1024, "skewed planes keep plane = offset >> 11");
 constexpr int kThreads = TX * TY;                    // one z-column per thread
 constexpr int kWarps = kThreads / 32;
 constexpr int kLutWords = (1 << 14) / 16;            // 2 bits per 14-bit upper mask: beta0+ >= 2, beta0+ == 0
@@ -429,17 +440,17 @@ __global__ void __launch_bounds__(kThreads, 2)
     // compare with it is false, so the truncated link (reading L3) falls out
     // of the same code for every tile.
     auto bplus = [&](const float *s, int dz) -> VK {    // (0,0) (1,0) (0,1) (1,1)
-        VK m{s[0], 2 * (dz * PS)};
-        m = vmax(m, VK{s[1], 2 * (1 + dz * PS)});
-        m = vmax(m, VK{s[2], 2 * (BX + dz * PS)});
-        m = vmax(m, VK{s[3], 2 * (BX + 1 + dz * PS)});
+        VK m{s[0], dz * PSB};
+        m = vmax(m, VK{s[1], 2 * 1 + dz * PSB});
+        m = vmax(m, VK{s[2], 2 * BX + dz * PSB});
+        m = vmax(m, VK{s[3], 2 * (BX + 1) + dz * PSB});
         return m;
     };
     auto bminus = [&](const float *s, int dz) -> VK {   // (0,0) (-1,0) (0,-1) (-1,-1), backwards
-        VK m{s[0], 2 * (dz * PS)};
-        m = vearlier(m, VK{s[4], 2 * (-1 + dz * PS)});
-        m = vearlier(m, VK{s[5], 2 * (-BX + dz * PS)});
-        m = vearlier(m, VK{s[6], 2 * (-BX - 1 + dz * PS)});
+        VK m{s[0], dz * PSB};
+        m = vearlier(m, VK{s[4], 2 * (-1) + dz * PSB});
+        m = vearlier(m, VK{s[5], 2 * (-BX) + dz * PSB});
+        m = vearlier(m, VK{s[6], 2 * (-BX - 1) + dz * PSB});
         return m;
     };
 
@@ -464,8 +475,8 @@ __global__ void __launch_bounds__(kThreads, 2)
         const VK U = vmax(bp_cur, bp_next);        // B+(z+1) is later (NaN beyond the domain)
         const VK L = vearlier(bm_cur, bm_prev);     // B-(z-1) is earlier (NaN below the domain)
         int d = vmax(L, U).d;
-        bp_cur = VK{bp_next.v, bp_next.d - 2 * PS};
-        bm_prev = VK{bm_cur.v, bm_cur.d - 2 * PS};
+        bp_cur = VK{bp_next.v, bp_next.d - PSB};
+        bm_prev = VK{bm_cur.v, bm_cur.d - PSB};
         // S3: upper mask, bit k = k-th link vertex in ascending index order:
         // lower group (index < v: up iff f > fv), then the upper group (>=).
         uint32_t mask = 0u;
@@ -486,7 +497,7 @@ __global__ void __launch_bounds__(kThreads, 2)
         // an empty upper link points to itself; this also makes a NaN vertex
         // (every compare false) terminal, so no pointer cycle can form
         d = mask ? d : 0;
-        const int c = cfb + 2 * (z + 1) * PS;
+        const int c = cfb + (z + 1) * PSB;
         own[z] = uint32_t(kInterior || ok ? c + d : c);
         P(c) = uint16_t(own[z]);
         // 2-bit class code from the LUT: bit 0 saddle (beta0+ >= 2), bit 1
@@ -537,7 +548,7 @@ __global__ void __launch_bounds__(kThreads, 2)
     for (int round = 0; round < A.rounds; ++round) {
 #pragma unroll
         for (int z = 0; z < TZ; ++z) {
-            const int c = cfb + 2 * (z + 1) * PS;
+            const int c = cfb + (z + 1) * PSB;
             own[z] = ld16(pbase + own[z]);   // benign-race: a reader sees the old or the new pointer, both on the path
             P(c) = uint16_t(own[z]);
         }
@@ -556,7 +567,7 @@ __global__ void __launch_bounds__(kThreads, 2)
     for (int zz = 0; zz < TZ; ++zz) {
         const int z = TZ - 1 - zz;   // top down: measured 1.5 % faster than bottom up on C3
         const bool ok = col_ok && (kInterior || z0 + z < A.z_hi);
-        const int c = cfb + 2 * (z + 1) * PS;
+        const int c = cfb + (z + 1) * PSB;
         // chase to the root (a cell that points to itself), two hops per
         // loop turn so that no register copies are needed
         uint32_t r = own[z];
@@ -568,7 +579,7 @@ __global__ void __launch_bounds__(kThreads, 2)
         }
         P(c) = uint16_t(r);   // benign-race: the root is a later vertex of every path through c
         const int bz = r >> 11;
-        const int32_t t = *reinterpret_cast<const int32_t *>(reinterpret_cast<const char *>(ptab) + ((r & (2 * PS - 2)) << 1));
+        const int32_t t = *reinterpret_cast<const int32_t *>(reinterpret_cast<const char *>(ptab) + (((r & (2 * PS - 1)) - bz * SKEW) << 1));
         // exit: the root is in the halo shell of the box, or (last tile of a
         // slab) in a plane the slab does not own
         bool exit = t < 0 || unsigned(bz - 1) >= unsigned(TZ);
@@ -649,7 +660,7 @@ __global__ void __launch_bounds__(kThreads, 2)
         const uint32_t b = __ballot_sync(0xffffffffu, m);
         if (m) {
             const unsigned long long j = slot + __popc(b & lt);
-            if (j < (unsigned long long)A.ecap) A.elist[j] = g_box0 + (i >> 11) * nxy + (ptab[(i >> 1) & (PS - 1)] & 0x7fffffff);
+            if (j < (unsigned long long)A.ecap) A.elist[j] = g_box0 + (i >> 11) * nxy + (ptab[((i & (2 * PS - 1)) - (i >> 11) * SKEW) >> 1] & 0x7fffffff);
         }
         slot += __popc(b);
     }
@@ -846,7 +857,7 @@ eg_status tiled3d_local(Tiled3D *t, int ndim, const int64_t *dims, const Slab &s
             for (int by = 0; by < BY; ++by)
                 for (int bx = XO - 1; bx <= XO + TX; ++bx)
                     if (bz == 0 || bz == BZ - 1 || by == 0 || by == BY - 1 || bx == XO - 1 || bx == XO + TX)
-                        sh.push_back(uint16_t(2 * (bz * PS + by * BX + bx)));
+                        sh.push_back(uint16_t(2 * (bz * PS + by * BX + bx) + bz * SKEW));
         if (int(sh.size()) != kShell) {
             if (err) *err = "shell size";
             return EG_ERR_STATE;
