@@ -132,6 +132,7 @@ struct eg_ctx {
     bool h64_valid = false, h32_valid = false;   // which id width of the host graph is materialised
     HostBuf h_stage;
     HostBuf h_path_off, h_path_v;      // EG_ARC_PATHS
+    DevBuf path_nxt;                   // EG_ARC_PATHS: next step of every visited vertex (int32[N])
     HostBuf h_fmax, h_fsad;            // EG_NODE_VALUES: f at the maxima / saddles
     DevBuf d_fnode;
     bool node_values = false, last_minimum = false;
@@ -1295,14 +1296,16 @@ static eg_status compute_impl(eg_ctx *c, const eg_domain *d, const float *f, uin
         const int64_t nr = S.n_raw;
         CK(c->path_len.ensure(sizeof(int64_t) * std::max<int64_t>(nr, 1)));
         CK(c->path_off.ensure(sizeof(int64_t) * (nr + 1)));
-        auto paths = [&](const int64_t *off, int64_t *out) -> cudaError_t {
-            if (P.grid)
-                return launch_arc_paths_grid(c->host_tab, P.ndim, S.F, S.raw_s.as<int64_t>(), S.raw_rep.as<int64_t>(),
-                                             nr, off, out, c->stream);
-            return launch_arc_paths_csr(P.row_ptr, P.col_idx, f, S.raw_s.as<int64_t>(), S.raw_rep.as<int64_t>(), nr,
-                                        off, out, c->stream);
-        };
-        CK(paths(nullptr, c->path_len.as<int64_t>()));
+        // pass 1 walks every path (argmax recomputed from f) for its length and
+        // leaves each visited vertex's next step in path_nxt; pass 2 follows those
+        CK(c->path_nxt.ensure(sizeof(int32_t) * std::max<int64_t>(P.N, 1)));
+        int32_t *nxt = c->path_nxt.as<int32_t>();
+        if (P.grid)
+            CK(launch_arc_paths_grid(c->host_tab, P.ndim, S.F, S.raw_s.as<int64_t>(), S.raw_rep.as<int64_t>(), nr,
+                                     nullptr, c->path_len.as<int64_t>(), c->stream, nxt));
+        else
+            CK(launch_arc_paths_csr(P.row_ptr, P.col_idx, f, S.raw_s.as<int64_t>(), S.raw_rep.as<int64_t>(), nr,
+                                    nullptr, c->path_len.as<int64_t>(), c->stream, nxt));
         const size_t sb = scan64_scratch_bytes(std::max<int64_t>(nr, 1));
         CK(c->scratch.ensure(sb));
         CK(launch_scan_i64(c->path_len.as<int64_t>(), c->path_off.as<int64_t>(), nr, c->scratch.p, sb, c->stream));
@@ -1312,7 +1315,8 @@ static eg_status compute_impl(eg_ctx *c, const eg_domain *d, const float *f, uin
         CK(cudaStreamSynchronize(c->stream));
         const int64_t total = c->h_path_off.as<int64_t>()[nr];
         CK(c->path_v.ensure(sizeof(int64_t) * std::max<int64_t>(total, 1)));
-        CK(paths(c->path_off.as<int64_t>(), c->path_v.as<int64_t>()));
+        CK(launch_arc_paths_follow(S.raw_s.as<int64_t>(), S.raw_rep.as<int64_t>(), nr, c->path_off.as<int64_t>(), nxt,
+                                   P.grid ? S.F.v0 : 0, c->path_v.as<int64_t>(), c->stream));
         CK(c->h_path_v.ensure(sizeof(int64_t) * std::max<int64_t>(total, 1)));
         if (total)
             CK(cudaMemcpyAsync(c->h_path_v.p, c->path_v.p, sizeof(int64_t) * total, cudaMemcpyDeviceToHost,

@@ -215,10 +215,13 @@ cudaError_t launch_gather_f(const float *f, int64_t f_base, const int64_t *ids, 
 // into len_or_out[j]; else the vertices at len_or_out[off[j] ..]
 cudaError_t launch_arc_paths_grid(const LinkTable &tab, int ndim, FieldView F, const int64_t *raw_s,
                                   const int64_t *raw_rep, int64_t n_raw, const int64_t *off, int64_t *len_or_out,
-                                  cudaStream_t st);
+                                  cudaStream_t st, int32_t *nxt = nullptr);
 cudaError_t launch_arc_paths_csr(const int64_t *row_ptr, const int32_t *col_idx, const float *f, const int64_t *raw_s,
                                  const int64_t *raw_rep, int64_t n_raw, const int64_t *off, int64_t *len_or_out,
-                                 cudaStream_t st);
+                                 cudaStream_t st, int32_t *nxt = nullptr);
+// second pass of the arc geometry: follow the next steps the first pass left in nxt (index v - v0)
+cudaError_t launch_arc_paths_follow(const int64_t *raw_s, const int64_t *raw_rep, int64_t n_raw, const int64_t *off,
+                                    const int32_t *nxt, int64_t v0, int64_t *out, cudaStream_t st);
 // exclusive scan of int64 counts into int64 offsets (offsets[n] = total)
 size_t scan64_scratch_bytes(int64_t n);
 cudaError_t launch_scan_i64(const int64_t *in, int64_t *out, int64_t n, void *scratch, size_t scratch_bytes,

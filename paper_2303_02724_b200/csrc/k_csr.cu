@@ -797,7 +797,8 @@ __global__ void __launch_bounds__(128) k_arcs_csr_reps(const int64_t *__restrict
 __global__ void __launch_bounds__(128) k_arc_paths_csr(const int64_t *__restrict__ rp, const int32_t *__restrict__ ci,
                                                        const float *__restrict__ f, const int64_t *__restrict__ raw_s,
                                                        const int64_t *__restrict__ raw_rep, int64_t n_raw,
-                                                       const int64_t *__restrict__ off, int64_t *len_or_out) {
+                                                       const int64_t *__restrict__ off, int64_t *len_or_out,
+                                                       int32_t *nxt) {
     const int64_t j = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (j >= n_raw) return;
     int64_t *out = off ? len_or_out + off[j] : nullptr;
@@ -819,6 +820,7 @@ __global__ void __launch_bounds__(128) k_arc_paths_csr(const int64_t *__restrict
                 bv = u;
             }
         }
+        if (nxt) nxt[v] = bv;               // the next step (v itself at a maximum), for k_arc_paths_follow
         if (bv == v) break;                 // a maximum
         v = bv;
     }
@@ -867,10 +869,38 @@ cudaError_t launch_arcs_csr_reps(const int64_t *row_ptr, const int32_t *rep_buf,
 
 cudaError_t launch_arc_paths_csr(const int64_t *row_ptr, const int32_t *col_idx, const float *f, const int64_t *raw_s,
                                  const int64_t *raw_rep, int64_t n_raw, const int64_t *off, int64_t *len_or_out,
-                                 cudaStream_t st) {
+                                 cudaStream_t st, int32_t *nxt) {
     if (n_raw <= 0) return cudaSuccess;
     k_arc_paths_csr<<<blocks_for(n_raw, 128), 128, 0, st>>>(row_ptr, col_idx, f, raw_s, raw_rep, n_raw, off,
-                                                            len_or_out);
+                                                            len_or_out, nxt);
+    return cudaGetLastError();
+}
+
+// Second pass of the arc geometry: the first pass left every visited vertex's
+// next step in nxt (a vertex of a maximum points to itself), so a path is
+// re-walked by one dependent load per vertex instead of a recomputed argmax.
+__global__ void __launch_bounds__(128) k_arc_paths_follow(const int64_t *__restrict__ raw_s,
+                                                          const int64_t *__restrict__ raw_rep, int64_t n_raw,
+                                                          const int64_t *__restrict__ off,
+                                                          const int32_t *__restrict__ nxt, int64_t v0, int64_t *out) {
+    const int64_t j = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (j >= n_raw) return;
+    int64_t *o = out + off[j];
+    o[0] = raw_s[j];
+    int64_t k = 1;
+    int64_t v = raw_rep[j];
+    for (;;) {
+        o[k++] = v;
+        const int64_t w = __ldg(nxt + (v - v0));
+        if (w == v) break;
+        v = w;
+    }
+}
+
+cudaError_t launch_arc_paths_follow(const int64_t *raw_s, const int64_t *raw_rep, int64_t n_raw, const int64_t *off,
+                                    const int32_t *nxt, int64_t v0, int64_t *out, cudaStream_t st) {
+    if (n_raw <= 0) return cudaSuccess;
+    k_arc_paths_follow<<<blocks_for(n_raw, 128), 128, 0, st>>>(raw_s, raw_rep, n_raw, off, nxt, v0, out);
     return cudaGetLastError();
 }
 

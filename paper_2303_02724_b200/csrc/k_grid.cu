@@ -493,7 +493,8 @@ template <int NDIM>
 __global__ void __launch_bounds__(128) k_arc_paths_grid(const __grid_constant__ GridConst<NDIM> S, FieldView F,
                                                         const int64_t *__restrict__ raw_s,
                                                         const int64_t *__restrict__ raw_rep, int64_t n_raw,
-                                                        const int64_t *__restrict__ off, int64_t *len_or_out) {
+                                                        const int64_t *__restrict__ off, int64_t *len_or_out,
+                                                        int32_t *nxt) {
     const int64_t j = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (j >= n_raw) return;
     int64_t *out = off ? len_or_out + off[j] : nullptr;
@@ -507,7 +508,9 @@ __global__ void __launch_bounds__(128) k_arc_paths_grid(const __grid_constant__ 
         int64_t best;
         typename Lattice<NDIM>::W up, un;
         upper_link<NDIM, false>(S, F, v, F.at(v), up, un, &best);
-        if (!bool(up | un)) break;          // a maximum
+        const bool top = !bool(up | un);    // a maximum
+        if (nxt) nxt[v - F.v0] = int32_t(top ? v : best);   // the next step, for k_arc_paths_follow
+        if (top) break;
         v = best;
     }
     if (!off) len_or_out[j] = k;
@@ -570,11 +573,11 @@ cudaError_t launch_arcs_grid(const LinkTable &tab, int ndim, FieldView F, const 
 
 cudaError_t launch_arc_paths_grid(const LinkTable &tab, int ndim, FieldView F, const int64_t *raw_s,
                                   const int64_t *raw_rep, int64_t n_raw, const int64_t *off, int64_t *len_or_out,
-                                  cudaStream_t st) {
+                                  cudaStream_t st, int32_t *nxt) {
     if (n_raw <= 0) return cudaSuccess;
 #define CALL(D)                                                                                              \
     k_arc_paths_grid<D><<<blocks_for(n_raw, 128), 128, 0, st>>>(make_grid_const<D>(tab), F, raw_s, raw_rep, n_raw, off, \
-                                                                len_or_out)
+                                                                len_or_out, nxt)
     EG_DISPATCH_NDIM(ndim, CALL)
 #undef CALL
     return cudaGetLastError();
