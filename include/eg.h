@@ -125,8 +125,9 @@ enum {
     EG_RAW_ARCS = 2u,         /* also keep raw (s, rep, m) per component     */
     EG_CHECK_CSR = 4u,        /* validate CSR sortedness / symmetry           */
     EG_FORCE_GENERIC = 8u,    /* grid: use the generic n-D kernels even for n <= 3 */
-    EG_NO_GRAPH_D2H = 16u,    /* leave the graph in HBM: one process -> eg_get_graph* copy it on the
-                                 first request; several ranks -> eg_get_graph* fail (EG_ERR_STATE) */
+    EG_NO_GRAPH_D2H = 16u,    /* leave the graph (and arc paths) in HBM: one process -> eg_get_graph*,
+                                 eg_get_raw_arcs and eg_get_arc_paths copy it on the first request;
+                                 several ranks -> eg_get_graph* fail (EG_ERR_STATE) */
     /* The MINIMUM graph instead ("computes both maximum and
      * minimum graph"; reading L11): minima, 1-saddles (beta0 of the lower link
      * >= 2) and the descending arcs / labels -- the maximum graph under the

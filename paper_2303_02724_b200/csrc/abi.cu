@@ -133,6 +133,8 @@ struct eg_ctx {
     HostBuf h_stage;
     HostBuf h_path_off, h_path_v;      // EG_ARC_PATHS
     DevBuf path_nxt;                   // EG_ARC_PATHS: next step of every visited vertex (int32[N])
+    int64_t n_path_v = 0;
+    bool paths_on_host = false;
     HostBuf h_fmax, h_fsad;            // EG_NODE_VALUES: f at the maxima / saddles
     DevBuf d_fnode;
     bool node_values = false, last_minimum = false;
@@ -1226,6 +1228,21 @@ static eg_status bundle_arcs(eg_ctx *c) {
     return EG_OK;
 }
 
+// EG_ARC_PATHS: offsets and vertices to the host (at once, or on the first
+// eg_get_arc_paths after a compute with EG_NO_GRAPH_D2H)
+static eg_status fetch_paths(eg_ctx *c) {
+    if (c->paths_on_host) return EG_OK;
+    const int64_t nr = c->n_paths, total = c->n_path_v;
+    CK(c->h_path_off.ensure(sizeof(int64_t) * (nr + 1)));
+    CK(cudaMemcpyAsync(c->h_path_off.p, c->path_off.p, sizeof(int64_t) * (nr + 1), cudaMemcpyDeviceToHost, c->stream));
+    CK(c->h_path_v.ensure(sizeof(int64_t) * std::max<int64_t>(total, 1)));
+    if (total)
+        CK(cudaMemcpyAsync(c->h_path_v.p, c->path_v.p, sizeof(int64_t) * total, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    c->paths_on_host = true;
+    return EG_OK;
+}
+
 static eg_status compute_impl(eg_ctx *c, const eg_domain *d, const float *f, uint32_t flags, bool device_field) {
     if (!c) return EG_ERR_INVALID_ARG;
     if (c->poisoned)
@@ -1310,20 +1327,19 @@ static eg_status compute_impl(eg_ctx *c, const eg_domain *d, const float *f, uin
         CK(c->scratch.ensure(sb));
         CK(launch_scan_i64(c->path_len.as<int64_t>(), c->path_off.as<int64_t>(), nr, c->scratch.p, sb, c->stream));
         CK(c->h_path_off.ensure(sizeof(int64_t) * (nr + 1)));
-        CK(cudaMemcpyAsync(c->h_path_off.p, c->path_off.p, sizeof(int64_t) * (nr + 1), cudaMemcpyDeviceToHost,
-                           c->stream));
+        CK(cudaMemcpyAsync(c->h_path_off.as<int64_t>() + nr, c->path_off.as<int64_t>() + nr, sizeof(int64_t),
+                           cudaMemcpyDeviceToHost, c->stream));
         CK(cudaStreamSynchronize(c->stream));
         const int64_t total = c->h_path_off.as<int64_t>()[nr];
         CK(c->path_v.ensure(sizeof(int64_t) * std::max<int64_t>(total, 1)));
         CK(launch_arc_paths_follow(S.raw_s.as<int64_t>(), S.raw_rep.as<int64_t>(), nr, c->path_off.as<int64_t>(), nxt,
                                    P.grid ? S.F.v0 : 0, c->path_v.as<int64_t>(), c->stream));
-        CK(c->h_path_v.ensure(sizeof(int64_t) * std::max<int64_t>(total, 1)));
-        if (total)
-            CK(cudaMemcpyAsync(c->h_path_v.p, c->path_v.p, sizeof(int64_t) * total, cudaMemcpyDeviceToHost,
-                               c->stream));
-        c->stats.kernel_launches += 3;
         c->n_paths = nr;
+        c->n_path_v = total;
         c->paths_valid = true;
+        c->paths_on_host = false;
+        if (!(flags & EG_NO_GRAPH_D2H)) ST(fetch_paths(c));   // else on request (eg_get_arc_paths)
+        c->stats.kernel_launches += 3;
     }
     if (c->bundle) ST(bundle_arcs(c));
     if (c->min_reflect) {
@@ -1799,6 +1815,7 @@ eg_status eg_simplify(eg_ctx *c, double tau, eg_graph *out) {
 eg_status eg_get_arc_paths(eg_ctx *c, int64_t *n, const int64_t **offsets, const int64_t **vertices) {
     if (!c || !n || !offsets || !vertices) return EG_ERR_INVALID_ARG;
     if (!c->have_graph || !c->paths_valid) return set_err(c, EG_ERR_STATE, "arc paths need eg_compute with EG_ARC_PATHS");
+    ST(fetch_paths(c));
     *n = c->n_paths;
     *offsets = c->h_path_off.as<int64_t>();
     *vertices = c->h_path_v.as<int64_t>();

@@ -817,6 +817,12 @@ def test_deferred_graph(eg, ctx):
     csr = (torch.from_numpy(rp).cuda(), torch.from_numpy(ci).cuda())
     ctx.compute(torch.from_numpy(fc).cuda(), csr=csr, flags=eg.EG_NO_GRAPH_D2H | eg.EG_GRAPH32)
     assert_graph_equal(ctx.graph(), O.csr(fc, rp, ci), what="deferred csr")
+    # arc geometry stays on the device too; eg_get_arc_paths copies it
+    eager = ctx.compute(t, dims=dims, flags=eg.EG_ARC_PATHS)
+    ctx.compute(t, dims=dims, flags=eg.EG_ARC_PATHS | eg.EG_NO_GRAPH_D2H)
+    lazy = ctx.graph()
+    assert np.array_equal(lazy.arc_paths[0], eager.arc_paths[0]) and np.array_equal(lazy.arc_paths[1], eager.arc_paths[1])
+    assert np.array_equal(lazy.raw_arcs, eager.raw_arcs)
 
 
 @pytest.mark.parametrize("split", ["0", "2", "3"])
