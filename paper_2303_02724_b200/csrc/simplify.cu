@@ -15,7 +15,6 @@
 #include <cmath>
 #include <cstdint>
 #include <queue>
-#include <unordered_map>
 #include <utility>
 #include <vector>
 
@@ -27,10 +26,9 @@ void simplify_graph(int64_t n_max, const int64_t *maxima, const float *fmax, int
                     const int32_t *sbeta, const float *fsad, int64_t n_arc, const int64_t *arc_s,
                     const int64_t *arc_m, const int32_t *arc_mult, double tau, bool minimum, SimplifyResult &out) {
     const double sgn = minimum ? -1.0 : 1.0;
-    // maxima by index; saddles by index (arcs are sorted by saddle)
-    std::unordered_map<int64_t, int32_t> mi;
-    mi.reserve(size_t(n_max) * 2 + 1);
-    for (int64_t i = 0; i < n_max; ++i) mi[maxima[i]] = int32_t(i);
+    // maxima by position in the ascending maxima list (binary search); saddles
+    // by position in the ascending saddle list (arcs are sorted by saddle)
+    auto mi = [&](int64_t id) { return int32_t(std::lower_bound(maxima, maxima + n_max, id) - maxima); };
     std::vector<double> mval(n_max);
     for (int64_t i = 0; i < n_max; ++i) mval[i] = sgn * double(fmax[i]);
     // SoS order of maxima: (value, id), the id reversed for a minimum graph
@@ -44,36 +42,42 @@ void simplify_graph(int64_t n_max, const int64_t *maxima, const float *fmax, int
         int64_t j = 0;
         for (int64_t a = 0; a < n_arc; ++a) {
             while (j < n_sad && saddles[j] < arc_s[a]) ++j;
-            const int32_t m = mi.at(arc_m[a]);
+            const int32_t m = mi(arc_m[a]);
             sarcs[j].push_back({m, arc_mult[a]});
             by_max[m].push_back(int32_t(j));
         }
     }
     std::vector<char> sal(n_sad, 1), mal(n_max, 1);
+    // cost: the second highest adjacent maximum (the lower one of two) minus
+    // the saddle, in one pass over its distinct maxima
     auto cost = [&](int64_t j) -> double {
         const auto &v = sarcs[j];
         if (v.size() < 2) return INFINITY;
-        std::vector<int32_t> ms;
-        for (const auto &p : v) ms.push_back(p.first);
-        std::sort(ms.begin(), ms.end(), [&](int32_t a, int32_t b) { return higher(b, a); });   // ascending
-        const double sv = sgn * double(fsad[j]);
-        return (ms.size() == 2 ? mval[ms[0]] : mval[ms[ms.size() - 2]]) - sv;
+        int32_t t1 = v[0].first, t2 = -1;
+        for (size_t k = 1; k < v.size(); ++k) {
+            const int32_t m = v[k].first;
+            if (higher(m, t1)) {
+                t2 = t1;
+                t1 = m;
+            } else if (t2 < 0 || higher(m, t2)) {
+                t2 = m;
+            }
+        }
+        return mval[t2] - sgn * double(fsad[j]);
     };
-    using Item = std::pair<double, int64_t>;      // (cost, saddle id); ties by id
-    std::priority_queue<Item, std::vector<Item>, std::greater<Item>> pq;
-    std::unordered_map<int64_t, int64_t> sidx;
-    sidx.reserve(size_t(n_sad) * 2 + 1);
-    for (int64_t j = 0; j < n_sad; ++j) {
-        sidx[saddles[j]] = j;
-        pq.push({cost(j), saddles[j]});
-    }
+    // (cost, saddle position): positions are in ascending id order, so ties
+    // still go to the lower saddle id
+    using Item = std::pair<double, int64_t>;
+    std::vector<Item> init(static_cast<size_t>(n_sad));
+    for (int64_t j = 0; j < n_sad; ++j) init[size_t(j)] = {cost(j), j};
+    std::priority_queue<Item, std::vector<Item>, std::greater<Item>> pq(std::greater<Item>(), std::move(init));
     while (!pq.empty()) {
-        const int64_t j = sidx[pq.top().second];
+        const int64_t j = pq.top().second;
         pq.pop();
         const double c = cost(j);
         if (c > tau) continue;
         if (!pq.empty() && c > pq.top().first) {
-            pq.push({c, saddles[j]});
+            pq.push({c, j});
             continue;
         }
         // cancel: every maximum of s but the highest merges into the highest
