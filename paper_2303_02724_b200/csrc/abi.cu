@@ -112,6 +112,7 @@ struct eg_ctx {
     DevBuf field;                      // eg_compute_host staging target
     DevBuf mirror;                     // EG_MINIMUM: g[i] = -f[N-1-i]
     DevBuf typed;                      // eg_compute_typed: the field converted to float32
+    DevBuf padded;                     // generic n-D grids, one slab: NaN-padded copy of the field
     DevBuf rank_scratch;               // eg_compute_typed, rank types: sort keys / indices / cub scratch
     bool minimum = false;              // the current compute is a minimum graph
     bool min_reflect = false;          // ... by point reflection (ids mapped back afterwards)
@@ -355,9 +356,20 @@ static eg_status nccl_exchange(eg_ctx *c, const void *send_lo, const void *send_
 static eg_status generic_local(eg_ctx *c, const Problem &P, SlabState &S, bool multi, bool timed) {
     const int64_t n = S.s.v1 - S.s.v0;
     int *flags = c->flags.as<int>();
+    // one slab: classify on a NaN-padded copy of the field when it costs at most
+    // twice the field (every axis + 2; tuning knob EG_PAD=0 turns it off)
+    float *pad = nullptr;
+    const char *pv = std::getenv("EG_PAD");
+    if (!multi && (!pv || std::atoi(pv) != 0)) {
+        const int64_t pc = padded_cells(c->host_tab, P.ndim);
+        if (pc < (int64_t(1) << 31) && pc <= 2 * n + 4096) {
+            CK(c->padded.ensure(sizeof(float) * size_t(pc)));
+            pad = c->padded.as<float>();
+        }
+    }
     if (timed) CK(cudaEventRecord(c->ev_main[0], c->stream));
     CK(launch_classify_grid(c->host_tab, P.ndim, S.F, S.s, S.label, S.sad_bits.as<uint32_t>(),
-                            S.max_bits.as<uint32_t>(), nullptr, flags, c->stream));
+                            S.max_bits.as<uint32_t>(), nullptr, flags, c->stream, pad));
     if (timed) CK(cudaEventRecord(c->ev_main[1], c->stream));
     c->stats.kernel_launches += 1;
     // S2 inside the slab: rounds are launched in batches; a round whose

@@ -95,9 +95,12 @@ struct LabelView {
 
 // S1 + S3, generic n: ptr[i] (global id) for owned i, saddle / maximum bits
 // (bit i of word i/32), optional beta0+ per vertex.
+// pad (optional, padded_cells floats): one slab classifies on a copy padded by
+// a NaN cell on each side of every axis (no per-offset domain tests)
 cudaError_t launch_classify_grid(const LinkTable &tab, int ndim, FieldView F, const Slab &s, int32_t *ptr,
                                  uint32_t *sad_bits, uint32_t *max_bits, uint8_t *beta_out, int *nan_flag,
-                                 cudaStream_t st);
+                                 cudaStream_t st, float *pad = nullptr);
+int64_t padded_cells(const LinkTable &tab, int ndim);
 // CSR S1 + S3 in two warp-per-vertex passes, no degree cap (k_csr.cu).
 // S1 over [v0, v1): ptr[v - v0] = gradient, max_bits (nullable) = maxima of the
 // range, and the upper list of every v: upl[row_ptr[v] .. + nup[v]) (upl is

@@ -198,6 +198,8 @@ struct GridConst {
     uint32_t dims[NDIM];
     uint32_t mag[NDIM];       // r / dims[a] = umulhi(r, mag[a]) >> sh[a] for r < 2^31
     int32_t sh[NDIM];
+    int32_t dposP[1 << NDIM]; // offset of +d in the NaN-padded copy (every axis + 2)
+    int32_t pstride[NDIM];    // strides of the padded copy
 };
 
 template <int NDIM>
@@ -209,6 +211,19 @@ static GridConst<NDIM> make_grid_const(const LinkTable &t) {
             if ((d >> a) & 1) x += t.stride[a];
         S.dpos[d] = int32_t(x);
         S.dneg[d] = -int32_t(x);
+    }
+    {
+        int64_t ps = 1;
+        for (int a = 0; a < NDIM; ++a) {
+            S.pstride[a] = int32_t(ps);
+            ps *= t.dims[a] + 2;
+        }
+        for (int d = 0; d < (1 << NDIM); ++d) {
+            int64_t x = 0;
+            for (int a = 0; a < NDIM; ++a)
+                if ((d >> a) & 1) x += S.pstride[a];
+            S.dposP[d] = int32_t(x);
+        }
     }
     for (int a = 0; a < NDIM; ++a) {
         // round-up reciprocal: with l = ceil(log2 D) and m = ceil(2^(31+l) / D),
@@ -245,23 +260,28 @@ __device__ __forceinline__ float nan_f() { return __int_as_float(0x7fffffff); }
 // kPlain: the field is one array holding the whole domain (one slab, no halo
 // planes); a vertex whose whole link box lies inside it loads without
 // clamping the dropped offsets.
-template <int NDIM, bool kPlain>
+template <int NDIM, bool kPlain, bool kPad = false>
 __device__ __forceinline__ void upper_link(const GridConst<NDIM> &S, const FieldView &F, int64_t v, float fv,
                                            typename Lattice<NDIM>::W &Up, typename Lattice<NDIM>::W &Un,
-                                           int64_t *best) {
+                                           int64_t *best, const float *pad = nullptr) {
     using L = Lattice<NDIM>;
     using W = typename L::W;
     constexpr int M = L::M;
     W vp = L::full() & ~L::bit(0), vn = vp;
     uint32_t r = uint32_t(v);
+    int32_t pidx = 0;          // kPad: v's cell in the padded copy
 #pragma unroll
     for (int a = 0; a < NDIM; ++a) {
         const uint32_t D = S.dims[a];
         const uint32_t q = S.sh[a] < 0 ? r : (__umulhi(r, S.mag[a]) >> S.sh[a]);
         const uint32_t c = r - q * D;
         r = q;
-        if (c == 0) vn &= L::without(a);
-        if (c + 1 == D) vp &= L::without(a);
+        if constexpr (kPad) {
+            pidx += int32_t(c + 1) * S.pstride[a];
+        } else {
+            if (c == 0) vn &= L::without(a);
+            if (c + 1 == D) vp &= L::without(a);
+        }
     }
     W up{}, un{};
     float bf = -INFINITY;
@@ -303,7 +323,30 @@ __device__ __forceinline__ void upper_link(const GridConst<NDIM> &S, const Field
             }
         }
     };
-    if constexpr (kPlain) {
+    if constexpr (kPad) {
+        // the NaN border of the padded copy stands in for the truncated link
+        // (reading L3): every offset loads, no per-offset domain test
+        const float *p = pad + pidx;
+        asm("" : "+l"(p));
+#pragma unroll
+        for (int e = M - 1; e >= 1; --e) {
+            const float fu = __ldg(p - S.dposP[e]);
+            if (fu > fv) un |= L::bit(e);
+            if (fu >= bf) {
+                bf = fu;
+                bk = -e;
+            }
+        }
+#pragma unroll
+        for (int d = 1; d < M; ++d) {
+            const float fu = __ldg(p + S.dposP[d]);
+            if (fu >= fv) up |= L::bit(d);
+            if (fu >= bf) {
+                bf = fu;
+                bk = d;
+            }
+        }
+    } else if constexpr (kPlain) {
         // an opaque base keeps each address one wide multiply-add off it
         const float *p = F.own + (v - F.v0);
         asm("" : "+l"(p));
@@ -369,10 +412,10 @@ __device__ __forceinline__ int components(const GridConst<NDIM> &S, typename Lat
     return beta;
 }
 
-template <int NDIM, bool kPlain>
+template <int NDIM, bool kPlain, bool kPad = false>
 __global__ void __launch_bounds__(256) k_classify_grid(const __grid_constant__ GridConst<NDIM> S, FieldView F, Slab s,
                                                        int32_t *ptr, uint32_t *sad_bits, uint32_t *max_bits,
-                                                       uint8_t *beta_out, int *nan_flag) {
+                                                       uint8_t *beta_out, int *nan_flag, const float *pad = nullptr) {
     const int64_t nown = s.v1 - s.v0;
     const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     const bool active = i < nown;
@@ -383,7 +426,7 @@ __global__ void __launch_bounds__(256) k_classify_grid(const __grid_constant__ G
         if (fv != fv) atomicOr(nan_flag, 1);
         int64_t best;
         typename Lattice<NDIM>::W up, un;
-        upper_link<NDIM, kPlain>(S, F, v, fv, up, un, &best);
+        upper_link<NDIM, kPlain, kPad>(S, F, v, fv, up, un, &best, pad);
         is_max = !bool(up | un);
         const int beta = is_max ? 0 : components<NDIM>(S, up, un, F, v, nullptr);
         is_sad = beta >= 2;
@@ -531,12 +574,51 @@ __global__ void __launch_bounds__(128) k_arc_paths_grid(const __grid_constant__ 
 
 static inline unsigned blocks_for(int64_t n, int bs) { return unsigned((n + bs - 1) / bs); }
 
+// the field into the interior of a copy padded by one NaN cell on every side
+// of every axis (the border was filled with NaN bytes first)
+template <int NDIM>
+__global__ void __launch_bounds__(256) k_pad_grid(const __grid_constant__ GridConst<NDIM> S, const float *__restrict__ f,
+                                                  int64_t n, float *pad) {
+    for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
+        uint32_t r = uint32_t(i);
+        int32_t pidx = 0;
+#pragma unroll
+        for (int a = 0; a < NDIM; ++a) {
+            const uint32_t q = S.sh[a] < 0 ? r : (__umulhi(r, S.mag[a]) >> S.sh[a]);
+            pidx += int32_t(r - q * S.dims[a] + 1) * S.pstride[a];
+            r = q;
+        }
+        pad[pidx] = __ldg(f + i);
+    }
+}
+
+int64_t padded_cells(const LinkTable &tab, int ndim) {
+    int64_t c = 1;
+    for (int a = 0; a < ndim; ++a) c *= tab.dims[a] + 2;
+    return c;
+}
+
 cudaError_t launch_classify_grid(const LinkTable &tab, int ndim, FieldView F, const Slab &s, int32_t *ptr,
                                  uint32_t *sad_bits, uint32_t *max_bits, uint8_t *beta_out, int *nan_flag,
-                                 cudaStream_t st) {
+                                 cudaStream_t st, float *pad) {
     const int64_t n = s.v1 - s.v0;
     if (n <= 0) return cudaSuccess;
     const bool plain = F.lo == nullptr && F.hi == nullptr;
+    if (pad && plain && s.v0 == 0) {
+        // one slab: classify on a NaN-padded copy (no per-offset domain tests)
+        cudaError_t e = cudaMemsetAsync(pad, 0xff, sizeof(float) * size_t(padded_cells(tab, ndim)), st);
+        if (e != cudaSuccess) return e;
+#define CALL(D)                                                                                           \
+    {                                                                                                     \
+        const GridConst<D> G = make_grid_const<D>(tab);                                                   \
+        k_pad_grid<D><<<unsigned(std::min<int64_t>(blocks_for(n, 256), 148 * 16)), 256, 0, st>>>(G, F.own, n, pad); \
+        k_classify_grid<D, true, true><<<blocks_for(n, 256), 256, 0, st>>>(G, F, s, ptr, sad_bits, max_bits,   \
+                                                                           beta_out, nan_flag, pad);      \
+    }
+        EG_DISPATCH_NDIM(ndim, CALL)
+#undef CALL
+        return cudaGetLastError();
+    }
 #define CALL(D)                                                                                           \
     if (plain)                                                                                            \
         k_classify_grid<D, true><<<blocks_for(n, 256), 256, 0, st>>>(             \
