@@ -199,6 +199,7 @@ struct GridConst {
     uint32_t mag[NDIM];       // r / dims[a] = umulhi(r, mag[a]) >> sh[a] for r < 2^31
     int32_t sh[NDIM];
     int32_t dposP[1 << NDIM]; // offset of +d in the NaN-padded copy (every axis + 2)
+    int32_t dnegP[1 << NDIM]; // -dposP (no negation per load)
     int32_t pstride[NDIM];    // strides of the padded copy
 };
 
@@ -223,6 +224,7 @@ static GridConst<NDIM> make_grid_const(const LinkTable &t) {
             for (int a = 0; a < NDIM; ++a)
                 if ((d >> a) & 1) x += S.pstride[a];
             S.dposP[d] = int32_t(x);
+            S.dnegP[d] = -int32_t(x);
         }
     }
     for (int a = 0; a < NDIM; ++a) {
@@ -328,23 +330,23 @@ __device__ __forceinline__ void upper_link(const GridConst<NDIM> &S, const Field
         // (reading L3): every offset loads, no per-offset domain test
         const float *p = pad + pidx;
         asm("" : "+l"(p));
+        // running maximum by integer selects (FSEL issues at half rate on sm_100)
+        auto keep = [&](float fu, int k) {
+            asm("{\n\t.reg .pred q;\n\tsetp.ge.f32 q, %2, %3;\n\tselp.b32 %0, %2, %3, q;\n\tselp.b32 %1, %4, %5, q;\n\t}"
+                : "=f"(bf), "=r"(bk)
+                : "f"(fu), "f"(bf), "r"(k), "r"(bk));
+        };
 #pragma unroll
         for (int e = M - 1; e >= 1; --e) {
-            const float fu = __ldg(p - S.dposP[e]);
+            const float fu = __ldg(p + S.dnegP[e]);
             if (fu > fv) un |= L::bit(e);
-            if (fu >= bf) {
-                bf = fu;
-                bk = -e;
-            }
+            keep(fu, -e);
         }
 #pragma unroll
         for (int d = 1; d < M; ++d) {
             const float fu = __ldg(p + S.dposP[d]);
             if (fu >= fv) up |= L::bit(d);
-            if (fu >= bf) {
-                bf = fu;
-                bk = d;
-            }
+            keep(fu, d);
         }
     } else if constexpr (kPlain) {
         // an opaque base keeps each address one wide multiply-add off it
