@@ -385,6 +385,7 @@ __device__ __forceinline__ int components(const GridConst<NDIM> &S, typename Lat
             if (np == cp && nn == cn) break;
             cp = np;
             cn = nn;
+            if (cp == P && cn == N) break;   // every unassigned upper vertex reached: nothing can grow
         }
         P &= ~cp;
         N &= ~cn;
