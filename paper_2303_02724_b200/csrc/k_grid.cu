@@ -377,8 +377,21 @@ __device__ __forceinline__ int components(const GridConst<NDIM> &S, typename Lat
     W P = Up, N = Un;  // not yet assigned to a component
     int beta = 0;
     while (bool(P | N)) {
-        W cp = bool(P) ? L::lowest(P) : W{};
-        W cn = bool(P) ? W{} : L::lowest(N);
+        // seed: the member with the most axes (the highest bit; +1 / -1 when
+        // present, adjacent to every other member of its sign), so the closure
+        // reaches the rest in fewer steps; the components do not depend on it
+        W cp, cn;
+        if constexpr (std::is_integral<W>::value) {
+            auto top = [](W x) -> W {
+                if constexpr (sizeof(W) == 4) return W(1) << (31 - __clz(x));
+                else return W(1) << (63 - __clzll((long long)x));
+            };
+            cp = bool(P) ? top(P) : W{};
+            cn = bool(P) ? W{} : top(N);
+        } else {
+            cp = bool(P) ? L::lowest(P) : W{};
+            cn = bool(P) ? W{} : L::lowest(N);
+        }
         for (;;) {
             const W np = Up & (L::up(cp) | L::down(cp | L::rev(cn)));
             const W nn = Un & (L::up(cn) | L::down(cn | L::rev(cp)));
