@@ -302,6 +302,10 @@ def run_ours(args):
                   "trimmed_mean": round(float(np.mean(trim)), 4),
                   "rule": "per-step CUDA events (this rank); trimmed_mean drops the min and max (P:319: "
                           "middle 5 of 7 at --steps 7)"}
+    if world > 1:
+        # the deferred graph copy is one-process only: one untimed collective
+        # compute with the graph copied, for the parity sample and the counts
+        ctx.compute(f, flags=flags, materialize=False, **kw)
     g = ctx.graph()
     clk = clocks.stop()
     t_max = torch.tensor([ms], device=dev)
