@@ -12,16 +12,21 @@
 //               so the argmax is 2x2 in-plane maxima combined across z;
 //           S3  the 14-bit upper mask -> a 2-bit class code (saddle: beta0+ >= 2, maximum: empty mask) from a 4 KB LUT
 //               (Table 1; maximum iff the mask is empty).
-//         The gradients are stored as 16-bit byte offsets into a pointer box and
-//         compressed in shared memory (S2 inside the tile): every vertex ends
-//         at an in-tile maximum (its final label) or at the first halo vertex
-//         on its path (an exit: the path leaves the tile, the paper's partial
-//         path P:296).  label[v] = global id of that root, with bit 31 set for
-//         exits; the distinct exit targets of the tile are appended to a list E.
-// Pass E  (k_resolve_exits): for every e in E, follow label[] (one dependent
-//         load per tile hop) to the maximum and store it in label[e].
-// Pass X  (launch_finalize, k_slab.cu): every exiting vertex takes
-//         label[label[v]] (its exit target is in E, hence final).
+//         The gradients are stored as 16-bit byte offsets into a pointer box
+//         (also kept in registers for the thread's own column) and compressed
+//         in shared memory (S2 inside the tile): every vertex ends at an
+//         in-tile maximum (its final label) or at the first halo vertex on its
+//         path (an exit: the path leaves the tile, the paper's partial path
+//         P:296).  label[v] = global id of that root, with bit 31 set for
+//         exits.  The box of the tile one resident-CTA count ahead is
+//         prefetched into L2; the pointer-box template, LUT and plane table
+//         arrive by bulk copies.
+// Default (one slab, no exit list): the label pass (k_finalize_faces,
+//         k_slab.cu) chases every exit -- first the z-face plane pairs of the
+//         tile layers, then the rest, whose z-face exits end one load later.
+// EG_ELIST=1: the distinct exit targets of every tile are appended to a list
+//         E; k_resolve_exits follows label[] from each to its maximum, and
+//         the label pass then needs one load per exiting vertex.
 // All in-place updates are race-benign: every value ever stored on a chain is
 // a later vertex of the same ascending path.
 #include <cuda.h>
