@@ -265,7 +265,7 @@ __device__ __forceinline__ float nan_f() { return __int_as_float(0x7fffffff); }
 template <int NDIM, bool kPlain, bool kPad = false>
 __device__ __forceinline__ void upper_link(const GridConst<NDIM> &S, const FieldView &F, int64_t v, float fv,
                                            typename Lattice<NDIM>::W &Up, typename Lattice<NDIM>::W &Un,
-                                           int64_t *best, const float *pad = nullptr) {
+                                           int64_t *best, const float *pad = nullptr, float *fv_out = nullptr) {
     using L = Lattice<NDIM>;
     using W = typename L::W;
     constexpr int M = L::M;
@@ -330,6 +330,9 @@ __device__ __forceinline__ void upper_link(const GridConst<NDIM> &S, const Field
         // (reading L3): every offset loads, no per-offset domain test
         const float *p = pad + pidx;
         asm("" : "+l"(p));
+        // f(v) from the padded copy too (its load issues with the neighbours')
+        fv = __ldg(p);
+        if (fv_out) *fv_out = fv;
         // running maximum by integer selects (FSEL issues at half rate on sm_100)
         auto keep = [&](float fu, int k) {
             asm("{\n\t.reg .pred q;\n\tsetp.ge.f32 q, %2, %3;\n\tselp.b32 %0, %2, %3, q;\n\tselp.b32 %1, %4, %5, q;\n\t}"
@@ -438,11 +441,11 @@ __global__ void __launch_bounds__(256) k_classify_grid(const __grid_constant__ G
     bool is_sad = false, is_max = false;
     if (active) {
         const int64_t v = s.v0 + i;
-        const float fv = F.at(v);
-        if (fv != fv) atomicOr(nan_flag, 1);
+        float fv = kPad ? 0.f : F.at(v);
         int64_t best;
         typename Lattice<NDIM>::W up, un;
-        upper_link<NDIM, kPlain, kPad>(S, F, v, fv, up, un, &best, pad);
+        upper_link<NDIM, kPlain, kPad>(S, F, v, fv, up, un, &best, pad, &fv);
+        if (fv != fv) atomicOr(nan_flag, 1);
         is_max = !bool(up | un);
         const int beta = is_max ? 0 : components<NDIM>(S, up, un, F, v, nullptr);
         is_sad = beta >= 2;
