@@ -389,7 +389,8 @@ __global__ void __launch_bounds__(32 * kCsrWarps) k_csr_link(
 // atomicOr.  Components, UpperLinkReps and the outputs are those of
 // k_csr_link.
 constexpr int kFlatMax = 64;
-constexpr int kFlatHash = 256;          // direct-mapped id -> position table (|U| <= 32)
+constexpr int kFlatHash = 512;          // direct-mapped id -> position table (|U| <= 32)
+constexpr int kFlatShift = 23;          // slot = (id * golden) >> kFlatShift
 struct __align__(16) CsrFlatSmem {
     int32_t hkey[kFlatHash];        // U(v) member with this slot, -1 = empty
     uint32_t adj32[32];
@@ -474,10 +475,11 @@ __global__ void __launch_bounds__(32 * kCsrWarps) k_csr_link_flat(
                 const int lA = mine ? cl : 0;
                 const int64_t sA = mine ? cs : 0;
                 const uint32_t kA = mine ? fkey(cf) : 0u;
-                const uint32_t slot = (uint32_t(uA) * 2654435761u) >> 24;
-                reinterpret_cast<int4 *>(sm.hkey)[lane] = make_int4(-1, -1, -1, -1);
-                reinterpret_cast<int4 *>(sm.hkey)[lane + 32] = make_int4(-1, -1, -1, -1);
-                const uint32_t same = __match_any_sync(0xffffffffu, mine ? slot : 0x100u + lane);
+                const uint32_t slot = (uint32_t(uA) * 2654435761u) >> kFlatShift;
+#pragma unroll
+                for (int k = 0; k < kFlatHash / 128; ++k)
+                    reinterpret_cast<int4 *>(sm.hkey)[lane + 32 * k] = make_int4(-1, -1, -1, -1);
+                const uint32_t same = __match_any_sync(0xffffffffu, mine ? slot : uint32_t(kFlatHash) + lane);
                 const bool clash = __any_sync(0xffffffffu, mine && __popc(same) > 1);
                 int iA = lA;
 #pragma unroll
@@ -527,7 +529,7 @@ __global__ void __launch_bounds__(32 * kCsrWarps) k_csr_link_flat(
                         int q;
                         bool hit;
                         if (!clash) {
-                            q = sm.hkey[(uint32_t(b) * 2654435761u) >> 24];
+                            q = sm.hkey[(uint32_t(b) * 2654435761u) >> kFlatShift];
                             hit = q >= 0 && sm.su[q] == b;
                         } else {
                             q = bsearch_le(sm.su, nu, b);
